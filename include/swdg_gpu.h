@@ -1,0 +1,187 @@
+/*
+ * swdg_gpu.h — C ABI of the B200 (sm_100a) ES-DGSEM shallow-water stage path.
+ *
+ * Drop-in boundary for the reference solver `swdg` (arXiv 1804.02221,
+ * /root/reference/proj/include/swdg).  The reference has no plugin registry;
+ * its seams are the free functions and the TimeIntegrator class below.  Each
+ * entry point names the reference interface it replaces:
+ *
+ *   swdg_gpu_create          TimeIntegrator ctor          timeloop.hpp:148-151
+ *                            (+ Mesh/Operators1D inputs   mesh.hpp:35-112, operators.hpp:35-52)
+ *   swdg_gpu_try_step        TimeIntegrator::try_step     timeloop.hpp:156-170
+ *                            ssprk3_step                  timeloop.hpp:88-108
+ *                            post_stage (reject+limiter)  timeloop.hpp:202-234
+ *   swdg_gpu_evaluate_rhs    TimeIntegrator::evaluate_rhs timeloop.hpp:173-190
+ *   swdg_gpu_assemble_rhs    assemble_rhs (inviscid)      dg_rhs.hpp:267-303
+ *   swdg_gpu_compute_dt      compute_dt                   timeloop.hpp:53-75
+ *   swdg_gpu_diagnostics     total_mass/total_entropy/min_height  field.hpp:39-68
+ *                            min_positivity_dt            limiter.hpp:135-166
+ *   swdg_gpu_last_eps        TimeIntegrator::last_eps     timeloop.hpp:192
+ *   swdg_gpu_set_forcing     TimeIntegrator::forcing      timeloop.hpp:198 (ForcingFn dg_rhs.hpp:255)
+ *
+ * Conventions
+ *   - Return codes: SWDG_OK; SWDG_ERR_INPUT mirrors SwdgError (core.hpp:63);
+ *     SWDG_ERR_ABORT mirrors NumericalAbort (timeloop.hpp:46); these match the
+ *     CLI exit codes 2/3 (tools/swdg_main.cpp:168-185).  SWDG_ERR_CUDA is a
+ *     device/runtime failure (no reference counterpart).
+ *   - All arrays are FP64, layouts exactly as in the reference: nodal arrays
+ *     element-major e*(N+1)^2 + i*(N+1) + j (core.hpp:39-42), face arrays
+ *     (e*4+face)*(N+1)+t (mesh.hpp:70-75), matrices row-major (operators.hpp:30-33).
+ *   - Every host pointer is borrowed for the duration of the call only; the
+ *     context deep-copies mesh data to the device and owns all device memory.
+ *   - A context is single-threaded (the reference is single-threaded).
+ *   - There is no CPU fallback: without a CUDA device every call that needs
+ *     one returns SWDG_ERR_CUDA.
+ */
+#ifndef SWDG_GPU_H
+#define SWDG_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SWDG_OK 0
+#define SWDG_ERR_CUDA 1
+#define SWDG_ERR_INPUT 2
+#define SWDG_ERR_ABORT 3
+
+/* Arithmetic modes.  EXACT replays the reference expression trees and
+ * accumulation orders without FMA contraction (bitwise parity with the
+ * reference built at its own flags, proj/CMakeLists.txt:6-8).  FAST is the
+ * fused throughput kernel (FMA, symmetric two-point flux evaluation),
+ * validated at 1e-12 normwise per stage. */
+#define SWDG_MODE_EXACT 0
+#define SWDG_MODE_FAST 1
+
+/* Face tags, BoundaryTag (mesh.hpp:30). */
+#define SWDG_TAG_INTERIOR 0
+#define SWDG_TAG_WALL 1
+
+/* FaceInfo (mesh.hpp:35-44) without the periodic offsets (watertightness
+ * diagnostics only, never read on the stage path). */
+typedef struct swdg_face {
+  int32_t elem_minus, face_minus, elem_plus, face_plus;
+  int32_t reversed; /* plus-side nodes run opposite (MeshTopology::partner_node mesh.hpp:51) */
+  int32_t tag;      /* SWDG_TAG_* */
+} swdg_face;
+
+/* Borrowed view of a reference Mesh (mesh.hpp:101-112): Operators1D
+ * matrices, MeshGeometry arrays and MeshTopology.faces.  The metric-
+ * premultiplied bathymetry products b_yeta... (mesh.hpp:67-68) are not
+ * passed: sample_bathymetry (mesh.hpp:223-232) defines them as metric*b and
+ * the device recomputes that product bitwise. */
+typedef struct swdg_mesh_view {
+  int32_t n_elem; /* K (elements stored, owned first) */
+  int32_t degree; /* N */
+  int32_t n_owned; /* elements [0,n_owned) are advanced; the rest are halo
+                      (ghost) elements filled by swdg_gpu_halo_*; 0 = all */
+  int32_t n_faces;
+  const swdg_face* faces;
+  /* Operators1D, n1 or n1*n1 entries */
+  const double* weights;         /* LGL weights w */
+  const double* deriv;           /* D */
+  const double* deriv_modified;  /* Dtilde = 2D + S */
+  const double* deriv_weak;      /* Dhat = -M^-1 D^T M */
+  const double* vandermonde_inv; /* V^-1 */
+  /* MeshGeometry nodal arrays, K*n1*n1 entries */
+  const double *x, *y;
+  const double *x_xi, *x_eta, *y_xi, *y_eta;
+  const double* jac;
+  const double* b;
+  /* MeshGeometry face arrays, K*4*n1 entries */
+  const double *face_jsurf, *face_nx, *face_ny, *face_a;
+} swdg_mesh_view;
+
+/* PhysicsParams (physics.hpp:11-16) + ViscosityConfig (viscosity.hpp:14-19)
+ * + the stage-relevant RunConfig fields (timeloop.hpp:23-44). */
+typedef struct swdg_params {
+  double g, h_tol, h_des, h_ref;
+  double epsilon0, sigma_min, sigma_max;
+  int32_t visc_enabled;
+  int32_t limiter_enabled;
+  int32_t mode; /* SWDG_MODE_* */
+  int32_t reserved;
+} swdg_params;
+
+/* Per-try_step report: TimeIntegrator::last_limited_count / last_max_eps /
+ * last_min_stage_h (timeloop.hpp:192-195). */
+typedef struct swdg_step_info {
+  double min_stage_h;
+  double max_eps;
+  int32_t n_limited;
+  int32_t accepted;
+} swdg_step_info;
+
+/* StepDiagnostics fields computed from a state (driver.hpp:115-127). */
+typedef struct swdg_diagnostics {
+  double mass;
+  double entropy;
+  double min_h;
+  double positivity_dt;
+} swdg_diagnostics;
+
+/* Host forcing callback standing in for ForcingFn (dg_rhs.hpp:255): fill
+ * (fh,fhu,fhv)[n] = forcing(x[n], y[n], t) for n < count. */
+typedef void (*swdg_forcing_fn)(void* user, double t, int64_t count, const double* x,
+                                const double* y, double* fh, double* fhu, double* fhv);
+
+typedef struct swdg_gpu swdg_gpu;
+
+/* Context lifetime (TimeIntegrator ctor, timeloop.hpp:148-151: viscosity
+ * needs degree >= 2).  `device` is the CUDA ordinal; *out is NULL on error
+ * and swdg_gpu_create_error() holds the message. */
+int swdg_gpu_create(const swdg_mesh_view* mesh, const swdg_params* params, int device,
+                    swdg_gpu** out);
+const char* swdg_gpu_create_error(void);
+void swdg_gpu_destroy(swdg_gpu* ctx);
+const char* swdg_gpu_last_error(const swdg_gpu* ctx);
+
+/* Run every launch of this context on `stream` (a cudaStream_t); NULL = the
+ * context's own stream. */
+int swdg_gpu_set_stream(swdg_gpu* ctx, void* stream);
+int swdg_gpu_synchronize(swdg_gpu* ctx);
+
+/* State transfer: State h/hu/hv (field.hpp:12-34), K*n1*n1 each, host memory
+ * (pinned memory gives full PCIe bandwidth). */
+int swdg_gpu_upload_state(swdg_gpu* ctx, const double* h, const double* hu, const double* hv);
+int swdg_gpu_download_state(swdg_gpu* ctx, double* h, double* hu, double* hv);
+/* Device pointers of the current state (for device-resident callers). */
+int swdg_gpu_device_state(swdg_gpu* ctx, double** h, double** hu, double** hv);
+
+/* dW/dt of the current state at time t, downloaded to host buffers. */
+int swdg_gpu_evaluate_rhs(swdg_gpu* ctx, double t, double* rh, double* rhu, double* rhv);
+int swdg_gpu_assemble_rhs(swdg_gpu* ctx, double t, double* rh, double* rhu, double* rhv);
+
+/* CFL time step of the current state (compute_dt): SWDG_ERR_INPUT unless
+ * 0 < cfl <= 1. */
+int swdg_gpu_compute_dt(swdg_gpu* ctx, double cfl, double* dt);
+
+/* One SSPRK3 step of the current device state.  info->accepted = 0 leaves
+ * the state untouched (reject signal, timeloop.hpp:205-209).  Returns
+ * SWDG_ERR_ABORT when the limiter is disabled and a stage goes negative
+ * (timeloop.hpp:211-218). */
+int swdg_gpu_try_step(swdg_gpu* ctx, double t, double dt, swdg_step_info* info);
+
+/* Device-resident throughput entry: `nsteps` SSPRK3 steps with fixed dt and
+ * no host synchronisation (reject flags accumulate on the device; read them
+ * with swdg_gpu_last_info). */
+int swdg_gpu_run_steps(swdg_gpu* ctx, int nsteps, double t, double dt);
+int swdg_gpu_last_info(swdg_gpu* ctx, swdg_step_info* info);
+
+int swdg_gpu_last_eps(swdg_gpu* ctx, double* eps);
+int swdg_gpu_diagnostics(swdg_gpu* ctx, swdg_diagnostics* out);
+
+/* Forcing: a host callback evaluated at the stage times t, t+dt, t+dt/2
+ * (ssprk3_stage_times timeloop.hpp:82) and uploaded, or NULL to clear. */
+int swdg_gpu_set_forcing(swdg_gpu* ctx, swdg_forcing_fn fn, void* user);
+
+/* Number of kernels this context has launched (instrumentation). */
+int64_t swdg_gpu_launch_count(const swdg_gpu* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SWDG_GPU_H */
