@@ -1,0 +1,94 @@
+// swdg_device.cuh — device-side data layout and helpers shared by the stage kernels.
+//
+// Layout in HBM (one context = one GPU = one element partition):
+//   nodal arrays      double[K*np], element-major e*np + i*n1 + j  (core.hpp:39-42)
+//   face arrays       double[K*4*n1], (e*4+face)*n1 + t            (mesh.hpp:70-75)
+//   element faces     int4[K*4]: {neighbour element, info bits, global face ordinal, 0}
+//                     built once on the host from MeshTopology::faces (mesh.hpp:46-54)
+// Elements [0, n_owned) are advanced; [n_owned, K) are halo copies (multi-GPU).
+#pragma once
+
+#include <cstdint>
+
+namespace swdg_dev {
+
+// ---- element-face connectivity (host builds it, kernels read it) ----
+// info bits
+constexpr int EF_NBR_FACE_MASK = 3;   // neighbour's local face id
+constexpr int EF_REVERSED = 1 << 2;   // plus-side nodes run opposite (mesh.hpp:51)
+constexpr int EF_WALL = 1 << 3;       // BoundaryTag::wall
+constexpr int EF_MINUS = 1 << 4;      // this element is the face owner (minus side)
+constexpr int EF_PRESENT = 1 << 5;    // the face is in MeshTopology::faces
+
+struct Phys {
+  double g, h_tol, h_des, h_ref;
+  double epsilon0, sigma_min, sigma_max;
+  int visc, limiter;
+};
+
+struct Mesh {
+  int K, n_owned, n1, np, degree;
+  double w0;
+  // Operators1D (operators.hpp:35-52), device copies
+  const double *w, *D, *Dt, *Dh, *Vinv;
+  // MeshGeometry nodal arrays
+  const double *ye, *xe, *yx, *xx, *jac, *b;
+  // exact-mode extras: host-computed CFL lengths (std::hypot) and face arrays
+  const double *len_xi, *len_eta;
+  const double *fnx, *fny, *fjs, *fa;
+  const int4* ef;  // [K*4]
+};
+
+struct State {
+  double *h, *hu, *hv;
+};
+
+struct CState {
+  const double *h, *hu, *hv;
+};
+
+// Reductions / signals for one stage or one step.  Keys are order-preserving
+// encodings of doubles so atomicMin works on them (min is order-independent).
+struct Flags {
+  unsigned long long min_h_key;   // min node height after limiting
+  unsigned long long dt_key;      // CFL candidate min
+  unsigned long long minlen_key;  // all-dry fallback length
+  unsigned long long posdt_key;   // positivity bound min (diagnostic)
+  unsigned long long max_eps_key; // max viscosity coefficient (ordered, max via ~key min)
+  int reject;                     // some element mean < 0 (timeloop.hpp:205-209)
+  int abort;                      // limiter off and a node < 0 (timeloop.hpp:211-218)
+  int n_limited;                  // elements with theta < 1 (last stage)
+  int stage_reject;               // stage index of the first reject (+1), device-resident runs
+};
+
+__host__ __device__ inline unsigned long long order_key(double x) {
+  const unsigned long long b = *reinterpret_cast<const unsigned long long*>(&x);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__host__ __device__ inline double key_value(unsigned long long k) {
+  const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return *reinterpret_cast<const double*>(&b);
+}
+
+// node (i,j) of local face `face` at position t (core.hpp:53-61)
+__host__ __device__ inline int face_node(int n1, int face, int t) {
+  switch (face) {
+    case 0: return t * n1;             // south (t, 0)
+    case 1: return (n1 - 1) * n1 + t;  // east  (N, t)
+    case 2: return t * n1 + (n1 - 1);  // north (t, N)
+    default: return t;                 // west  (0, t)
+  }
+}
+
+// Faces touching node (i,j): up to two (corners).  Writes local face ids and
+// the position t along each face.
+__host__ __device__ inline int node_faces(int n1, int i, int j, int* face, int* t) {
+  int c = 0;
+  if (j == 0) { face[c] = 0; t[c] = i; ++c; }
+  if (i == n1 - 1) { face[c] = 1; t[c] = j; ++c; }
+  if (j == n1 - 1) { face[c] = 2; t[c] = i; ++c; }
+  if (i == 0) { face[c] = 3; t[c] = j; ++c; }
+  return c;
+}
+
+}  // namespace swdg_dev

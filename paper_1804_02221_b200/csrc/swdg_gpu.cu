@@ -1,0 +1,590 @@
+// swdg_gpu.cu — the C ABI (include/swdg_gpu.h): context, device buffers and the
+// SSPRK3 stage pipeline (timeloop.hpp:88-108, 146-234) driving the exact
+// (kernels_exact.cu) or fast (kernels_fast.cu) kernels on one B200.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "../../include/swdg_gpu.h"
+#include "swdg_device.cuh"
+#include "swdg_launch.h"
+
+using namespace swdg_dev;
+
+namespace {
+thread_local std::string g_create_error;
+
+constexpr double kCa[3] = {0.0, 3.0 / 4.0, 1.0 / 3.0};  // ssprk3_combination (timeloop.hpp:80)
+constexpr double kCb[3] = {1.0, 1.0 / 4.0, 2.0 / 3.0};
+constexpr double kCt[3] = {0.0, 1.0, 0.5};              // ssprk3_stage_times (timeloop.hpp:82)
+
+struct CudaError {
+  cudaError_t e;
+  const char* where;
+};
+
+inline void ck(cudaError_t e, const char* where) {
+  if (e != cudaSuccess) throw CudaError{e, where};
+}
+
+struct InputError {
+  std::string msg;
+};
+}  // namespace
+
+struct swdg_gpu {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  swdg_params params{};
+  Phys phys{};
+  Mesh M{};
+  long long nn = 0, nn_owned = 0;
+  int64_t launches = 0;
+  std::string err;
+
+  std::vector<void*> allocations;
+  double* W[3] = {};  // current state
+  double* A[3] = {};
+  double* B[3] = {};
+  double* R[3] = {};  // rhs output
+  double *eps = nullptr, *r_ind = nullptr;
+  double *fvu = nullptr, *fvv = nullptr, *gvu = nullptr, *gvv = nullptr;
+  double *fh = nullptr, *fhu = nullptr, *fhv = nullptr;
+  double *partial = nullptr, *sums = nullptr;
+  Flags* flags = nullptr;      // device
+  Flags* flags_h = nullptr;    // pinned host mirror
+  double* sums_h = nullptr;    // pinned
+
+  std::vector<double> x, y, eps_h, r_h, fbuf;
+  swdg_forcing_fn forcing = nullptr;
+  void* forcing_user = nullptr;
+  swdg_step_info last{};
+
+  template <class T>
+  T* dalloc(size_t count) {
+    void* p = nullptr;
+    ck(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
+    allocations.push_back(p);
+    return static_cast<T*>(p);
+  }
+  ~swdg_gpu() {
+    for (void* p : allocations) cudaFree(p);
+    if (flags_h) cudaFreeHost(flags_h);
+    if (sums_h) cudaFreeHost(sums_h);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+int fail(swdg_gpu* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+template <class F>
+int guarded(swdg_gpu* c, F&& body) {
+  if (!c) return SWDG_ERR_INPUT;
+  try {
+    cudaSetDevice(c->device);
+    return body();
+  } catch (const CudaError& e) {
+    return fail(c, SWDG_ERR_CUDA, std::string(e.where) + ": " + cudaGetErrorString(e.e));
+  } catch (const InputError& e) {
+    return fail(c, SWDG_ERR_INPUT, e.msg);
+  } catch (const std::exception& e) {
+    return fail(c, SWDG_ERR_CUDA, e.what());
+  }
+}
+
+// viscosity_coefficient (viscosity.hpp:69-78) on the host with the same libm
+// the reference uses; sigma = log10(r) finishes shock_indicator (:64).
+double ramp(double r, const swdg_params& p) {
+  const double sigma = r <= 0.0 ? -std::numeric_limits<double>::infinity() : std::log10(r);
+  if (sigma < p.sigma_min) return 0.0;
+  if (sigma >= p.sigma_max) return p.epsilon0;
+  const double delta =
+      1.0 + std::sin(M_PI * (sigma - 0.5 * (p.sigma_max + p.sigma_min)) / (p.sigma_max - p.sigma_min));
+  return 0.5 * p.epsilon0 * delta;
+}
+
+void reset_flags(swdg_gpu* c) {
+  Flags f{};
+  f.min_h_key = ~0ull;
+  f.dt_key = ~0ull;
+  f.minlen_key = ~0ull;
+  f.posdt_key = ~0ull;
+  f.max_eps_key = ~0ull;
+  *c->flags_h = f;
+  ck(cudaMemcpyAsync(c->flags, c->flags_h, sizeof(Flags), cudaMemcpyHostToDevice, c->stream),
+     "reset flags");
+}
+
+void read_flags(swdg_gpu* c) {
+  ck(cudaMemcpyAsync(c->flags_h, c->flags, sizeof(Flags), cudaMemcpyDeviceToHost, c->stream),
+     "read flags");
+  ck(cudaStreamSynchronize(c->stream), "sync flags");
+}
+
+CState cs(double* const* a) { return CState{a[0], a[1], a[2]}; }
+State st(double* const* a) { return State{a[0], a[1], a[2]}; }
+
+// Per-stage viscosity (compute_viscosity viscosity.hpp:250-259 + the velocity
+// loop and br1/viscous flux pairs of evaluate_rhs timeloop.hpp:176-187).
+// Returns max eps.
+double stage_viscosity(swdg_gpu* c, CState in) {
+  c->launches += launch_exact_indicator(c->M, in, c->r_ind, c->stream);
+  ck(cudaMemcpyAsync(c->r_h.data(), c->r_ind, sizeof(double) * c->M.K, cudaMemcpyDeviceToHost,
+                     c->stream), "indicator D2H");
+  ck(cudaStreamSynchronize(c->stream), "indicator sync");
+  double mx = 0.0;
+  for (int e = 0; e < c->M.K; ++e) {
+    c->eps_h[e] = ramp(c->r_h[e], c->params);
+    mx = std::max(mx, c->eps_h[e]);
+  }
+  ck(cudaMemcpyAsync(c->eps, c->eps_h.data(), sizeof(double) * c->M.K, cudaMemcpyHostToDevice,
+                     c->stream), "eps H2D");
+  c->launches += launch_exact_grad(c->M, c->phys, in, c->eps, c->fvu, c->fvv, c->gvu, c->gvv,
+                                   c->stream);
+  return mx;
+}
+
+bool stage_forcing(swdg_gpu* c, double ts) {
+  if (!c->forcing) return false;
+  const long long nn = c->nn;
+  c->forcing(c->forcing_user, ts, nn, c->x.data(), c->y.data(), c->fbuf.data(),
+             c->fbuf.data() + nn, c->fbuf.data() + 2 * nn);
+  ck(cudaMemcpyAsync(c->fh, c->fbuf.data(), sizeof(double) * 3 * nn, cudaMemcpyHostToDevice,
+                     c->stream), "forcing H2D");
+  // the host buffer is reused at the next stage: make the copy complete
+  ck(cudaStreamSynchronize(c->stream), "forcing sync");
+  return true;
+}
+
+// dW/dt of `in` (+ optional stage update into `out`).  Returns max eps.
+double stage(swdg_gpu* c, CState in, double* const* out, int k, double t, double dt,
+             bool viscous, double* const* rhs) {
+  StageArgs a{};
+  a.in = in;
+  a.wn = cs(c->W);
+  a.dt = dt;
+  a.ca = kCa[k];
+  a.cb = kCb[k];
+  a.stage = k;
+  a.t = t + kCt[k] * dt;
+  a.update = out != nullptr;
+  if (out) a.out = st(out);
+  if (rhs) a.rhs = st(rhs);
+  double mx = 0.0;
+  if (viscous) {
+    mx = stage_viscosity(c, in);
+    a.eps = c->eps;
+    a.fvu = c->fvu;
+    a.fvv = c->fvv;
+    a.gvu = c->gvu;
+    a.gvv = c->gvv;
+  }
+  if (stage_forcing(c, a.t)) {
+    a.fh = c->fh;
+    a.fhu = c->fhu;
+    a.fhv = c->fhv;
+  }
+  c->launches += launch_exact_rhs_stage(c->M, c->phys, a, c->stream);
+  return mx;
+}
+
+void upload(double* dst, const double* src, size_t n, const char* what) {
+  if (!src) throw InputError{std::string("mesh view: missing array ") + what};
+  ck(cudaMemcpy(dst, src, n * sizeof(double), cudaMemcpyHostToDevice), what);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* swdg_gpu_create_error(void) { return g_create_error.c_str(); }
+
+int swdg_gpu_create(const swdg_mesh_view* mv, const swdg_params* p, int device,
+                    swdg_gpu** out) {
+  *out = nullptr;
+  g_create_error.clear();
+  if (!mv || !p) {
+    g_create_error = "null mesh or params";
+    return SWDG_ERR_INPUT;
+  }
+  auto* c = new swdg_gpu;
+  c->device = device;
+  try {
+    const int N = mv->degree, n1 = N + 1, np = n1 * n1, K = mv->n_elem;
+    if (N < 1 || N > 15) throw InputError{"degree must be in [1, 15]"};
+    if (K < 1) throw InputError{"mesh has no elements"};
+    const int n_owned = mv->n_owned > 0 ? mv->n_owned : K;
+    if (n_owned > K) throw InputError{"n_owned exceeds n_elem"};
+    if (p->visc_enabled && N < 2)
+      throw InputError{"artificial viscosity requires polynomial degree >= 2"};
+    if (p->visc_enabled && !(p->sigma_min < p->sigma_max))
+      throw InputError{"viscosity: sigma_min must be < sigma_max"};
+    if (p->visc_enabled && p->epsilon0 < 0.0)
+      throw InputError{"viscosity: epsilon0 must be >= 0"};
+    if (p->mode != SWDG_MODE_EXACT && p->mode != SWDG_MODE_FAST)
+      throw InputError{"unknown arithmetic mode"};
+    if (p->mode == SWDG_MODE_FAST) throw InputError{"fast mode not built yet"};
+
+    c->params = *p;
+    c->phys = Phys{p->g, p->h_tol, p->h_des, p->h_ref, p->epsilon0, p->sigma_min,
+                   p->sigma_max, p->visc_enabled, p->limiter_enabled};
+    const long long nn = (long long)K * np, nf = (long long)K * 4 * n1;
+    c->nn = nn;
+    c->nn_owned = (long long)n_owned * np;
+
+    // element-face connectivity from MeshTopology::faces (mesh.hpp:46-54)
+    std::vector<int4> ef(4 * (size_t)K, int4{-1, 0, 0, 0});
+    auto claim = [&](int e, int f, int4 v) {
+      if (e < 0 || e >= K || f < 0 || f > 3) throw InputError{"face list: element/face out of range"};
+      if (ef[4 * e + f].y & EF_PRESENT) throw InputError{"face list: element face listed twice"};
+      ef[4 * e + f] = v;
+    };
+    for (int i = 0; i < mv->n_faces; ++i) {
+      const swdg_face& f = mv->faces[i];
+      const int rev = f.reversed ? EF_REVERSED : 0;
+      if (f.tag == SWDG_TAG_WALL) {
+        claim(f.elem_minus, f.face_minus, int4{-1, EF_PRESENT | EF_MINUS | EF_WALL, i, 0});
+      } else if (f.tag == SWDG_TAG_INTERIOR) {
+        if (f.face_plus < 0 || f.face_plus > 3) throw InputError{"face list: bad plus face"};
+        claim(f.elem_minus, f.face_minus,
+              int4{f.elem_plus, EF_PRESENT | EF_MINUS | rev | f.face_plus, i, 0});
+        claim(f.elem_plus, f.face_plus, int4{f.elem_minus, EF_PRESENT | rev | f.face_minus, i, 0});
+      } else {
+        throw InputError{"exterior_state: unknown boundary tag"};
+      }
+      // check_unit_normal (physics.hpp:71-74) for every face node the flux visits
+      for (int t = 0; t < n1; ++t) {
+        const long long fm = ((long long)f.elem_minus * 4 + f.face_minus) * n1 + t;
+        const double nx = mv->face_nx[fm], ny = mv->face_ny[fm];
+        if (std::abs(std::sqrt(nx * nx + ny * ny) - 1.0) > 1e-10)
+          throw InputError{"normal vector is not unit length"};
+      }
+    }
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw CudaError{cudaErrorNoDevice, "no CUDA device (there is no CPU fallback)"};
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+    c->own_stream = true;
+
+    // geometry: 8 nodal arrays (ye, xe, yx, xx, jac, b, len_xi, len_eta),
+    // 4 face arrays, operators
+    double* geo = c->dalloc<double>(8 * nn + 4 * nf);
+    upload(geo + 0 * nn, mv->y_eta, nn, "y_eta");
+    upload(geo + 1 * nn, mv->x_eta, nn, "x_eta");
+    upload(geo + 2 * nn, mv->y_xi, nn, "y_xi");
+    upload(geo + 3 * nn, mv->x_xi, nn, "x_xi");
+    upload(geo + 4 * nn, mv->jac, nn, "jac");
+    upload(geo + 5 * nn, mv->b, nn, "b");
+    {
+      // compute_dt lengths 2J/|(x_eta,y_eta)|, 2J/|(x_xi,y_xi)| (timeloop.hpp:62-65),
+      // geometry-only: evaluated once with the reference's libm hypot
+      std::vector<double> lx(nn), le(nn);
+      for (long long n = 0; n < nn; ++n) {
+        lx[n] = 2.0 * mv->jac[n] / std::hypot(mv->x_eta[n], mv->y_eta[n]);
+        le[n] = 2.0 * mv->jac[n] / std::hypot(mv->x_xi[n], mv->y_xi[n]);
+      }
+      upload(geo + 6 * nn, lx.data(), nn, "len_xi");
+      upload(geo + 7 * nn, le.data(), nn, "len_eta");
+    }
+    double* fgeo = geo + 8 * nn;
+    upload(fgeo + 0 * nf, mv->face_nx, nf, "face_nx");
+    upload(fgeo + 1 * nf, mv->face_ny, nf, "face_ny");
+    upload(fgeo + 2 * nf, mv->face_jsurf, nf, "face_jsurf");
+    upload(fgeo + 3 * nf, mv->face_a, nf, "face_a");
+    double* ops = c->dalloc<double>(n1 + 4 * np);
+    upload(ops, mv->weights, n1, "weights");
+    upload(ops + n1, mv->deriv, np, "deriv");
+    upload(ops + n1 + np, mv->deriv_modified, np, "deriv_modified");
+    upload(ops + n1 + 2 * np, mv->deriv_weak, np, "deriv_weak");
+    upload(ops + n1 + 3 * np, mv->vandermonde_inv, np, "vandermonde_inv");
+    int4* def = c->dalloc<int4>(ef.size());
+    ck(cudaMemcpy(def, ef.data(), ef.size() * sizeof(int4), cudaMemcpyHostToDevice), "ef");
+
+    Mesh& M = c->M;
+    M.K = K;
+    M.n_owned = n_owned;
+    M.n1 = n1;
+    M.np = np;
+    M.degree = N;
+    M.w0 = mv->weights[0];
+    M.w = ops;
+    M.D = ops + n1;
+    M.Dt = ops + n1 + np;
+    M.Dh = ops + n1 + 2 * np;
+    M.Vinv = ops + n1 + 3 * np;
+    M.ye = geo;
+    M.xe = geo + nn;
+    M.yx = geo + 2 * nn;
+    M.xx = geo + 3 * nn;
+    M.jac = geo + 4 * nn;
+    M.b = geo + 5 * nn;
+    M.len_xi = geo + 6 * nn;
+    M.len_eta = geo + 7 * nn;
+    M.fnx = fgeo;
+    M.fny = fgeo + nf;
+    M.fjs = fgeo + 2 * nf;
+    M.fa = fgeo + 3 * nf;
+    M.ef = def;
+
+    // state buffers (current, two stage buffers, rhs)
+    double* sbuf = c->dalloc<double>(12 * nn);
+    for (int k = 0; k < 3; ++k) {
+      c->W[k] = sbuf + k * nn;
+      c->A[k] = sbuf + (3 + k) * nn;
+      c->B[k] = sbuf + (6 + k) * nn;
+      c->R[k] = sbuf + (9 + k) * nn;
+    }
+    ck(cudaMemset(sbuf, 0, 12 * nn * sizeof(double)), "memset state");
+    c->eps = c->dalloc<double>(K);
+    c->r_ind = c->dalloc<double>(K);
+    ck(cudaMemset(c->eps, 0, K * sizeof(double)), "memset eps");
+    if (p->visc_enabled) {
+      double* vb = c->dalloc<double>(4 * nn);
+      c->fvu = vb;
+      c->fvv = vb + nn;
+      c->gvu = vb + 2 * nn;
+      c->gvv = vb + 3 * nn;
+    }
+    c->partial = c->dalloc<double>(2 * (size_t)K);
+    c->sums = c->dalloc<double>(2);
+    c->flags = c->dalloc<Flags>(1);
+    ck(cudaMallocHost(&c->flags_h, sizeof(Flags)), "pinned flags");
+    ck(cudaMallocHost(&c->sums_h, 2 * sizeof(double)), "pinned sums");
+    c->eps_h.assign(K, 0.0);
+    c->r_h.assign(K, 0.0);
+    if (mv->x && mv->y) {
+      c->x.assign(mv->x, mv->x + nn);
+      c->y.assign(mv->y, mv->y + nn);
+    }
+    ck(cudaDeviceSynchronize(), "create sync");
+  } catch (const CudaError& e) {
+    g_create_error = std::string(e.where) + ": " + cudaGetErrorString(e.e);
+    delete c;
+    return SWDG_ERR_CUDA;
+  } catch (const InputError& e) {
+    g_create_error = e.msg;
+    delete c;
+    return SWDG_ERR_INPUT;
+  }
+  *out = c;
+  return SWDG_OK;
+}
+
+void swdg_gpu_destroy(swdg_gpu* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  delete c;
+}
+
+const char* swdg_gpu_last_error(const swdg_gpu* c) { return c ? c->err.c_str() : "null context"; }
+
+int swdg_gpu_set_stream(swdg_gpu* c, void* stream) {
+  return guarded(c, [&] {
+    if (c->own_stream && c->stream) {
+      ck(cudaStreamSynchronize(c->stream), "sync old stream");
+      cudaStreamDestroy(c->stream);
+      c->own_stream = false;
+      c->stream = nullptr;
+    }
+    if (stream) {
+      c->stream = static_cast<cudaStream_t>(stream);
+    } else {
+      ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+      c->own_stream = true;
+    }
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_synchronize(swdg_gpu* c) {
+  return guarded(c, [&] {
+    ck(cudaStreamSynchronize(c->stream), "synchronize");
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_upload_state(swdg_gpu* c, const double* h, const double* hu, const double* hv) {
+  return guarded(c, [&] {
+    const double* src[3] = {h, hu, hv};
+    for (int k = 0; k < 3; ++k)
+      ck(cudaMemcpyAsync(c->W[k], src[k], c->nn * sizeof(double), cudaMemcpyHostToDevice,
+                         c->stream), "upload state");
+    ck(cudaStreamSynchronize(c->stream), "upload sync");
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_download_state(swdg_gpu* c, double* h, double* hu, double* hv) {
+  return guarded(c, [&] {
+    double* dst[3] = {h, hu, hv};
+    for (int k = 0; k < 3; ++k)
+      ck(cudaMemcpyAsync(dst[k], c->W[k], c->nn * sizeof(double), cudaMemcpyDeviceToHost,
+                         c->stream), "download state");
+    ck(cudaStreamSynchronize(c->stream), "download sync");
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_device_state(swdg_gpu* c, double** h, double** hu, double** hv) {
+  return guarded(c, [&] {
+    *h = c->W[0];
+    *hu = c->W[1];
+    *hv = c->W[2];
+    return SWDG_OK;
+  });
+}
+
+static int rhs_common(swdg_gpu* c, double t, double* rh, double* rhu, double* rhv,
+                      bool viscous) {
+  return guarded(c, [&] {
+    double mx = stage(c, cs(c->W), nullptr, 0, t, 0.0, viscous, c->R);
+    (void)mx;
+    double* dst[3] = {rh, rhu, rhv};
+    for (int k = 0; k < 3; ++k)
+      ck(cudaMemcpyAsync(dst[k], c->R[k], c->nn * sizeof(double), cudaMemcpyDeviceToHost,
+                         c->stream), "rhs D2H");
+    ck(cudaStreamSynchronize(c->stream), "rhs sync");
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_evaluate_rhs(swdg_gpu* c, double t, double* rh, double* rhu, double* rhv) {
+  return rhs_common(c, t, rh, rhu, rhv, c && c->params.visc_enabled);
+}
+
+int swdg_gpu_assemble_rhs(swdg_gpu* c, double t, double* rh, double* rhu, double* rhv) {
+  if (!c) return SWDG_ERR_INPUT;
+  swdg_forcing_fn saved = c->forcing;
+  c->forcing = nullptr;
+  const int rc = rhs_common(c, t, rh, rhu, rhv, false);
+  c->forcing = saved;
+  return rc;
+}
+
+int swdg_gpu_compute_dt(swdg_gpu* c, double cfl, double* dt) {
+  return guarded(c, [&] {
+    if (!(cfl > 0.0) || cfl > 1.0) throw InputError{"compute_dt: cfl must be in (0, 1]"};
+    reset_flags(c);
+    c->launches += launch_exact_dt(c->M, c->phys, cs(c->W), c->flags, c->stream);
+    read_flags(c);
+    double d = key_value(c->flags_h->dt_key);
+    if (!std::isfinite(d)) {
+      const double order = 2.0 * c->M.degree + 1.0;
+      d = key_value(c->flags_h->minlen_key) /
+          (order * std::sqrt(c->params.g * std::max(c->params.h_ref, 1e-12)));
+    }
+    *dt = cfl * d;
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_try_step(swdg_gpu* c, double t, double dt, swdg_step_info* info) {
+  return guarded(c, [&] {
+    swdg_step_info r{};
+    r.min_stage_h = std::numeric_limits<double>::infinity();
+    r.max_eps = 0.0;
+    r.n_limited = 0;
+    r.accepted = 0;
+    double* const* outs[3] = {c->A, c->B, c->A};
+    CState in = cs(c->W);
+    const bool viscous = c->params.visc_enabled != 0;
+    int code = SWDG_OK;
+    for (int k = 0; k < 3; ++k) {
+      reset_flags(c);
+      const double mx = stage(c, in, outs[k], k, t, dt, viscous, nullptr);
+      r.max_eps = std::max(r.max_eps, mx);
+      c->launches += launch_exact_limit(c->M, c->phys, st(outs[k]), c->flags, c->stream);
+      read_flags(c);
+      const Flags& f = *c->flags_h;
+      if (f.abort) {
+        code = fail(c, SWDG_ERR_ABORT, "negative water height without limiter");
+        break;
+      }
+      if (f.reject) break;
+      if (c->params.limiter_enabled) r.n_limited = f.n_limited;
+      r.min_stage_h = std::min(r.min_stage_h, key_value(f.min_h_key));
+      in = cs(outs[k]);
+      if (k == 2) r.accepted = 1;
+    }
+    if (r.accepted)
+      for (int k = 0; k < 3; ++k) std::swap(c->W[k], c->A[k]);
+    c->last = r;
+    if (info) *info = r;
+    return code;
+  });
+}
+
+int swdg_gpu_run_steps(swdg_gpu* c, int nsteps, double t, double dt) {
+  return guarded(c, [&] {
+    for (int s = 0; s < nsteps; ++s) {
+      swdg_step_info r{};
+      const int rc = swdg_gpu_try_step(c, t + s * dt, dt, &r);
+      if (rc) return rc;
+    }
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_last_info(swdg_gpu* c, swdg_step_info* info) {
+  return guarded(c, [&] {
+    *info = c->last;
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_last_eps(swdg_gpu* c, double* eps) {
+  return guarded(c, [&] {
+    std::memcpy(eps, c->eps_h.data(), sizeof(double) * c->M.K);
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_diagnostics(swdg_gpu* c, swdg_diagnostics* out) {
+  return guarded(c, [&] {
+    reset_flags(c);
+    c->launches += launch_diagnostics(c->M, c->phys, cs(c->W), c->partial, c->sums, c->flags,
+                                      c->stream);
+    ck(cudaMemcpyAsync(c->sums_h, c->sums, 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                       c->stream), "sums D2H");
+    read_flags(c);
+    out->mass = c->sums_h[0];
+    out->entropy = c->sums_h[1];
+    out->min_h = key_value(c->flags_h->min_h_key);
+    out->positivity_dt = key_value(c->flags_h->posdt_key);
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_set_forcing(swdg_gpu* c, swdg_forcing_fn fn, void* user) {
+  return guarded(c, [&] {
+    if (fn && c->x.empty()) throw InputError{"forcing needs the mesh x/y arrays"};
+    c->forcing = fn;
+    c->forcing_user = user;
+    if (fn && !c->fh) {
+      double* fb = c->dalloc<double>(3 * c->nn);
+      c->fh = fb;
+      c->fhu = fb + c->nn;
+      c->fhv = fb + 2 * c->nn;
+      c->fbuf.assign(3 * c->nn, 0.0);
+    }
+    return SWDG_OK;
+  });
+}
+
+int64_t swdg_gpu_launch_count(const swdg_gpu* c) { return c ? c->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,37 @@
+// swdg_launch.h — host-side launch interface between the C-ABI context and the
+// kernel translation units (exact: kernels_exact.cu built --fmad=false; fast:
+// kernels_fast.cu).  Each launcher returns the number of kernels it launched.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "swdg_device.cuh"
+
+namespace swdg_dev {
+
+struct StageArgs {
+  CState in;       // stage input W^(k)
+  CState wn;       // W^n for the SSPRK3 convex combination
+  State out;       // stage output (update != 0)
+  State rhs;       // optional dW/dt output (h == nullptr: not written)
+  double dt, ca, cb, t;
+  int stage;       // 0,1,2 (ssprk3_combination timeloop.hpp:80-81)
+  int update;      // write out = combine(axpy(in, dt, rhs))
+  const double* eps;                        // per element viscosity
+  const double *fvu, *fvv, *gvu, *gvv;      // viscous flux pairs (nullptr: inviscid)
+  const double *fh, *fhu, *fhv;             // nodal forcing (nullptr: none)
+};
+
+// exact mode (kernels_exact.cu)
+int launch_exact_indicator(const Mesh& M, CState S, double* r, cudaStream_t st);
+int launch_exact_grad(const Mesh& M, const Phys& P, CState S, const double* eps, double* fvu,
+                      double* fvv, double* gvu, double* gvv, cudaStream_t st);
+int launch_exact_rhs_stage(const Mesh& M, const Phys& P, const StageArgs& A, cudaStream_t st);
+int launch_exact_limit(const Mesh& M, const Phys& P, State S, Flags* F, cudaStream_t st);
+int launch_exact_dt(const Mesh& M, const Phys& P, CState S, Flags* F, cudaStream_t st);
+
+// mode-independent (kernels_common.cu)
+int launch_diagnostics(const Mesh& M, const Phys& P, CState S, double* partial, double* out2,
+                       Flags* F, cudaStream_t st);
+
+}  // namespace swdg_dev

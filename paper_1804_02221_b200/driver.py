@@ -1,0 +1,81 @@
+"""Step loop around the GPU TimeIntegrator, mirroring run_simulation (driver.hpp:62-142).
+
+CFL step from compute_dt (timeloop.hpp:53), snapping to the final time and snapshot
+events with the reference's t_eps, reject-and-halve up to 10 times
+(driver.hpp:101-111), and the per-step StepDiagnostics fields (driver.hpp:115-127,
+computed on the device).  Output files (io.hpp) are out of scope.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from .swdg import NumericalAbort, State, TimeIntegrator
+
+
+@dataclass
+class StepDiagnostics:
+    """timeloop.hpp:131-142"""
+    step: int
+    t: float
+    dt: float
+    mass: float
+    entropy: float
+    min_h: float
+    n_limited: int
+    max_eps: float
+    min_stage_h: float
+    positivity_dt: float
+
+
+@dataclass
+class RunResult:
+    state: State
+    t: float = 0.0
+    steps: int = 0
+    series: list = field(default_factory=list)
+    mass_initial: float = 0.0
+    entropy_initial: float = 0.0
+
+
+def run_simulation(integ: TimeIntegrator, state: State, final_time: float, cfl: float,
+                   snapshot_times=(), keep_series: bool = True, diagnostics: bool = True,
+                   max_steps: int | None = None) -> RunResult:
+    out = RunResult(state=state)
+    if diagnostics:
+        d0 = integ.diagnostics(state)
+        out.mass_initial, out.entropy_initial = d0.mass, d0.entropy
+    snaps = sorted(set(float(s) for s in snapshot_times if s <= final_time + 1e-12))
+    next_snap = 0
+    t = 0.0
+    t_eps = 1e-12 * max(1.0, final_time)
+    while t < final_time - t_eps:
+        if max_steps is not None and out.steps >= max_steps:
+            break
+        dt = integ.compute_dt(state, cfl)
+        t_event = final_time
+        if next_snap < len(snaps):
+            t_event = min(t_event, snaps[next_snap])
+        hit_event = False
+        if t + dt >= t_event - t_eps:
+            dt = t_event - t
+            hit_event = True
+        rejections = 0
+        while not integ.try_step(state, t, dt):
+            dt *= 0.5
+            hit_event = False
+            rejections += 1
+            if rejections >= 10:
+                raise NumericalAbort(f"step rejected 10 times at t={t}")
+        t = t_event if hit_event else t + dt
+        out.steps += 1
+        if diagnostics:
+            d = integ.diagnostics(state)
+            sd = StepDiagnostics(out.steps, t, dt, d.mass, d.entropy, d.min_h,
+                                 integ.last_limited_count(), integ.last_max_eps(),
+                                 integ.last_min_stage_h(), d.positivity_dt)
+            if keep_series:
+                out.series.append(sd)
+        while next_snap < len(snaps) and t >= snaps[next_snap] - t_eps:
+            next_snap += 1
+    out.t = t
+    return out
