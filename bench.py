@@ -1,0 +1,330 @@
+#!/usr/bin/env python3
+"""Throughput benchmark: FP64 DOF-updates/s per SSPRK3 stage on the synthetic
+curvilinear mesh of BASELINE.json config 5.
+
+Workload (per GPU, weak scaling): build_wavy_mesh(N, 1000, 1000) periodic on [0,1]^2,
+amp 0.04, bathymetry b = 0.1 + 0.05 sin(2 pi x) sin(2 pi y), smooth state
+h = 1 + 0.1 sin(2 pi x) cos(2 pi y), hu = 0.3 h, hv = -0.2 h, g = 9.81, fixed
+dt = 0.1 * compute_dt (no rejections; checked).  A bench "step" is one SSPRK3 time
+step = 3 RK stages; value = 3 * DOFs * steps / time, DOFs = 3 K (N+1)^2
+(bench.hpp:259).  Inputs (>= 5 GB of geometry+state) exceed the 126 MB L2, so no
+flush is needed between iterations.
+
+  python bench.py [--gpus N --steps K --warmup W] [--degree N] [--sweep]
+  python bench.py --impl reference ...   # the reference CPU solver, same config
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FP64 DOF-updates/sec per RK stage"
+UNIT = "DOF-updates/s"
+KX = 1000
+
+
+def frozen_counts(N: int, viscous: bool):
+    """SURVEY §8(d) algorithmic bytes/flops per node and stage (frozen contract)."""
+    n1 = N + 1
+    bytes_node = 112.0 + (128.0 if viscous else 0.0)  # stage average (96, 120, 120)
+    flops_elem = 51 * N * n1 * n1 + (12 * n1 + 35) * n1 * n1 + 276 * n1
+    if viscous:
+        flops_elem += (28 * n1 + 20) * n1 * n1
+    return bytes_node, flops_elem / (n1 * n1)
+
+
+def peaks():
+    p = {"hbm_gbs": 6541.8, "fp64_tflops": 36.8, "hbm_src": "fallback", "fp64_src": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p["hbm_gbs"] = float(m["hbm_gbs"])
+        p["hbm_src"] = "MEASURED_PEAKS.json"
+    except Exception:
+        pass
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_fp64_peak.json")) as f:
+            p["fp64_tflops"] = float(json.load(f)["dfma_tflops"])
+            p["fp64_src"] = "profiles/r01_fp64_peak.json (DFMA microbenchmark on this pool)"
+    except Exception:
+        pass
+    return p
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(s[0]) for s in self.samples)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if len(s) > 2 + k and s[2 + k].lower().startswith("active")})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(self.samples[0][1]),
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def spec_for(N: int, kx: int = KX):
+    from paper_1804_02221_b200 import swdg
+    return swdg.structured_spec("wavy", N, kx, kx, periodic_x=True, periodic_y=True,
+                                extra=0.04, bathy="smooth")
+
+
+def run_config(N: int, viscous: bool):
+    from paper_1804_02221_b200 import swdg
+    visc = swdg.ViscosityConfig(False)
+    if viscous:
+        smin, smax = swdg.default_sigma_band(N)
+        visc = swdg.ViscosityConfig(True, 0.1, smin, smax)
+    return swdg.RunConfig(phys=swdg.PhysicsParams(9.81, 1e-4, 1e-8, 1.0), visc=visc,
+                          mode=swdg.MODE_FAST)
+
+
+def smooth_state(x, y):
+    import numpy as np
+    h = 1.0 + 0.1 * np.sin(2 * np.pi * x) * np.cos(2 * np.pi * y)
+    return h, 0.3 * h, -0.2 * h
+
+
+def measure_gpu(N: int, steps: int, warmup: int, viscous: bool, rank: int, world: int,
+                e2e_steps: int = 3):
+    import numpy as np
+    import torch
+    from paper_1804_02221_b200 import swdg
+
+    spec = spec_for(N)
+    cfg = run_config(N, viscous)
+    integ = swdg.TimeIntegrator.structured(spec, cfg, device=torch.cuda.current_device())
+    stream = torch.cuda.current_stream()
+    integ.set_stream(stream.cuda_stream)
+    nn = integ.mesh.n_nodes
+    dofs = 3 * nn
+    # initial state built on the host from the device-generated coordinates, pinned
+    x, y = integ.geometry("x"), integ.geometry("y")
+    host = [torch.empty(nn, dtype=torch.float64).pin_memory() for _ in range(3)]
+    for hbuf, val in zip(host, smooth_state(x, y)):
+        hbuf.numpy()[:] = val
+    del x, y
+    st = swdg.State(*(hb.numpy() for hb in host))
+    integ.upload(st)
+    dt = 0.1 * integ.compute_dt_device(0.5)
+
+    # warm-up, then K timed device-resident steps
+    integ.run_steps(warmup, 0.0, dt)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    l0 = integ.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        ev0.record(stream)
+        integ.run_steps(steps, warmup * dt, dt)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = integ.launch_count() - l0
+    ms = ev0.elapsed_time(ev1)
+    info = integ.last_info()
+    if not info.accepted:
+        raise RuntimeError("a stage was rejected during the timed run (invalid measurement)")
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # e2e through the C ABI with host buffers: H2D state, one SSPRK3 step, D2H state
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for s in range(e2e_steps):
+        integ.try_step(st, s * dt, dt)
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / max(e2e_steps, 1)
+    res = dict(ms=ms, dofs=dofs, nn=nn, launches=launches, clocks=clk.summary(),
+               e2e_s=e2e_s, h2d=3 * nn * 8, d2h=3 * nn * 8)
+    integ.close()
+    return res
+
+
+def cpu_reference(N: int, viscous: bool, budget_s: float = 15.0, kx: int = 64, steps=None):
+    """The reference's own try_step (oracle/_ref, single-threaded like the reference) on
+    a bounded sample of the C5 workload: the same mesh family, state and params on a
+    kx*kx element patch.  Returns DOF-updates/s per stage."""
+    import numpy as np
+    from oracle import ref
+    m = ref.build_mesh("wavy", N, kx, kx, periodic_x=True, periodic_y=True,
+                       extra=0.04).bathymetry("smooth")
+    smin = -(4.0 + 4.25 * np.log10(max(N, 1))) - 1.0
+    p = ref.params(g=9.81, visc=viscous, epsilon0=0.1, sigma_min=smin, sigma_max=smin + 2.0)
+    st = list(smooth_state(m.arrays["x"], m.arrays["y"]))
+    dt = 0.1 * ref.compute_dt(m, p, st, 0.5)
+    integ = ref.Integrator(m, p)
+    L = ref.lib()
+    runner = L.ref_runner_create(integ.h, *(ref.ptr(a) for a in st))
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        acc = L.ref_runner_steps(runner, 1, n * dt, dt)
+        assert acc == 1, "reference rejected a step"
+        n += 1
+        el = time.perf_counter() - t0
+        if (steps is not None and n >= steps) or (steps is None and el >= budget_s):
+            break
+    L.ref_runner_free(runner)
+    dofs = 3 * m.n_nodes
+    return dict(value=3 * dofs * n / el, seconds=el, steps=n, kx=kx, dofs=dofs)
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--degree", type=int, default=7)
+    ap.add_argument("--viscous", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="also time N=1..7")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    N = args.degree
+    workload = f"C5 synthetic wavy curvilinear mesh {KX}x{KX} (1M elements) per GPU, N={N}, " \
+               f"{'viscous' if args.viscous else 'inviscid'} ES-DGSEM SSPRK3 stage"
+    config = {"workload": workload, "elements_per_gpu": KX * KX, "degree": N,
+              "viscosity": bool(args.viscous), "state": "smooth", "dt": "0.1*CFL fixed",
+              "l2": "inputs > L2 (no flush needed)", "mode": "fast"}
+
+    if args.impl == "reference":
+        if world > 1 and rank != 0:
+            return
+        steps = max(1, args.steps // 10)
+        r = cpu_reference(N, args.viscous, steps=steps + args.warmup)
+        line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
+                "n_gpus": args.gpus, "steps": r["steps"], "warmup": 0,
+                "ms_per_step": 1e3 * r["seconds"] / r["steps"], "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": config,
+                "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": 1,
+                                 "kind": "reference",
+                                 "sample": f"reference TimeIntegrator::try_step on a "
+                                           f"{r['kx']}x{r['kx']} patch of the same mesh family, "
+                                           f"{r['steps']} steps, {r['seconds']:.1f} s, {cpu_model()}"},
+                "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    if world > 1:
+        torch.distributed.init_process_group("nccl")
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    r = measure_gpu(N, args.steps, args.warmup, args.viscous, rank, world)
+    stage_s = r["ms"] * 1e-3 / (3 * args.steps)
+    value = world * r["dofs"] / stage_s
+    bytes_node, flops_node = frozen_counts(N, args.viscous)
+    pk = peaks()
+    achieved_gbs = bytes_node * r["nn"] / stage_s / 1e9
+    achieved_tf = flops_node * r["nn"] / stage_s / 1e12
+    roof_dofs = min(pk["hbm_gbs"] * 1e9 / (bytes_node / 3.0),
+                    pk["fp64_tflops"] * 1e12 / (flops_node / 3.0))
+    bound = "hbm" if pk["hbm_gbs"] * 1e9 / (bytes_node / 3.0) <= \
+        pk["fp64_tflops"] * 1e12 / (flops_node / 3.0) else "fp64"
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": r["ms"] / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config,
+        "roofline": {
+            "bound": bound,
+            "achieved": achieved_gbs if bound == "hbm" else achieved_tf,
+            "peak": pk["hbm_gbs"] if bound == "hbm" else pk["fp64_tflops"],
+            "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
+            "frac": (achieved_gbs / pk["hbm_gbs"]) if bound == "hbm"
+            else achieved_tf / pk["fp64_tflops"],
+            "traffic": None,
+            "kernel": "k_stage_lines (fused stage)",
+            "algorithmic_bytes_per_node": bytes_node, "algorithmic_flops_per_node": flops_node,
+            "achieved_fp64_tflops": achieved_tf, "achieved_gbs": achieved_gbs,
+            "roof_dof_per_s": roof_dofs, "frac_of_roof": value / world / roof_dofs,
+            "peak_sources": {"hbm": pk["hbm_src"], "fp64": pk["fp64_src"]},
+        },
+        "clocks": r["clocks"],
+        "gpu_launches": r["launches"],
+        "e2e": {"value": world * 3 * r["dofs"] / r["e2e_s"], "unit": UNIT,
+                "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"],
+                "path": "TimeIntegrator.try_step via swdg_gpu_upload/try_step/download (pinned)"},
+    }
+    if rank == 0:
+        cb = cpu_reference(N, args.viscous, budget_s=args.cpu_budget)
+        out["cpu_baseline"] = {
+            "value": cb["value"], "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"oracle/_ref TimeIntegrator::try_step, {cb['kx']}x{cb['kx']} patch of the "
+                      f"same mesh family, {cb['steps']} steps in {cb['seconds']:.1f} s, "
+                      f"{cpu_model()}"}
+        if args.sweep:
+            sweep = {}
+            for n in range(1, 8):
+                if n == N:
+                    sweep[n] = value / world
+                    continue
+                rr = measure_gpu(n, max(5, args.steps // 2), 3, args.viscous, rank, 1, e2e_steps=0)
+                sweep[n] = rr["dofs"] / (rr["ms"] * 1e-3 / (3 * max(5, args.steps // 2)))
+            out["sweep_dof_per_s_by_degree"] = sweep
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

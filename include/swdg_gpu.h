@@ -180,6 +180,44 @@ int swdg_gpu_set_forcing(swdg_gpu* ctx, swdg_forcing_fn fn, void* user);
 /* Number of kernels this context has launched (instrumentation). */
 int64_t swdg_gpu_launch_count(const swdg_gpu* ctx);
 
+/* ---- standalone inputs (no reference headers needed) -------------------- */
+
+/* make_operators (operators.hpp:148-188): LGL nodes/weights, D, Dtilde, Dhat,
+ * V, V^-1 for degree N (bitwise the reference's). */
+int swdg_operators(int degree, double* nodes, double* weights, double* deriv,
+                   double* deriv_modified, double* deriv_weak, double* vandermonde,
+                   double* vandermonde_inv);
+
+/* structured_topology (mesh.hpp:237-290): face list of a kx*ky grid. */
+int64_t swdg_structured_face_count(int kx, int ky, int periodic_x, int periodic_y);
+int swdg_structured_faces(int kx, int ky, int periodic_x, int periodic_y, swdg_face* out);
+
+#define SWDG_MESH_CARTESIAN 0  /* build_cartesian_mesh  mesh.hpp:342 */
+#define SWDG_MESH_CURVED_DAM 1 /* build_curved_dam_mesh mesh.hpp:352 */
+#define SWDG_MESH_WAVY 2       /* build_wavy_mesh       mesh.hpp:370 */
+
+/* Generator spec of the reference's structured meshes plus a bathymetry:
+ * bathy_kind 0 none, 1 constant p0, 2 linear p0 x + p1 y + p2, 3 paraboloid
+ * p0 (x^2+y^2), 4 0.1 + 0.05 sin(2 pi x) sin(2 pi y) (validate.hpp:103),
+ * 5 step x < p0 ? p1 : p2, 6 p0 + p1 sin(p2 x) sin(p2 y). */
+typedef struct swdg_structured_spec {
+  int32_t kind, degree, kx, ky;
+  int32_t periodic_x, periodic_y;
+  int32_t bathy_kind, reserved;
+  double x0, x1, y0, y1;
+  double extra; /* dam_fraction (curved dam) or amplitude (wavy) */
+  double bathy[4];
+} swdg_structured_spec;
+
+/* Context whose mesh is generated on the device (the 1M-element throughput
+ * meshes never touch host memory).  Geometry agrees with the host-built
+ * reference mesh to rounding (device libm + FMA), not bitwise. */
+int swdg_gpu_create_structured(const swdg_structured_spec* spec, const swdg_params* params,
+                               int device, swdg_gpu** out);
+
+/* Copy a device geometry array ("y_eta", "jac", "b", "face_nx", "x", ...) to host. */
+int swdg_gpu_download_geometry(swdg_gpu* ctx, const char* name, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,6 +28,8 @@ SOURCES = {
     "kernels_exact.cu": ["--fmad=false"],
     "kernels_common.cu": [],
     "kernels_fast.cu": [],
+    "kernels_mesh.cu": [],
+    "host_mesh.cpp": [],
 }
 
 
@@ -52,7 +54,7 @@ def build(verbose: bool = False, force: bool = False, ptxas_v: bool = False) -> 
         path = os.path.join(CSRC, src)
         if not os.path.exists(path):
             continue
-        obj = os.path.join(OBJ_DIR, src.replace(".cu", ".o"))
+        obj = os.path.join(OBJ_DIR, os.path.splitext(src)[0] + ".o")
         objs.append(obj)
         if force or _stale(obj, [path] + hdrs):
             cmd = [NVCC, *ARCH, *COMMON, *extra, "-c", path, "-o", obj]

@@ -12,9 +12,15 @@
 
 #include "../../include/swdg_gpu.h"
 #include "swdg_device.cuh"
+#include "swdg_host.h"
 #include "swdg_launch.h"
+#include "swdg_mesh.h"
 
 using namespace swdg_dev;
+
+extern "C" int swdg_operators(int degree, double* nodes, double* weights, double* deriv,
+                              double* deriv_modified, double* deriv_weak, double* vand,
+                              double* vand_inv);
 
 namespace {
 thread_local std::string g_create_error;
@@ -44,22 +50,26 @@ struct swdg_gpu {
   swdg_params params{};
   Phys phys{};
   Mesh M{};
-  long long nn = 0, nn_owned = 0;
+  long long nn = 0, nf = 0;
   int64_t launches = 0;
   std::string err;
+  bool fast = false;   // fused fast stage kernel in use
 
   std::vector<void*> allocations;
-  double* W[3] = {};  // current state
+  double* geo = nullptr;   // 8 nodal + 4 face arrays
+  double* xy = nullptr;    // device x,y (structured meshes)
+  double* W[3] = {};       // current state
   double* A[3] = {};
   double* B[3] = {};
-  double* R[3] = {};  // rhs output
+  double* R[3] = {};       // rhs output
   double *eps = nullptr, *r_ind = nullptr;
   double *fvu = nullptr, *fvv = nullptr, *gvu = nullptr, *gvv = nullptr;
   double *fh = nullptr, *fhu = nullptr, *fhv = nullptr;
   double *partial = nullptr, *sums = nullptr;
-  Flags* flags = nullptr;      // device
-  Flags* flags_h = nullptr;    // pinned host mirror
-  double* sums_h = nullptr;    // pinned
+  Flags* flags = nullptr;       // device, 3 (one per stage)
+  Flags* flags_init = nullptr;  // device, reset image
+  Flags* flags_h = nullptr;     // pinned host mirror, 3
+  double* sums_h = nullptr;     // pinned
 
   std::vector<double> x, y, eps_h, r_h, fbuf;
   swdg_forcing_fn forcing = nullptr;
@@ -115,19 +125,12 @@ double ramp(double r, const swdg_params& p) {
 }
 
 void reset_flags(swdg_gpu* c) {
-  Flags f{};
-  f.min_h_key = ~0ull;
-  f.dt_key = ~0ull;
-  f.minlen_key = ~0ull;
-  f.posdt_key = ~0ull;
-  f.max_eps_key = ~0ull;
-  *c->flags_h = f;
-  ck(cudaMemcpyAsync(c->flags, c->flags_h, sizeof(Flags), cudaMemcpyHostToDevice, c->stream),
-     "reset flags");
+  ck(cudaMemcpyAsync(c->flags, c->flags_init, 3 * sizeof(Flags), cudaMemcpyDeviceToDevice,
+                     c->stream), "reset flags");
 }
 
 void read_flags(swdg_gpu* c) {
-  ck(cudaMemcpyAsync(c->flags_h, c->flags, sizeof(Flags), cudaMemcpyDeviceToHost, c->stream),
+  ck(cudaMemcpyAsync(c->flags_h, c->flags, 3 * sizeof(Flags), cudaMemcpyDeviceToHost, c->stream),
      "read flags");
   ck(cudaStreamSynchronize(c->stream), "sync flags");
 }
@@ -155,6 +158,15 @@ double stage_viscosity(swdg_gpu* c, CState in) {
   return mx;
 }
 
+void ensure_xy(swdg_gpu* c) {
+  if (!c->x.empty() || !c->xy) return;
+  c->x.resize(c->nn);
+  c->y.resize(c->nn);
+  ck(cudaMemcpy(c->x.data(), c->xy, c->nn * sizeof(double), cudaMemcpyDeviceToHost), "x D2H");
+  ck(cudaMemcpy(c->y.data(), c->xy + c->nn, c->nn * sizeof(double), cudaMemcpyDeviceToHost),
+     "y D2H");
+}
+
 bool stage_forcing(swdg_gpu* c, double ts) {
   if (!c->forcing) return false;
   const long long nn = c->nn;
@@ -167,9 +179,10 @@ bool stage_forcing(swdg_gpu* c, double ts) {
   return true;
 }
 
-// dW/dt of `in` (+ optional stage update into `out`).  Returns max eps.
+// dW/dt of `in` (+ optional stage update into `out`, limiter into flags[k]).
+// Returns max eps.
 double stage(swdg_gpu* c, CState in, double* const* out, int k, double t, double dt,
-             bool viscous, double* const* rhs) {
+             bool viscous, double* const* rhs, Flags* F) {
   StageArgs a{};
   a.in = in;
   a.wn = cs(c->W);
@@ -195,13 +208,177 @@ double stage(swdg_gpu* c, CState in, double* const* out, int k, double t, double
     a.fhu = c->fhu;
     a.fhv = c->fhv;
   }
-  c->launches += launch_exact_rhs_stage(c->M, c->phys, a, c->stream);
+  if (c->fast && !viscous) {
+    c->launches += launch_fast_stage(c->M, c->phys, a, F, c->stream);
+  } else {
+    c->launches += launch_exact_rhs_stage(c->M, c->phys, a, c->stream);
+    if (out) c->launches += launch_exact_limit(c->M, c->phys, st(out), F, c->stream);
+  }
   return mx;
 }
 
 void upload(double* dst, const double* src, size_t n, const char* what) {
   if (!src) throw InputError{std::string("mesh view: missing array ") + what};
   ck(cudaMemcpy(dst, src, n * sizeof(double), cudaMemcpyHostToDevice), what);
+}
+
+void validate_params(const swdg_params* p, int N) {
+  if (N < 1 || N > 15) throw InputError{"degree must be in [1, 15]"};
+  if (p->visc_enabled && N < 2)
+    throw InputError{"artificial viscosity requires polynomial degree >= 2"};
+  if (p->visc_enabled && !(p->sigma_min < p->sigma_max))
+    throw InputError{"viscosity: sigma_min must be < sigma_max"};
+  if (p->visc_enabled && p->epsilon0 < 0.0) throw InputError{"viscosity: epsilon0 must be >= 0"};
+  if (p->mode != SWDG_MODE_EXACT && p->mode != SWDG_MODE_FAST)
+    throw InputError{"unknown arithmetic mode"};
+}
+
+// element-face connectivity from MeshTopology::faces (mesh.hpp:46-54)
+std::vector<int4> connectivity(int K, const swdg_face* faces, int n_faces) {
+  std::vector<int4> ef(4 * (size_t)K, int4{-1, 0, 0, 0});
+  auto claim = [&](int e, int f, int4 v) {
+    if (e < 0 || e >= K || f < 0 || f > 3) throw InputError{"face list: element/face out of range"};
+    if (ef[4 * e + f].y & EF_PRESENT) throw InputError{"face list: element face listed twice"};
+    ef[4 * e + f] = v;
+  };
+  for (int i = 0; i < n_faces; ++i) {
+    const swdg_face& f = faces[i];
+    const int rev = f.reversed ? EF_REVERSED : 0;
+    if (f.tag == SWDG_TAG_WALL) {
+      claim(f.elem_minus, f.face_minus, int4{-1, EF_PRESENT | EF_MINUS | EF_WALL, i, 0});
+    } else if (f.tag == SWDG_TAG_INTERIOR) {
+      if (f.face_plus < 0 || f.face_plus > 3) throw InputError{"face list: bad plus face"};
+      claim(f.elem_minus, f.face_minus,
+            int4{f.elem_plus, EF_PRESENT | EF_MINUS | rev | f.face_plus, i, 0});
+      claim(f.elem_plus, f.face_plus, int4{f.elem_minus, EF_PRESENT | rev | f.face_minus, i, 0});
+    } else {
+      throw InputError{"exterior_state: unknown boundary tag"};
+    }
+  }
+  return ef;
+}
+
+// Device allocation shared by both constructors.  Geometry arrays are left for
+// the caller to fill.
+void allocate(swdg_gpu* c, int K, int n_owned, int N, const std::vector<int4>& ef,
+              const double* ops_w, const double* ops_d, const double* ops_dt,
+              const double* ops_dh, const double* ops_vinv) {
+  const int n1 = N + 1, np = n1 * n1;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    throw CudaError{cudaErrorNoDevice, "no CUDA device (there is no CPU fallback)"};
+  ck(cudaSetDevice(c->device), "cudaSetDevice");
+  ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+  c->own_stream = true;
+  const long long nn = (long long)K * np, nf = (long long)K * 4 * n1;
+  c->nn = nn;
+  c->nf = nf;
+  c->geo = c->dalloc<double>(8 * nn + 4 * nf);
+  double* ops = c->dalloc<double>(n1 + 4 * np);
+  upload(ops, ops_w, n1, "weights");
+  upload(ops + n1, ops_d, np, "deriv");
+  upload(ops + n1 + np, ops_dt, np, "deriv_modified");
+  upload(ops + n1 + 2 * np, ops_dh, np, "deriv_weak");
+  upload(ops + n1 + 3 * np, ops_vinv, np, "vandermonde_inv");
+  int4* def = c->dalloc<int4>(ef.size());
+  ck(cudaMemcpy(def, ef.data(), ef.size() * sizeof(int4), cudaMemcpyHostToDevice), "ef");
+
+  Mesh& M = c->M;
+  M.K = K;
+  M.n_owned = n_owned;
+  M.n1 = n1;
+  M.np = np;
+  M.degree = N;
+  M.w0 = ops_w[0];
+  M.w = ops;
+  M.D = ops + n1;
+  M.Dt = ops + n1 + np;
+  M.Dh = ops + n1 + 2 * np;
+  M.Vinv = ops + n1 + 3 * np;
+  double* geo = c->geo;
+  M.ye = geo;
+  M.xe = geo + nn;
+  M.yx = geo + 2 * nn;
+  M.xx = geo + 3 * nn;
+  M.jac = geo + 4 * nn;
+  M.b = geo + 5 * nn;
+  M.len_xi = geo + 6 * nn;
+  M.len_eta = geo + 7 * nn;
+  double* fgeo = geo + 8 * nn;
+  M.fnx = fgeo;
+  M.fny = fgeo + nf;
+  M.fjs = fgeo + 2 * nf;
+  M.fa = fgeo + 3 * nf;
+  M.ef = def;
+
+  if (c->params.mode == SWDG_MODE_FAST) {
+    const int rc = upload_fast_ops(n1, ops_d, ops_dt, ops_dh, ops_vinv, ops_w);
+    if (rc == -1) throw InputError{"fast mode: operators differ from the LGL operators of this degree"};
+    if (rc < 0) throw CudaError{cudaErrorInvalidSymbol, "upload operators"};
+    c->fast = fast_stage_supported(n1);
+  }
+
+  double* sbuf = c->dalloc<double>(12 * nn);
+  for (int k = 0; k < 3; ++k) {
+    c->W[k] = sbuf + k * nn;
+    c->A[k] = sbuf + (3 + k) * nn;
+    c->B[k] = sbuf + (6 + k) * nn;
+    c->R[k] = sbuf + (9 + k) * nn;
+  }
+  ck(cudaMemset(sbuf, 0, 12 * nn * sizeof(double)), "memset state");
+  c->eps = c->dalloc<double>(K);
+  c->r_ind = c->dalloc<double>(K);
+  ck(cudaMemset(c->eps, 0, K * sizeof(double)), "memset eps");
+  if (c->params.visc_enabled) {
+    double* vb = c->dalloc<double>(4 * nn);
+    c->fvu = vb;
+    c->fvv = vb + nn;
+    c->gvu = vb + 2 * nn;
+    c->gvv = vb + 3 * nn;
+  }
+  c->partial = c->dalloc<double>(2 * (size_t)K);
+  c->sums = c->dalloc<double>(2);
+  c->flags = c->dalloc<Flags>(3);
+  c->flags_init = c->dalloc<Flags>(3);
+  ck(cudaMallocHost(&c->flags_h, 3 * sizeof(Flags)), "pinned flags");
+  ck(cudaMallocHost(&c->sums_h, 2 * sizeof(double)), "pinned sums");
+  Flags f{};
+  f.min_h_key = ~0ull;
+  f.dt_key = ~0ull;
+  f.minlen_key = ~0ull;
+  f.posdt_key = ~0ull;
+  f.max_eps_key = ~0ull;
+  for (int k = 0; k < 3; ++k) c->flags_h[k] = f;
+  ck(cudaMemcpy(c->flags_init, c->flags_h, 3 * sizeof(Flags), cudaMemcpyHostToDevice), "flags");
+  c->eps_h.assign(K, 0.0);
+  c->r_h.assign(K, 0.0);
+}
+
+swdg_gpu* new_context(const swdg_params* p, int device) {
+  auto* c = new swdg_gpu;
+  c->device = device;
+  c->params = *p;
+  c->phys = Phys{p->g, p->h_tol, p->h_des, p->h_ref, p->epsilon0, p->sigma_min,
+                 p->sigma_max, p->visc_enabled, p->limiter_enabled};
+  return c;
+}
+
+template <class F>
+int create_guarded(swdg_gpu* c, swdg_gpu** out, F&& body) {
+  try {
+    body();
+    ck(cudaDeviceSynchronize(), "create sync");
+  } catch (const CudaError& e) {
+    g_create_error = std::string(e.where) + ": " + cudaGetErrorString(e.e);
+    delete c;
+    return SWDG_ERR_CUDA;
+  } catch (const InputError& e) {
+    g_create_error = e.msg;
+    delete c;
+    return SWDG_ERR_INPUT;
+  }
+  *out = c;
+  return SWDG_OK;
 }
 
 }  // namespace
@@ -218,52 +395,17 @@ int swdg_gpu_create(const swdg_mesh_view* mv, const swdg_params* p, int device,
     g_create_error = "null mesh or params";
     return SWDG_ERR_INPUT;
   }
-  auto* c = new swdg_gpu;
-  c->device = device;
-  try {
+  swdg_gpu* c = new_context(p, device);
+  return create_guarded(c, out, [&] {
     const int N = mv->degree, n1 = N + 1, np = n1 * n1, K = mv->n_elem;
-    if (N < 1 || N > 15) throw InputError{"degree must be in [1, 15]"};
+    validate_params(p, N);
     if (K < 1) throw InputError{"mesh has no elements"};
     const int n_owned = mv->n_owned > 0 ? mv->n_owned : K;
     if (n_owned > K) throw InputError{"n_owned exceeds n_elem"};
-    if (p->visc_enabled && N < 2)
-      throw InputError{"artificial viscosity requires polynomial degree >= 2"};
-    if (p->visc_enabled && !(p->sigma_min < p->sigma_max))
-      throw InputError{"viscosity: sigma_min must be < sigma_max"};
-    if (p->visc_enabled && p->epsilon0 < 0.0)
-      throw InputError{"viscosity: epsilon0 must be >= 0"};
-    if (p->mode != SWDG_MODE_EXACT && p->mode != SWDG_MODE_FAST)
-      throw InputError{"unknown arithmetic mode"};
-    if (p->mode == SWDG_MODE_FAST) throw InputError{"fast mode not built yet"};
-
-    c->params = *p;
-    c->phys = Phys{p->g, p->h_tol, p->h_des, p->h_ref, p->epsilon0, p->sigma_min,
-                   p->sigma_max, p->visc_enabled, p->limiter_enabled};
-    const long long nn = (long long)K * np, nf = (long long)K * 4 * n1;
-    c->nn = nn;
-    c->nn_owned = (long long)n_owned * np;
-
-    // element-face connectivity from MeshTopology::faces (mesh.hpp:46-54)
-    std::vector<int4> ef(4 * (size_t)K, int4{-1, 0, 0, 0});
-    auto claim = [&](int e, int f, int4 v) {
-      if (e < 0 || e >= K || f < 0 || f > 3) throw InputError{"face list: element/face out of range"};
-      if (ef[4 * e + f].y & EF_PRESENT) throw InputError{"face list: element face listed twice"};
-      ef[4 * e + f] = v;
-    };
+    const std::vector<int4> ef = connectivity(K, mv->faces, mv->n_faces);
+    // check_unit_normal (physics.hpp:71-74) for every face node a flux visits
     for (int i = 0; i < mv->n_faces; ++i) {
       const swdg_face& f = mv->faces[i];
-      const int rev = f.reversed ? EF_REVERSED : 0;
-      if (f.tag == SWDG_TAG_WALL) {
-        claim(f.elem_minus, f.face_minus, int4{-1, EF_PRESENT | EF_MINUS | EF_WALL, i, 0});
-      } else if (f.tag == SWDG_TAG_INTERIOR) {
-        if (f.face_plus < 0 || f.face_plus > 3) throw InputError{"face list: bad plus face"};
-        claim(f.elem_minus, f.face_minus,
-              int4{f.elem_plus, EF_PRESENT | EF_MINUS | rev | f.face_plus, i, 0});
-        claim(f.elem_plus, f.face_plus, int4{f.elem_minus, EF_PRESENT | rev | f.face_minus, i, 0});
-      } else {
-        throw InputError{"exterior_state: unknown boundary tag"};
-      }
-      // check_unit_normal (physics.hpp:71-74) for every face node the flux visits
       for (int t = 0; t < n1; ++t) {
         const long long fm = ((long long)f.elem_minus * 4 + f.face_minus) * n1 + t;
         const double nx = mv->face_nx[fm], ny = mv->face_ny[fm];
@@ -271,17 +413,10 @@ int swdg_gpu_create(const swdg_mesh_view* mv, const swdg_params* p, int device,
           throw InputError{"normal vector is not unit length"};
       }
     }
-
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
-      throw CudaError{cudaErrorNoDevice, "no CUDA device (there is no CPU fallback)"};
-    ck(cudaSetDevice(device), "cudaSetDevice");
-    ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
-    c->own_stream = true;
-
-    // geometry: 8 nodal arrays (ye, xe, yx, xx, jac, b, len_xi, len_eta),
-    // 4 face arrays, operators
-    double* geo = c->dalloc<double>(8 * nn + 4 * nf);
+    allocate(c, K, n_owned, N, ef, mv->weights, mv->deriv, mv->deriv_modified, mv->deriv_weak,
+             mv->vandermonde_inv);
+    const long long nn = (long long)K * np, nf = (long long)K * 4 * n1;
+    double* geo = c->geo;
     upload(geo + 0 * nn, mv->y_eta, nn, "y_eta");
     upload(geo + 1 * nn, mv->x_eta, nn, "x_eta");
     upload(geo + 2 * nn, mv->y_xi, nn, "y_xi");
@@ -304,83 +439,55 @@ int swdg_gpu_create(const swdg_mesh_view* mv, const swdg_params* p, int device,
     upload(fgeo + 1 * nf, mv->face_ny, nf, "face_ny");
     upload(fgeo + 2 * nf, mv->face_jsurf, nf, "face_jsurf");
     upload(fgeo + 3 * nf, mv->face_a, nf, "face_a");
-    double* ops = c->dalloc<double>(n1 + 4 * np);
-    upload(ops, mv->weights, n1, "weights");
-    upload(ops + n1, mv->deriv, np, "deriv");
-    upload(ops + n1 + np, mv->deriv_modified, np, "deriv_modified");
-    upload(ops + n1 + 2 * np, mv->deriv_weak, np, "deriv_weak");
-    upload(ops + n1 + 3 * np, mv->vandermonde_inv, np, "vandermonde_inv");
-    int4* def = c->dalloc<int4>(ef.size());
-    ck(cudaMemcpy(def, ef.data(), ef.size() * sizeof(int4), cudaMemcpyHostToDevice), "ef");
-
-    Mesh& M = c->M;
-    M.K = K;
-    M.n_owned = n_owned;
-    M.n1 = n1;
-    M.np = np;
-    M.degree = N;
-    M.w0 = mv->weights[0];
-    M.w = ops;
-    M.D = ops + n1;
-    M.Dt = ops + n1 + np;
-    M.Dh = ops + n1 + 2 * np;
-    M.Vinv = ops + n1 + 3 * np;
-    M.ye = geo;
-    M.xe = geo + nn;
-    M.yx = geo + 2 * nn;
-    M.xx = geo + 3 * nn;
-    M.jac = geo + 4 * nn;
-    M.b = geo + 5 * nn;
-    M.len_xi = geo + 6 * nn;
-    M.len_eta = geo + 7 * nn;
-    M.fnx = fgeo;
-    M.fny = fgeo + nf;
-    M.fjs = fgeo + 2 * nf;
-    M.fa = fgeo + 3 * nf;
-    M.ef = def;
-
-    // state buffers (current, two stage buffers, rhs)
-    double* sbuf = c->dalloc<double>(12 * nn);
-    for (int k = 0; k < 3; ++k) {
-      c->W[k] = sbuf + k * nn;
-      c->A[k] = sbuf + (3 + k) * nn;
-      c->B[k] = sbuf + (6 + k) * nn;
-      c->R[k] = sbuf + (9 + k) * nn;
-    }
-    ck(cudaMemset(sbuf, 0, 12 * nn * sizeof(double)), "memset state");
-    c->eps = c->dalloc<double>(K);
-    c->r_ind = c->dalloc<double>(K);
-    ck(cudaMemset(c->eps, 0, K * sizeof(double)), "memset eps");
-    if (p->visc_enabled) {
-      double* vb = c->dalloc<double>(4 * nn);
-      c->fvu = vb;
-      c->fvv = vb + nn;
-      c->gvu = vb + 2 * nn;
-      c->gvv = vb + 3 * nn;
-    }
-    c->partial = c->dalloc<double>(2 * (size_t)K);
-    c->sums = c->dalloc<double>(2);
-    c->flags = c->dalloc<Flags>(1);
-    ck(cudaMallocHost(&c->flags_h, sizeof(Flags)), "pinned flags");
-    ck(cudaMallocHost(&c->sums_h, 2 * sizeof(double)), "pinned sums");
-    c->eps_h.assign(K, 0.0);
-    c->r_h.assign(K, 0.0);
     if (mv->x && mv->y) {
       c->x.assign(mv->x, mv->x + nn);
       c->y.assign(mv->y, mv->y + nn);
     }
-    ck(cudaDeviceSynchronize(), "create sync");
-  } catch (const CudaError& e) {
-    g_create_error = std::string(e.where) + ": " + cudaGetErrorString(e.e);
-    delete c;
-    return SWDG_ERR_CUDA;
-  } catch (const InputError& e) {
-    g_create_error = e.msg;
-    delete c;
+  });
+}
+
+int swdg_gpu_create_structured(const swdg_structured_spec* s, const swdg_params* p, int device,
+                               swdg_gpu** out) {
+  *out = nullptr;
+  g_create_error.clear();
+  if (!s || !p) {
+    g_create_error = "null spec or params";
     return SWDG_ERR_INPUT;
   }
-  *out = c;
-  return SWDG_OK;
+  swdg_gpu* c = new_context(p, device);
+  return create_guarded(c, out, [&] {
+    const int N = s->degree, n1 = N + 1, np = n1 * n1;
+    validate_params(p, N);
+    if (s->kx < 1 || s->ky < 1) throw InputError{"mesh: element counts must be >= 1"};
+    if (s->kind < 0 || s->kind > 2) throw InputError{"unknown mesh kind"};
+    const long long Kl = (long long)s->kx * s->ky;
+    if (Kl * np > (1ll << 31) - 1) throw InputError{"mesh too large for int32 node indices"};
+    const int K = (int)Kl;
+    const std::vector<swdg_face> faces =
+        swdg_host::structured_faces(s->kx, s->ky, s->periodic_x != 0, s->periodic_y != 0);
+    const std::vector<int4> ef = connectivity(K, faces.data(), (int)faces.size());
+    std::vector<double> nodes(n1), w(n1), D(np), Dt(np), Dh(np), V(np), Vi(np);
+    swdg_operators(N, nodes.data(), w.data(), D.data(), Dt.data(), Dh.data(), V.data(), Vi.data());
+    allocate(c, K, K, N, ef, w.data(), D.data(), Dt.data(), Dh.data(), Vi.data());
+    const long long nn = c->nn, nf = c->nf;
+    c->xy = c->dalloc<double>(2 * nn);
+    double* dnodes = c->dalloc<double>(n1);
+    ck(cudaMemcpy(dnodes, nodes.data(), n1 * sizeof(double), cudaMemcpyHostToDevice), "nodes");
+    int* bad = c->dalloc<int>(1);
+    ck(cudaMemset(bad, 0, sizeof(int)), "memset");
+    MeshSpecDev sd{s->kind, s->kx, s->ky, s->bathy_kind, s->x0, s->x1, s->y0, s->y1, s->extra,
+                   {s->bathy[0], s->bathy[1], s->bathy[2], s->bathy[3]}};
+    double* geo = c->geo;
+    double* fgeo = geo + 8 * nn;
+    MeshOut o{c->xy, c->xy + nn, geo + 3 * nn, geo + 1 * nn, geo + 2 * nn, geo + 0 * nn,
+              geo + 4 * nn, geo + 5 * nn, geo + 6 * nn, geo + 7 * nn,
+              fgeo, fgeo + nf, fgeo + 2 * nf, fgeo + 3 * nf, bad};
+    c->launches += launch_structured_mesh(sd, dnodes, c->M.D, n1, o, c->stream);
+    int hbad = 0;
+    ck(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "bad D2H");
+    ck(cudaStreamSynchronize(c->stream), "mesh sync");
+    if (hbad) throw InputError{"mesh rejected: nonpositive Jacobian"};
+  });
 }
 
 void swdg_gpu_destroy(swdg_gpu* c) {
@@ -448,11 +555,38 @@ int swdg_gpu_device_state(swdg_gpu* c, double** h, double** hu, double** hv) {
   });
 }
 
+int swdg_gpu_download_geometry(swdg_gpu* c, const char* name, double* out) {
+  return guarded(c, [&] {
+    const std::string n(name);
+    const double* src = nullptr;
+    long long len = c->nn;
+    const Mesh& M = c->M;
+    if (n == "y_eta") src = M.ye;
+    else if (n == "x_eta") src = M.xe;
+    else if (n == "y_xi") src = M.yx;
+    else if (n == "x_xi") src = M.xx;
+    else if (n == "jac") src = M.jac;
+    else if (n == "b") src = M.b;
+    else if (n == "x" && c->xy) src = c->xy;
+    else if (n == "y" && c->xy) src = c->xy + c->nn;
+    else {
+      len = c->nf;
+      if (n == "face_nx") src = M.fnx;
+      else if (n == "face_ny") src = M.fny;
+      else if (n == "face_jsurf") src = M.fjs;
+      else if (n == "face_a") src = M.fa;
+    }
+    if (!src) throw InputError{"unknown geometry array " + n};
+    ck(cudaMemcpy(out, src, len * sizeof(double), cudaMemcpyDeviceToHost), "geometry D2H");
+    return SWDG_OK;
+  });
+}
+
 static int rhs_common(swdg_gpu* c, double t, double* rh, double* rhu, double* rhv,
                       bool viscous) {
   return guarded(c, [&] {
-    double mx = stage(c, cs(c->W), nullptr, 0, t, 0.0, viscous, c->R);
-    (void)mx;
+    reset_flags(c);
+    stage(c, cs(c->W), nullptr, 0, t, 0.0, viscous, c->R, c->flags);
     double* dst[3] = {rh, rhu, rhv};
     for (int k = 0; k < 3; ++k)
       ck(cudaMemcpyAsync(dst[k], c->R[k], c->nn * sizeof(double), cudaMemcpyDeviceToHost,
@@ -481,10 +615,10 @@ int swdg_gpu_compute_dt(swdg_gpu* c, double cfl, double* dt) {
     reset_flags(c);
     c->launches += launch_exact_dt(c->M, c->phys, cs(c->W), c->flags, c->stream);
     read_flags(c);
-    double d = key_value(c->flags_h->dt_key);
+    double d = key_value(c->flags_h[0].dt_key);
     if (!std::isfinite(d)) {
       const double order = 2.0 * c->M.degree + 1.0;
-      d = key_value(c->flags_h->minlen_key) /
+      d = key_value(c->flags_h[0].minlen_key) /
           (order * std::sqrt(c->params.g * std::max(c->params.h_ref, 1e-12)));
     }
     *dt = cfl * d;
@@ -492,33 +626,55 @@ int swdg_gpu_compute_dt(swdg_gpu* c, double cfl, double* dt) {
   });
 }
 
+// Fold per-stage flags into the reference's try_step report.  Returns the
+// index of the first rejecting stage (3 = none).
+static int fold_flags(swdg_gpu* c, swdg_step_info& r, int& code) {
+  for (int k = 0; k < 3; ++k) {
+    const Flags& f = c->flags_h[k];
+    if (f.abort) {
+      code = fail(c, SWDG_ERR_ABORT, "negative water height without limiter");
+      return k;
+    }
+    if (f.reject) return k;
+    if (c->params.limiter_enabled) r.n_limited = f.n_limited;
+    r.min_stage_h = std::min(r.min_stage_h, key_value(f.min_h_key));
+  }
+  return 3;
+}
+
 int swdg_gpu_try_step(swdg_gpu* c, double t, double dt, swdg_step_info* info) {
   return guarded(c, [&] {
     swdg_step_info r{};
     r.min_stage_h = std::numeric_limits<double>::infinity();
-    r.max_eps = 0.0;
-    r.n_limited = 0;
-    r.accepted = 0;
     double* const* outs[3] = {c->A, c->B, c->A};
     CState in = cs(c->W);
     const bool viscous = c->params.visc_enabled != 0;
     int code = SWDG_OK;
-    for (int k = 0; k < 3; ++k) {
-      reset_flags(c);
-      const double mx = stage(c, in, outs[k], k, t, dt, viscous, nullptr);
-      r.max_eps = std::max(r.max_eps, mx);
-      c->launches += launch_exact_limit(c->M, c->phys, st(outs[k]), c->flags, c->stream);
-      read_flags(c);
-      const Flags& f = *c->flags_h;
-      if (f.abort) {
-        code = fail(c, SWDG_ERR_ABORT, "negative water height without limiter");
-        break;
+    reset_flags(c);
+    if (c->fast && !viscous && !c->forcing) {
+      // device-resident: three stages back to back, one flag read per step
+      for (int k = 0; k < 3; ++k) {
+        stage(c, in, outs[k], k, t, dt, false, nullptr, c->flags + k);
+        in = cs(outs[k]);
       }
-      if (f.reject) break;
-      if (c->params.limiter_enabled) r.n_limited = f.n_limited;
-      r.min_stage_h = std::min(r.min_stage_h, key_value(f.min_h_key));
-      in = cs(outs[k]);
-      if (k == 2) r.accepted = 1;
+      read_flags(c);
+      r.accepted = fold_flags(c, r, code) == 3 && code == SWDG_OK;
+    } else {
+      for (int k = 0; k < 3; ++k) {
+        const double mx = stage(c, in, outs[k], k, t, dt, viscous, nullptr, c->flags + k);
+        r.max_eps = std::max(r.max_eps, mx);
+        read_flags(c);
+        const Flags& f = c->flags_h[k];
+        if (f.abort) {
+          code = fail(c, SWDG_ERR_ABORT, "negative water height without limiter");
+          break;
+        }
+        if (f.reject) break;
+        if (c->params.limiter_enabled) r.n_limited = f.n_limited;
+        r.min_stage_h = std::min(r.min_stage_h, key_value(f.min_h_key));
+        in = cs(outs[k]);
+        if (k == 2) r.accepted = 1;
+      }
     }
     if (r.accepted)
       for (int k = 0; k < 3; ++k) std::swap(c->W[k], c->A[k]);
@@ -530,12 +686,34 @@ int swdg_gpu_try_step(swdg_gpu* c, double t, double dt, swdg_step_info* info) {
 
 int swdg_gpu_run_steps(swdg_gpu* c, int nsteps, double t, double dt) {
   return guarded(c, [&] {
-    for (int s = 0; s < nsteps; ++s) {
-      swdg_step_info r{};
-      const int rc = swdg_gpu_try_step(c, t + s * dt, dt, &r);
-      if (rc) return rc;
+    const bool viscous = c->params.visc_enabled != 0;
+    if (!(c->fast && !viscous && !c->forcing)) {
+      for (int s = 0; s < nsteps; ++s) {
+        swdg_step_info r{};
+        const int rc = swdg_gpu_try_step(c, t + s * dt, dt, &r);
+        if (rc) return rc;
+      }
+      return SWDG_OK;
     }
-    return SWDG_OK;
+    // device-resident: no host synchronisation; reject/abort/min h accumulate
+    // over the run in the per-stage flags and are folded at the end
+    reset_flags(c);
+    double* const* outs[3] = {c->A, c->B, c->A};
+    for (int s = 0; s < nsteps; ++s) {
+      CState in = cs(c->W);
+      for (int k = 0; k < 3; ++k) {
+        stage(c, in, outs[k], k, t + s * dt, dt, false, nullptr, c->flags + k);
+        in = cs(outs[k]);
+      }
+      for (int k = 0; k < 3; ++k) std::swap(c->W[k], c->A[k]);
+    }
+    read_flags(c);
+    swdg_step_info r{};
+    r.min_stage_h = std::numeric_limits<double>::infinity();
+    int code = SWDG_OK;
+    r.accepted = fold_flags(c, r, code) == 3 && code == SWDG_OK;
+    c->last = r;
+    return code;
   });
 }
 
@@ -563,14 +741,15 @@ int swdg_gpu_diagnostics(swdg_gpu* c, swdg_diagnostics* out) {
     read_flags(c);
     out->mass = c->sums_h[0];
     out->entropy = c->sums_h[1];
-    out->min_h = key_value(c->flags_h->min_h_key);
-    out->positivity_dt = key_value(c->flags_h->posdt_key);
+    out->min_h = key_value(c->flags_h[0].min_h_key);
+    out->positivity_dt = key_value(c->flags_h[0].posdt_key);
     return SWDG_OK;
   });
 }
 
 int swdg_gpu_set_forcing(swdg_gpu* c, swdg_forcing_fn fn, void* user) {
   return guarded(c, [&] {
+    if (fn) ensure_xy(c);
     if (fn && c->x.empty()) throw InputError{"forcing needs the mesh x/y arrays"};
     c->forcing = fn;
     c->forcing_user = user;

@@ -30,6 +30,13 @@ int launch_exact_rhs_stage(const Mesh& M, const Phys& P, const StageArgs& A, cud
 int launch_exact_limit(const Mesh& M, const Phys& P, State S, Flags* F, cudaStream_t st);
 int launch_exact_dt(const Mesh& M, const Phys& P, CState S, Flags* F, cudaStream_t st);
 
+// fast mode (kernels_fast.cu)
+int upload_fast_ops(int n1, const double* D, const double* Dt, const double* Dh,
+                    const double* Vinv, const double* w);
+bool fast_stage_supported(int n1);
+int launch_fast_stage(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
+                      cudaStream_t st);
+
 // mode-independent (kernels_common.cu)
 int launch_diagnostics(const Mesh& M, const Phys& P, CState S, double* partial, double* out2,
                        Flags* F, cudaStream_t st);

@@ -72,6 +72,52 @@ class DiagnosticsC(C.Structure):
                 ("positivity_dt", C.c_double)]
 
 
+class StructuredSpecC(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("degree", C.c_int32), ("kx", C.c_int32), ("ky", C.c_int32),
+                ("periodic_x", C.c_int32), ("periodic_y", C.c_int32),
+                ("bathy_kind", C.c_int32), ("reserved", C.c_int32),
+                ("x0", C.c_double), ("x1", C.c_double), ("y0", C.c_double), ("y1", C.c_double),
+                ("extra", C.c_double), ("bathy", C.c_double * 4)]
+
+
+MESH_KINDS = {"cartesian": 0, "curved_dam": 1, "wavy": 2}
+BATHY_KINDS = {"none": 0, "constant": 1, "linear": 2, "paraboloid": 3, "smooth": 4,
+               "step": 5, "sine": 6}
+
+
+def structured_spec(kind: str, degree: int, kx: int, ky: int, x0=0.0, x1=1.0, y0=0.0, y1=1.0,
+                    periodic_x=False, periodic_y=False, extra=None, bathy="none",
+                    bathy_params=()) -> StructuredSpecC:
+    """Generator spec of build_cartesian/curved_dam/wavy_mesh (mesh.hpp:342-379)."""
+    if extra is None:
+        extra = 0.5 if kind == "curved_dam" else 0.04
+    if kind == "curved_dam" and (x0, x1, y0, y1) == (0.0, 1.0, 0.0, 1.0):
+        x0, x1, y0, y1 = -5.0, 7.5, -5.0, 5.0
+    bp = (C.c_double * 4)(*(list(bathy_params) + [0.0] * (4 - len(bathy_params))))
+    return StructuredSpecC(MESH_KINDS[kind], degree, kx, ky, int(periodic_x), int(periodic_y),
+                           BATHY_KINDS[bathy], 0, x0, x1, y0, y1, extra, bp)
+
+
+def operators(degree: int) -> dict:
+    """make_operators (operators.hpp:148) from the host library (no device needed)."""
+    n1 = degree + 1
+    keys = ("nodes", "weights", "deriv", "deriv_modified", "deriv_weak", "vandermonde",
+            "vandermonde_inv")
+    out = {k: np.zeros(n1 if k in ("nodes", "weights") else n1 * n1) for k in keys}
+    rc = lib().swdg_operators(degree, *(_ptr(out[k]) for k in keys))
+    if rc != SWDG_OK:
+        raise SwdgError("swdg_operators: degree must be in [1, 15]")
+    return out
+
+
+def structured_faces(kx: int, ky: int, periodic_x=False, periodic_y=False) -> np.ndarray:
+    """structured_topology (mesh.hpp:237-290) as an (F, 6) int32 table."""
+    n = lib().swdg_structured_face_count(kx, ky, int(periodic_x), int(periodic_y))
+    out = np.zeros((n, 6), np.int32)
+    lib().swdg_structured_faces(kx, ky, int(periodic_x), int(periodic_y), out.ctypes.data)
+    return out
+
+
 FORCING_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_double, C.c_int64, _dp, _dp, _dp, _dp, _dp)
 
 _lib = None
@@ -107,6 +153,13 @@ def lib():
             "swdg_gpu_diagnostics": (C.c_int, [vp, C.POINTER(DiagnosticsC)]),
             "swdg_gpu_set_forcing": (C.c_int, [vp, FORCING_FN, vp]),
             "swdg_gpu_launch_count": (C.c_int64, [vp]),
+            "swdg_operators": (C.c_int, [C.c_int] + [_dp] * 7),
+            "swdg_structured_face_count": (C.c_int64, [C.c_int] * 4),
+            "swdg_structured_faces": (C.c_int, [C.c_int] * 4 + [vp]),
+            "swdg_gpu_create_structured": (C.c_int, [C.POINTER(StructuredSpecC),
+                                                     C.POINTER(ParamsC), C.c_int,
+                                                     C.POINTER(vp)]),
+            "swdg_gpu_download_geometry": (C.c_int, [vp, C.c_char_p, _dp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -212,6 +265,35 @@ class Mesh:
                          *(_ptr(a[k]) if k in a else None for k in _VIEW_PTRS))
 
 
+class _DeviceMesh:
+    """Shape-only stand-in for a mesh generated on the device; arrays download lazily."""
+
+    def __init__(self, degree: int, n_elem: int):
+        self.degree = degree
+        self.n_elem = n_elem
+        self.n_owned = 0
+        self.owner = None
+        self._arrays = {}
+
+    @property
+    def n1(self):
+        return self.degree + 1
+
+    @property
+    def n_nodes(self):
+        return self.n_elem * self.n1 * self.n1
+
+    @property
+    def arrays(self):
+        class _Lazy(dict):
+            def __missing__(d, k):
+                d[k] = self.owner.geometry(k)
+                return d[k]
+        if not isinstance(self._arrays, _Lazy):
+            self._arrays = _Lazy(self._arrays)
+        return self._arrays
+
+
 class State:
     """field.hpp:12-34: nodal (h, hu, hv), element-major."""
 
@@ -247,21 +329,46 @@ class TimeIntegrator:
     device-resident throughput entry is `run_steps`.
     """
 
-    def __init__(self, mesh, cfg: RunConfig, device: int = 0):
-        self.mesh = Mesh.from_any(mesh)
+    def __init__(self, mesh, cfg: RunConfig, device: int = 0, _handle=None):
         self.cfg = cfg
-        self._view = self.mesh.view()  # keeps pointers alive for the create call
-        p = cfg.c_params()
-        h = C.c_void_p()
-        rc = lib().swdg_gpu_create(C.byref(self._view), C.byref(p), device, C.byref(h))
-        if rc != SWDG_OK:
-            _raise(rc, lib().swdg_gpu_create_error().decode())
-        self._h = h
+        if _handle is None:
+            self.mesh = Mesh.from_any(mesh)
+            self._view = self.mesh.view()  # keeps pointers alive for the create call
+            p = cfg.c_params()
+            h = C.c_void_p()
+            rc = lib().swdg_gpu_create(C.byref(self._view), C.byref(p), device, C.byref(h))
+            if rc != SWDG_OK:
+                _raise(rc, lib().swdg_gpu_create_error().decode())
+            self._h = h
+        else:
+            self.mesh = mesh
+            self._h = _handle
         self._resident = None  # id of the State mirrored on the device
         self._info = StepInfoC()
         self._forcing = None
         self._forcing_c = None
         self.forcing: Optional[Callable] = None
+
+    @classmethod
+    def structured(cls, spec: StructuredSpecC, cfg: RunConfig, device: int = 0):
+        """Context over a device-generated structured mesh (swdg_gpu_create_structured)."""
+        p = cfg.c_params()
+        h = C.c_void_p()
+        rc = lib().swdg_gpu_create_structured(C.byref(spec), C.byref(p), device, C.byref(h))
+        if rc != SWDG_OK:
+            _raise(rc, lib().swdg_gpu_create_error().decode())
+        integ = cls(_DeviceMesh(spec.degree, spec.kx * spec.ky), cfg, device, _handle=h)
+        integ.mesh.owner = integ
+        return integ
+
+    def geometry(self, name: str) -> np.ndarray:
+        """Device geometry array (nodal or face layout) copied to host."""
+        n = self.mesh.n_nodes
+        if name.startswith("face_"):
+            n = self.mesh.n_elem * 4 * (self.mesh.degree + 1)
+        out = np.empty(n)
+        self._check(lib().swdg_gpu_download_geometry(self._h, name.encode(), _ptr(out)))
+        return out
 
     # -- plumbing
     def _check(self, rc):
@@ -341,7 +448,26 @@ class TimeIntegrator:
         return d
 
     def run_steps(self, nsteps: int, t: float, dt: float):
+        """Device-resident SSPRK3 steps with fixed dt (no host synchronisation)."""
         self._check(lib().swdg_gpu_run_steps(self._h, nsteps, t, dt))
+
+    def last_info(self) -> StepInfoC:
+        info = StepInfoC()
+        self._check(lib().swdg_gpu_last_info(self._h, C.byref(info)))
+        return info
+
+    def compute_dt_device(self, cfl: float) -> float:
+        """compute_dt of the device-resident state (no upload)."""
+        dt = C.c_double()
+        self._check(lib().swdg_gpu_compute_dt(self._h, cfl, C.byref(dt)))
+        return dt.value
+
+    def set_stream(self, stream_handle: int | None):
+        """Launch on an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)."""
+        self._check(lib().swdg_gpu_set_stream(self._h, C.c_void_p(stream_handle or None)))
+
+    def synchronize(self):
+        self._check(lib().swdg_gpu_synchronize(self._h))
 
     def last_eps(self) -> np.ndarray:
         e = np.zeros(self.mesh.n_elem)

@@ -1,0 +1,157 @@
+"""GPU parity, fast mode (FMA, symmetric pair evaluation, fused stage kernel): within
+the north_star tolerance of the reference — 1e-12 normwise after one stage — plus the
+device mesh generator against the reference's host-built meshes."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import ref
+from paper_1804_02221_b200 import swdg
+from tests.conftest import gpu_available
+from tests.helpers import (MESHES, build, normwise, random_state, reversed_mesh,
+                           scenario_params, smooth_state)
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device"),
+              pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")]
+
+TOL_STAGE = 1e-12  # north_star: "within 1e-12 relative error after one stage"
+
+
+def cfg_from(p, mode=swdg.MODE_FAST):
+    return swdg.RunConfig(
+        phys=swdg.PhysicsParams(p.g, p.h_tol, p.h_des, p.h_ref),
+        visc=swdg.ViscosityConfig(bool(p.visc_enabled), p.epsilon0, p.sigma_min, p.sigma_max),
+        limiter_enabled=bool(p.limiter_enabled), mode=mode)
+
+
+def S(arrs):
+    return swdg.State(*[a.copy() for a in arrs])
+
+
+def rhs_tol(m, p, s, out, want):
+    """The residual is a difference of O(|F|/J) terms: normalise by that scale."""
+    return normwise(out, want)
+
+
+@pytest.mark.parametrize("name", sorted(MESHES))
+def test_fast_assemble_rhs(name):
+    m = build(name)
+    p = ref.params(g=9.81)
+    integ = swdg.TimeIntegrator(m, cfg_from(p))
+    rng = np.random.default_rng(3)
+    for dry in (0.0, 0.2):
+        s = random_state(m.n_nodes, rng, dry_prob=dry)
+        out = integ.assemble_rhs(S(s))
+        assert normwise(out.arrays(), ref.assemble_rhs(m, p, s)) <= TOL_STAGE
+
+
+@pytest.mark.parametrize("degree", list(range(1, 16)))
+def test_fast_all_degrees(degree):
+    m = ref.build_mesh("wavy", degree, 3, 2, periodic_x=True, periodic_y=True).bathymetry("smooth")
+    p = ref.params(g=9.81)
+    s = random_state(m.n_nodes, np.random.default_rng(degree), dry_prob=0.1)
+    out = swdg.TimeIntegrator(m, cfg_from(p)).assemble_rhs(S(s))
+    assert normwise(out.arrays(), ref.assemble_rhs(m, p, s)) <= TOL_STAGE
+
+
+def test_fast_reversed_faces():
+    from oracle import port
+    m, _, _ = reversed_mesh(build("wavy_N4"))
+    p = ref.params(g=9.81)
+    s = random_state(m.n_nodes, np.random.default_rng(5), dry_prob=0.1)
+    out = swdg.TimeIntegrator(m, cfg_from(p)).assemble_rhs(S(s))
+    assert normwise(out.arrays(), port.assemble_rhs(m, p, s)) <= TOL_STAGE
+
+
+def test_fast_lake_at_rest_config1():
+    """BASELINE config 1: lake at rest, discontinuous b, curved 16x16, N=4."""
+    m = ref.build_mesh("curved_dam", 4, 16, 16).bathymetry("step", 0.0, 0.3, 0.1)
+    p = ref.params(g=9.81)
+    b = m.arrays["b"]
+    s = [1.0 - b, np.zeros_like(b), np.zeros_like(b)]
+    integ = swdg.TimeIntegrator(m, cfg_from(p))
+    r = integ.assemble_rhs(S(s))
+    assert max(np.abs(a).max() for a in r.arrays()) < 1e-11
+    st = S(s)
+    t = 0.0
+    for _ in range(20):
+        dt = integ.compute_dt(st, 0.5)
+        assert integ.try_step(st, t, dt)
+        t += dt
+    drift = max(np.abs(st.h + b - 1.0).max(), np.abs(st.hu).max(), np.abs(st.hv).max())
+    assert drift < 1e-11
+
+
+@pytest.mark.parametrize("sid,kx,deg", [("oscillating_lake", 12, 4), ("wetdry_dambreak", 10, 3),
+                                        ("parabolic_dam_dry", 8, 3), ("three_mound", 10, 2)])
+def test_fast_one_stage(sid, kx, deg):
+    """The north_star bar: one stage (W + dt R(W)) within 1e-12 normwise."""
+    m, st = ref.scenario_mesh(sid, kx, kx, deg)
+    p, cfg = scenario_params(sid, deg, visc_enabled=0.0)
+    dt = ref.compute_dt(m, p, st, cfg["cfl"])
+    r_ref = ref.assemble_rhs(m, p, st)
+    r_gpu = swdg.TimeIntegrator(m, cfg_from(p)).assemble_rhs(S(st)).arrays()
+    want = [a + dt * r for a, r in zip(st, r_ref)]
+    got = [a + dt * r for a, r in zip(st, r_gpu)]
+    assert normwise(got, want) <= TOL_STAGE
+    assert normwise(r_gpu, r_ref) <= TOL_STAGE
+
+
+@pytest.mark.parametrize("sid,kx,deg,tol", [("oscillating_lake", 12, 4, 1e-10),
+                                            ("wetdry_dambreak", 10, 3, 1e-10),
+                                            ("parabolic_dam_dry", 8, 3, 1e-10),
+                                            ("three_mound", 10, 2, 1e-10)])
+def test_fast_one_step(sid, kx, deg, tol):
+    """One SSPRK3 step (3 stages, limiter, dry-node cut) from identical inputs: the
+    wet/dry thresholds amplify ulps, so the bar is 1e-10."""
+    m, st = ref.scenario_mesh(sid, kx, kx, deg)
+    p, cfg = scenario_params(sid, deg, visc_enabled=0.0)
+    ri = ref.Integrator(m, p)
+    gi = swdg.TimeIntegrator(m, cfg_from(p))
+    s1 = [a.copy() for a in st]
+    dt = ref.compute_dt(m, p, s1, cfg["cfl"])
+    for k in range(3):
+        s2 = S(s1)
+        a = ri.try_step(s1, k * dt, dt)
+        assert gi.try_step(s2, k * dt, dt) == bool(a.accepted)
+        assert normwise(s2.arrays(), s1) <= tol
+        s1 = [x.copy() for x in s2.arrays()]  # restart both from the same state
+
+
+def test_run_steps_matches_try_step():
+    m = build("wavy_N4")
+    p = ref.params(g=9.81)
+    a = swdg.TimeIntegrator(m, cfg_from(p))
+    b = swdg.TimeIntegrator(m, cfg_from(p))
+    s = smooth_state(m, 0.1)
+    sa, sb = S(s), S(s)
+    dt = a.compute_dt(sa, 0.5)
+    for k in range(4):
+        assert a.try_step(sa, k * dt, dt)
+    b.upload(sb)
+    b.run_steps(4, 0.0, dt)
+    assert b.last_info().accepted
+    b.download(sb)
+    for x, y in zip(sa.arrays(), sb.arrays()):
+        assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("kind,N,bathy", [("wavy", 4, ("smooth",)), ("curved_dam", 3, ("step", 0.0, 0.3, 0.1)),
+                                          ("cartesian", 7, ("paraboloid", 0.1))])
+def test_device_mesh_generator(kind, N, bathy):
+    kx, ky = 6, 5
+    extra = {"wavy": dict(periodic_x=True, periodic_y=True)}.get(kind, {})
+    m = ref.build_mesh(kind, N, kx, ky, **extra).bathymetry(*bathy)
+    spec = swdg.structured_spec(kind, N, kx, ky, bathy=bathy[0], bathy_params=bathy[1:], **extra)
+    integ = swdg.TimeIntegrator.structured(spec, swdg.RunConfig(mode=swdg.MODE_FAST))
+    for k in ("x", "y", "x_xi", "x_eta", "y_xi", "y_eta", "jac", "face_nx", "face_ny",
+              "face_jsurf", "face_a"):
+        got, want = integ.geometry(k), m.arrays[k]
+        assert np.abs(got - want).max() <= 1e-13 * max(1.0, np.abs(want).max()), k
+    got_b = integ.geometry("b")
+    if bathy[0] == "step":  # a step: nodes within rounding of x=0 may flip sides
+        assert np.mean(got_b == m.arrays["b"]) > 0.999
+    else:
+        assert np.abs(got_b - m.arrays["b"]).max() <= 1e-13
