@@ -1,30 +1,44 @@
-// kernels_fast.cu — the throughput path (SWDG_MODE_FAST): one fused kernel per
-// SSPRK3 stage on sm_100a, FP64 with FMA.
+// kernels_fast.cu — the throughput path (SWDG_MODE_FAST): one fused, persistent
+// kernel per SSPRK3 stage on sm_100a, FP64 with FMA.
 //
-// Mapping: a CTA holds E elements; every element gets 2*(N+1) "line threads":
-// thread l < N+1 owns the xi-line j=l, thread l >= N+1 the eta-line i=l-(N+1).
-// A line thread keeps its line's nodal data and accumulators in registers and
-// runs the split-form flux differencing (dg_rhs.hpp:23-71) over the UNORDERED
-// node pairs of its line: the two-point flux F#(a,b) and the averaged metrics
-// are symmetric, so each pair is evaluated once and scattered
-// to both nodes with Dtilde(a,b) and Dtilde(b,a) — 19 DP instructions per
-// pair instead of 2x16.  The same thread then adds its share of the split
-// bathymetry source (dg_rhs.hpp:154-183: the xi or eta half) and the
-// entropy-stable interface flux (fluxes.hpp:136-166) at its two line
-// endpoints, which are exactly the element's face nodes.  After one barrier
-// the node phase sums the xi/eta accumulators, applies -1/J, the SSPRK3
-// update (timeloop.hpp:114-127), the element mean / Zhang-Shu limiter /
-// dry-node zeroing (limiter.hpp:24-84) and the reject signal
-// (timeloop.hpp:205-209), and writes the stage output once.  HBM traffic per
-// node and stage: state in (24 B), W^n (24 B, stages 2-3), 6 geometry fields
-// (48 B), state out (24 B) — face traces of neighbours are L2 hits.
+// Work decomposition.  Elements are processed in groups of E consecutive
+// elements; a CTA owns 2*(N+1) "line threads" per element of its group:
+// thread l < N+1 owns the xi-line j=l, thread l >= N+1 the eta-line
+// i=l-(N+1).  A line thread keeps its line's nodal data and accumulators in
+// registers and runs the split-form flux differencing (dg_rhs.hpp:23-71) over
+// the UNORDERED node pairs of its line: the two-point flux F#(a,b) and the
+// averaged metrics are symmetric, so each pair is evaluated
+// once and scattered to both nodes with Dtilde(a,b), Dtilde(b,a) — 19 DP
+// instructions per pair instead of 2x16.  The same thread adds its half of the
+// split bathymetry source (dg_rhs.hpp:154-183) and the entropy-stable
+// interface flux (fluxes.hpp:136-166) at its two endpoints, which are exactly
+// the element's face nodes.  The eta-line threads then finish their nodes:
+// -1/J, forcing, the SSPRK3 update (timeloop.hpp:114-127), the element mean,
+// Zhang-Shu limiter and dry-node cut (limiter.hpp:24-84) and the reject
+// signal (timeloop.hpp:205-209); the stage output is written once.
 //
-// Operators live in __constant__ memory, one table set per N, so the fully
-// unrolled pair loops issue DFMA with constant-bank operands.
+// Memory pipeline.  CTAs are persistent (grid = resident CTAs) and loop over
+// groups.  While group g is computed, the TMA engine streams group g+1's
+// line data (state + metrics + b + face connectivity) into shared memory with
+// cp.async.bulk (one instruction per field per group, completion on an
+// mbarrier), and group g's node-phase data (J, W^n) arrives the same way
+// behind the line phase.  Neighbour face traces are scattered 8-byte reads;
+// they are issued as cp.async (LDGSTS) right after the line data lands and
+// consumed after the volume loop, so their L2 latency hides behind it.
+//
+// Conservation: both sides of a face evaluate the same flux bitwise — the
+// minus side's normal/J_surf are computed from the minus element's face
+// metrics with explicit round-to-nearest intrinsics on both sides, and the
+// flux is evaluated at a single call site with the (minus, plus) ordering.
+//
+// HBM traffic per node and stage: state in 24 B, W^n 24 B (stages 2-3),
+// metrics + J + b 48 B, state out 24 B; neighbour traces are L2 hits.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 
+#include "ptx_async.cuh"
 #include "swdg_device.cuh"
 #include "swdg_launch.h"
 
@@ -76,6 +90,17 @@ __device__ __forceinline__ void vel(double h, double hu, double hv, double h_des
   }
 }
 
+// Minus-side outward normal and J_surf from the face metrics (compute_metrics,
+// mesh.hpp:192-218): E/W faces take (y_eta, x_eta), S/N faces (y_xi, x_xi).
+// Explicit _rn intrinsics: bitwise the same on both sides of the face.
+__device__ __forceinline__ void face_normal(int face, double m0, double m1, double& nx,
+                                            double& ny, double& js) {
+  js = __dsqrt_rn(__fma_rn(m0, m0, __dmul_rn(m1, m1)));
+  const double s = (face == 1 || face == 0) ? 1.0 : -1.0;  // E,S: +(m0,-m1); W,N: -(m0,-m1)
+  nx = __ddiv_rn(s * m0, js);
+  ny = __ddiv_rn(-s * m1, js);
+}
+
 // entropy-stable normal flux (fluxes.hpp:136-166), algebraically simplified:
 // R|Lambda|R^T applied directly (the zero/one entries of R dropped).
 __device__ __forceinline__ void es_flux_fast(double hm, double hum, double hvm, double hp,
@@ -111,82 +136,152 @@ __device__ __forceinline__ void es_flux_fast(double hm, double hum, double hvm, 
   f2 = ny * a1 + nx * a2;
 }
 
-// shared-memory slots per element: 10 nodal fields + 6 accumulators + 8 per
-// line thread for the element reductions
+// ---- shared-memory plan (in doubles) ---------------------------------------
 template <int N1>
-struct Smem {
+struct Plan {
   static constexpr int NP = N1 * N1;
-  static constexpr int H = 0, U = 1, V = 2, HU = 3, HV = 4, YE = 5, XE = 6, YX = 7, XX = 8,
-                       B = 9, AX = 10, AY = 13;
-  static constexpr int kFields = 16;
-  static constexpr int kRed = 8;
-  static constexpr int per_elem = kFields * NP + kRed * 2 * N1;
+  static constexpr int T = 2 * N1;  // threads per element
+  static constexpr int E = ((128 / T) & ~1) > 2 ? ((128 / T) & ~1) : 2;  // even
+  static constexpr int THREADS = T * E;
+  static constexpr int GNP = (E * NP + 1) & ~1;  // 16-byte aligned field stride
+  enum { F_H, F_HU, F_HV, F_YE, F_XE, F_YX, F_XX, F_B, kLineFields };
+  enum { N_JAC, N_WH, N_WHU, N_WHV, kNodeFields };
+  static constexpr int LINE = 0;
+  static constexpr int NODE = LINE + kLineFields * GNP;
+  static constexpr int ACC = NODE + kNodeFields * GNP;
+  static constexpr int TR = ACC + 3 * GNP;         // [E][4][N1][8] neighbour traces
+  static constexpr int EFO = TR + E * 4 * N1 * 8;  // int4 [E][4] = 2 doubles each
+  static constexpr int RED = EFO + E * 4 * 2;      // [E][T][6]
+  static constexpr int BAR = RED + E * T * 6;      // 2 mbarriers
+  static constexpr int TOTAL = BAR + 2;
+  static constexpr size_t bytes = TOTAL * sizeof(double);
 };
 
+__device__ __forceinline__ uint32_t round16(size_t b) { return (uint32_t)((b + 15) & ~size_t(15)); }
+
+// thread 0: stream one group's line data (8 fields + face connectivity)
 template <int N1>
-constexpr int elems_per_block() {
-  return (128 / (2 * N1)) > 0 ? (128 / (2 * N1)) : 1;
+__device__ __forceinline__ void issue_line(double* sm, const Mesh& M, const CState& in, int g,
+                                           uint64_t* bar) {
+  using P = Plan<N1>;
+  const int e0 = g * P::E, ne = min(P::E, M.n_owned - e0);
+  const uint32_t fb = round16((size_t)ne * P::NP * sizeof(double));
+  const uint32_t eb = (uint32_t)(ne * 4 * sizeof(int4));
+  mbar_expect_tx(bar, P::kLineFields * fb + eb);
+  const long long off = (long long)e0 * P::NP;
+  const double* src[P::kLineFields] = {in.h, in.hu, in.hv, M.ye, M.xe, M.yx, M.xx, M.b};
+#pragma unroll
+  for (int f = 0; f < P::kLineFields; ++f)
+    bulk_g2s(sm + P::LINE + f * P::GNP, src[f] + off, fb, bar);
+  bulk_g2s(sm + P::EFO, M.ef + (long long)e0 * 4, eb, bar);
 }
 
-// One RK stage for N1 <= 8 (a whole line in registers).
-template <int N1, bool FORCE>
-__global__ void __launch_bounds__(2 * N1 * elems_per_block<N1>())
-    k_stage_lines(Mesh M, Phys P, StageArgs A, Flags* F) {
-  constexpr int NP = N1 * N1, T = 2 * N1, E = elems_per_block<N1>();
-  using S = Smem<N1>;
-  using O = Ops<N1>;
-  extern __shared__ double smem[];
-  const int el = threadIdx.x / T, lt = threadIdx.x % T;
-  const int e = blockIdx.x * E + el;
-  const bool active = e < M.n_owned;
-  double* sm = smem + el * S::per_elem;
-  const long long base = (long long)e * NP;
-  const double g = P.g, h_des = P.h_des;
+// thread 0: stream one group's node-phase data (J and, for stages 2-3, W^n)
+template <int N1>
+__device__ __forceinline__ void issue_node(double* sm, const Mesh& M, const StageArgs& A, int g,
+                                           uint64_t* bar) {
+  using P = Plan<N1>;
+  const int e0 = g * P::E, ne = min(P::E, M.n_owned - e0);
+  const uint32_t fb = round16((size_t)ne * P::NP * sizeof(double));
+  const bool wn = A.update && A.stage > 0;
+  mbar_expect_tx(bar, (wn ? 4 : 1) * fb);
+  const long long off = (long long)e0 * P::NP;
+  bulk_g2s(sm + P::NODE + P::N_JAC * P::GNP, M.jac + off, fb, bar);
+  if (wn) {
+    bulk_g2s(sm + P::NODE + P::N_WH * P::GNP, A.wn.h + off, fb, bar);
+    bulk_g2s(sm + P::NODE + P::N_WHU * P::GNP, A.wn.hu + off, fb, bar);
+    bulk_g2s(sm + P::NODE + P::N_WHV * P::GNP, A.wn.hv + off, fb, bar);
+  }
+}
 
-  // ---- load phase: element fields -> smem (coalesced across the element)
-  if (active) {
-#pragma unroll 4
-    for (int k = lt; k < NP; k += T) {
-      const long long n = base + k;
-      const double h = A.in.h[n], hu = A.in.hu[n], hv = A.in.hv[n];
-      double u, v;
-      vel(h, hu, hv, h_des, u, v);
-      sm[S::H * NP + k] = h;
-      sm[S::U * NP + k] = u;
-      sm[S::V * NP + k] = v;
-      sm[S::HU * NP + k] = hu;
-      sm[S::HV * NP + k] = hv;
-      sm[S::YE * NP + k] = M.ye[n];
-      sm[S::XE * NP + k] = M.xe[n];
-      sm[S::YX * NP + k] = M.yx[n];
-      sm[S::XX * NP + k] = M.xx[n];
-      sm[S::B * NP + k] = M.b[n];
-    }
+template <int N1, bool FORCE>
+__global__ void __launch_bounds__(Plan<N1>::THREADS, 1)
+    k_stage(Mesh M, Phys Ph, StageArgs A, Flags* F) {
+  using P = Plan<N1>;
+  using O = Ops<N1>;
+  constexpr int NP = P::NP, T = P::T, E = P::E;
+  extern __shared__ __align__(16) double sm[];
+  uint64_t* bar_line = reinterpret_cast<uint64_t*>(sm + P::BAR);
+  uint64_t* bar_node = bar_line + 1;
+  const int tid = threadIdx.x, el = tid / T, lt = tid % T;
+  const bool xi = lt < N1;
+  const int li = xi ? lt : lt - N1;
+  const int ngroups = (M.n_owned + E - 1) / E;
+  const double g = Ph.g, h_des = Ph.h_des, inv2g = 1.0 / (2.0 * g), iw0 = 1.0 / M.w0;
+
+  if (tid == 0) {
+    mbar_init(bar_line, 1);
+    mbar_init(bar_node, 1);
+    fence_mbar_init();
   }
   __syncthreads();
+  if ((int)blockIdx.x >= ngroups) return;  // uniform across the CTA
+  if (tid == 0) issue_line<N1>(sm, M, A.in, blockIdx.x, bar_line);
+  uint32_t ph_line = 0, ph_node = 0;
 
-  // ---- line phase
-  if (active) {
-    const bool xi = lt < N1;
-    const int li = xi ? lt : lt - N1;
-    // node k of this line: xi-line j=li -> (k, li); eta-line i=li -> (li, k)
-    auto idx = [&](int k) { return xi ? k * N1 + li : li * N1 + k; };
-    double h[N1], u[N1], v[N1], hu[N1], hv[N1], Am[N1], Bm[N1];
+  // node k of this thread's line inside the element: xi-line j=li -> (k,li),
+  // eta-line i=li -> (li,k)
+  auto idx = [&](int k) { return xi ? k * N1 + li : li * N1 + k; };
+
+  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    const int e0 = grp * E, ne = min(E, M.n_owned - e0);
+    const bool active = el < ne;
+    const int e = e0 + el;
+    mbar_wait(bar_line, ph_line);
+    ph_line ^= 1;
+
+    // ---- line data -> registers; gathers for the two endpoints
+    double h[N1], u[N1], v[N1], hu[N1], hv[N1], Am[N1], Bm[N1], bb[N1];
     double r0[N1], r1[N1], r2[N1];
+    int efy[2] = {0, 0};
+    const double* L = sm + P::LINE + el * NP;
 #pragma unroll
     for (int k = 0; k < N1; ++k) {
       const int q = idx(k);
-      h[k] = sm[S::H * NP + q];
-      u[k] = sm[S::U * NP + q];
-      v[k] = sm[S::V * NP + q];
-      hu[k] = sm[S::HU * NP + q];
-      hv[k] = sm[S::HV * NP + q];
-      Am[k] = xi ? sm[S::YE * NP + q] : -sm[S::YX * NP + q];
-      Bm[k] = xi ? sm[S::XE * NP + q] : -sm[S::XX * NP + q];
+      h[k] = L[P::F_H * P::GNP + q];
+      hu[k] = L[P::F_HU * P::GNP + q];
+      hv[k] = L[P::F_HV * P::GNP + q];
+      Am[k] = xi ? L[P::F_YE * P::GNP + q] : -L[P::F_YX * P::GNP + q];
+      Bm[k] = xi ? L[P::F_XE * P::GNP + q] : -L[P::F_XX * P::GNP + q];
+      bb[k] = L[P::F_B * P::GNP + q];
       r0[k] = r1[k] = r2[k] = 0.0;
     }
+    if (active) {
+      const int4* ef4 = reinterpret_cast<const int4*>(sm + P::EFO) + el * 4;
+#pragma unroll
+      for (int end = 0; end < 2; ++end) {
+        const int face = xi ? (end ? 1 : 3) : (end ? 2 : 0);
+        const int4 ef = ef4[face];
+        efy[end] = ef.y;
+        if ((ef.y & EF_PRESENT) && !(ef.y & EF_WALL)) {
+          const int nf = ef.y & EF_NBR_FACE_MASK;
+          const int tp = (ef.y & EF_REVERSED) ? N1 - 1 - li : li;
+          const long long nb = (long long)ef.x * NP + face_node(N1, nf, tp);
+          double* tr = sm + P::TR + ((el * 4 + face) * N1 + li) * 8;
+          cp_async8(tr + 0, A.in.h + nb);
+          cp_async8(tr + 1, A.in.hu + nb);
+          cp_async8(tr + 2, A.in.hv + nb);
+          cp_async8(tr + 3, M.b + nb);
+          if (!(ef.y & EF_MINUS)) {  // plus side: the minus side's face metrics
+            const bool ew = nf == 1 || nf == 3;
+            cp_async8(tr + 4, (ew ? M.ye : M.yx) + nb);
+            cp_async8(tr + 5, (ew ? M.xe : M.xx) + nb);
+          }
+        }
+      }
+    }
+    cp_async_commit();
+    __syncthreads();  // line buffer and connectivity consumed
+    if (tid == 0) {
+      const int gn = grp + gridDim.x;
+      if (gn < ngroups) issue_line<N1>(sm, M, A.in, gn, bar_line);
+      issue_node<N1>(sm, M, A, grp, bar_node);
+    }
+#pragma unroll
+    for (int k = 0; k < N1; ++k) vel(h[k], hu[k], hv[k], h_des, u[k], v[k]);
+
+    // ---- volume: unordered pairs (a<b) plus the two corner diagonals
     const double g2 = 2.0 * g;
-    // volume: unordered pairs (a<b) plus the two corner diagonals
 #pragma unroll
     for (int a = 0; a < N1; ++a) {
 #pragma unroll
@@ -195,10 +290,10 @@ __global__ void __launch_bounds__(2 * N1 * elems_per_block<N1>())
         const double Shu = hu[a] + hu[b], Shv = hv[a] + hv[b];
         const double Su = u[a] + u[b], Sv = v[a] + v[b];
         const double SA = Am[a] + Am[b], SB = Bm[a] + Bm[b];
-        const double F0 = SA * Shu - SB * Shv;  // 4*Ftilde_0
+        const double F0 = SA * Shu - SB * Shv;  // 4 Ftilde_0
         const double Q = g2 * h[a] * h[b];
-        const double T1 = Su * F0 + Q * SA;     // 8*Ftilde_1
-        const double T2 = Sv * F0 - Q * SB;     // 8*Ftilde_2
+        const double T1 = Su * F0 + Q * SA;     // 8 Ftilde_1
+        const double T2 = Sv * F0 - Q * SB;     // 8 Ftilde_2
         r0[a] += O::D4(a, b) * F0;
         r1[a] += O::D8(a, b) * T1;
         r2[a] += O::D8(a, b) * T2;
@@ -209,192 +304,746 @@ __global__ void __launch_bounds__(2 * N1 * elems_per_block<N1>())
         }
       }
     }
-    // split bathymetry source, this direction's half (dg_rhs.hpp:171-176)
-    {
-      double bb[N1];
-#pragma unroll
-      for (int k = 0; k < N1; ++k) bb[k] = sm[S::B * NP + idx(k)];
-#pragma unroll
-      for (int k = 0; k < N1; ++k) {
-        double db = 0.0, dAb = 0.0, dBb = 0.0;
-#pragma unroll
-        for (int m = 0; m < N1; ++m) {
-          const double d = O::D(k, m);
-          db += d * bb[m];
-          dAb += d * (Am[m] * bb[m]);
-          dBb += d * (Bm[m] * bb[m]);
-        }
-        const double hg2 = 0.5 * g * h[k];
-        r1[k] += hg2 * (Am[k] * db + dAb);
-        r2[k] -= hg2 * (Bm[k] * db + dBb);
-      }
-    }
-    // interface fluxes at the two line endpoints (dg_rhs.hpp:202-252)
-    const double inv2g = 1.0 / (2.0 * g), iw0 = 1.0 / M.w0;
-#pragma unroll
-    for (int end = 0; end < 2; ++end) {
-      const int k = end ? N1 - 1 : 0;
-      const int face = xi ? (end ? 1 : 3) : (end ? 2 : 0);
-      const int t = li;
-      const int4 ef = M.ef[e * 4 + face];
-      if (!(ef.y & EF_PRESENT)) continue;
-      const double hm = h[k], hum = hu[k], hvm = hv[k], bo = sm[S::B * NP + idx(k)];
-      double f0, f1, f2, js, sgn;
-      if (ef.y & EF_WALL) {
-        const long long fi = ((long long)e * 4 + face) * N1 + t;
-        const double nx = M.fnx[fi], ny = M.fny[fi];
-        js = M.fjs[fi];
-        const double mn = hum * nx + hvm * ny;
-        es_flux_fast(hm, hum, hvm, hm, hum - 2.0 * mn * nx, hvm - 2.0 * mn * ny, bo, bo, nx,
-                     ny, g, inv2g, h_des, f0, f1, f2);
-        sgn = 1.0;
-      } else {
-        const int nf = ef.y & EF_NBR_FACE_MASK;
-        const int tp = (ef.y & EF_REVERSED) ? N1 - 1 - t : t;
-        const long long nb = (long long)ef.x * NP + face_node(N1, nf, tp);
-        const double hn = A.in.h[nb], hun = A.in.hu[nb], hvn = A.in.hv[nb], bn = M.b[nb];
-        if (ef.y & EF_MINUS) {
-          const long long fi = ((long long)e * 4 + face) * N1 + t;
-          const double nx = M.fnx[fi], ny = M.fny[fi];
-          js = M.fjs[fi];
-          es_flux_fast(hm, hum, hvm, hn, hun, hvn, bo, bn, nx, ny, g, inv2g, h_des, f0, f1, f2);
-          sgn = 1.0;
-        } else {
-          const long long fi = ((long long)ef.x * 4 + nf) * N1 + tp;
-          const double nx = M.fnx[fi], ny = M.fny[fi];
-          js = M.fjs[fi];
-          es_flux_fast(hn, hun, hvn, hm, hum, hvm, bn, bo, nx, ny, g, inv2g, h_des, f0, f1, f2);
-          sgn = -1.0;
-        }
-      }
-      const double c = sgn * js * iw0;
-      r0[k] += c * f0;
-      r1[k] += c * f1;
-      r2[k] += c * f2;
-    }
-    // publish this line's accumulators
-    const int acc = xi ? S::AX : S::AY;
+    // ---- split bathymetry source, this direction's half (dg_rhs.hpp:171-176)
 #pragma unroll
     for (int k = 0; k < N1; ++k) {
-      const int q = idx(k);
-      sm[(acc + 0) * NP + q] = r0[k];
-      sm[(acc + 1) * NP + q] = r1[k];
-      sm[(acc + 2) * NP + q] = r2[k];
-    }
-  }
-  __syncthreads();
-
-  // ---- node phase: dW/dt, SSPRK3 update, element mean
-  double* red = sm + S::kFields * NP + lt * S::kRed;
-  if (active) {
-    double s_area = 0.0, s0 = 0.0, s1 = 0.0, s2 = 0.0, mmin = 1.0e300;
-#pragma unroll 2
-    for (int k = lt; k < NP; k += T) {
-      const long long n = base + k;
-      const double jac = M.jac[n];
-      const double ij = -1.0 / jac;
-      double rh = (sm[S::AX * NP + k] + sm[S::AY * NP + k]) * ij;
-      double rhu = (sm[(S::AX + 1) * NP + k] + sm[(S::AY + 1) * NP + k]) * ij;
-      double rhv = (sm[(S::AX + 2) * NP + k] + sm[(S::AY + 2) * NP + k]) * ij;
-      if (FORCE) {
-        rh += A.fh[n];
-        rhu += A.fhu[n];
-        rhv += A.fhv[n];
-      }
-      if (A.rhs.h) {
-        A.rhs.h[n] = rh;
-        A.rhs.hu[n] = rhu;
-        A.rhs.hv[n] = rhv;
-      }
-      double sh = sm[S::H * NP + k] + A.dt * rh;
-      double shu = sm[S::HU * NP + k] + A.dt * rhu;
-      double shv = sm[S::HV * NP + k] + A.dt * rhv;
-      if (A.stage > 0) {
-        sh = A.ca * A.wn.h[n] + A.cb * sh;
-        shu = A.ca * A.wn.hu[n] + A.cb * shu;
-        shv = A.ca * A.wn.hv[n] + A.cb * shv;
-      }
-      sm[S::H * NP + k] = sh;
-      sm[S::HU * NP + k] = shu;
-      sm[S::HV * NP + k] = shv;
-      const int i = k / N1, j = k % N1;
-      const double wj = O::w(i) * O::w(j) * jac;
-      s_area += wj;
-      s0 += wj * sh;
-      s1 += wj * shu;
-      s2 += wj * shv;
-      mmin = smin(mmin, sh);
-    }
-    red[0] = s_area;
-    red[1] = s0;
-    red[2] = s1;
-    red[3] = s2;
-    red[4] = mmin;
-  }
-  __syncthreads();
-
-  // ---- limiter (limit_element, limiter.hpp:43-84) and write-out.  No early
-  // returns before the last barrier: every thread of the block reaches it.
-  bool lim = active && A.update;
-  double area = 0.0, a0 = 0.0, a1 = 0.0, a2 = 0.0, mmin = 1.0e300;
-  const double* red0 = sm + S::kFields * NP;
-  if (lim) {
+      double db = 0.0, dAb = 0.0, dBb = 0.0;
 #pragma unroll
-    for (int q = 0; q < T; ++q) {
-      area += red0[q * S::kRed + 0];
-      a0 += red0[q * S::kRed + 1];
-      a1 += red0[q * S::kRed + 2];
-      a2 += red0[q * S::kRed + 3];
-      mmin = smin(mmin, red0[q * S::kRed + 4]);
-    }
-  }
-  const double inv = 1.0 / area;
-  const double avg0 = inv * a0, avg1 = inv * a1, avg2 = inv * a2;
-  if (lim && avg0 < 0.0) {
-    if (lt == 0) {
-      atomicExch(&F->reject, 1);
-      if (!P.limiter) atomicExch(&F->abort, 1);
-    }
-    lim = false;
-  }
-  double theta = 1.0;
-  if (lim && P.limiter && mmin < 0.0) {
-    const double denom = avg0 - mmin;
-    theta = denom < 1e-14 ? 1.0 : smin(1.0, avg0 / denom);
-  }
-  if (lim && !P.limiter && mmin < 0.0 && lt == 0) atomicExch(&F->abort, 1);
-  double mine = 1.0e300;
-  if (lim) {
-    for (int k = lt; k < NP; k += T) {
-      const long long n = base + k;
-      double sh = sm[S::H * NP + k], shu = sm[S::HU * NP + k], shv = sm[S::HV * NP + k];
-      if (theta < 1.0) {
-        sh = smax(theta * (sh - avg0) + avg0, 0.0);
-        shu = theta * (shu - avg1) + avg1;
-        shv = theta * (shv - avg2) + avg2;
+      for (int m = 0; m < N1; ++m) {
+        const double d = O::D(k, m);
+        db += d * bb[m];
+        dAb += d * (Am[m] * bb[m]);
+        dBb += d * (Bm[m] * bb[m]);
       }
-      if (P.limiter && sh < P.h_tol) {
-        shu = 0.0;
-        shv = 0.0;
-      }
-      A.out.h[n] = sh;
-      A.out.hu[n] = shu;
-      A.out.hv[n] = shv;
-      mine = smin(mine, sh);
+      const double hg2 = 0.5 * g * h[k];
+      r1[k] += hg2 * (Am[k] * db + dAb);
+      r2[k] -= hg2 * (Bm[k] * db + dBb);
     }
-  }
-  red[5] = mine;
-  __syncthreads();
-  // per-element min and limited count, one atomic per element
-  if (lim && lt == 0) {
-    double m = red0[5];
-    for (int q = 1; q < T; ++q) m = smin(m, red0[q * S::kRed + 5]);
-    atomicMin(&F->min_h_key, order_key(m));
-    if (theta < 1.0) atomicAdd(&F->n_limited, 1);
+
+    // ---- interface fluxes at the two endpoints (dg_rhs.hpp:202-252)
+    cp_async_wait_all();
+    if (active) {
+#pragma unroll
+      for (int end = 0; end < 2; ++end) {
+        const int k = end ? N1 - 1 : 0;
+        const int face = xi ? (end ? 1 : 3) : (end ? 2 : 0);
+        const int fy = efy[end];
+        if (!(fy & EF_PRESENT)) continue;
+        const double* tr = sm + P::TR + ((el * 4 + face) * N1 + li) * 8;
+        // own face metrics: xi-lines (y_eta,x_eta) = (A,B); eta-lines (y_xi,x_xi) = -(A,B)
+        const double om0 = xi ? Am[k] : -Am[k], om1 = xi ? Bm[k] : -Bm[k];
+        double wm0, wm1, wm2, wp0, wp1, wp2, bm, bp, nx, ny, js;
+        double sgn = 1.0;
+        if (fy & EF_MINUS) {
+          face_normal(face, om0, om1, nx, ny, js);
+          wm0 = h[k];
+          wm1 = hu[k];
+          wm2 = hv[k];
+          bm = bb[k];
+          if (fy & EF_WALL) {  // exterior_state (mesh.hpp:382-386)
+            const double mn = wm1 * nx + wm2 * ny;
+            wp0 = wm0;
+            wp1 = wm1 - 2.0 * mn * nx;
+            wp2 = wm2 - 2.0 * mn * ny;
+            bp = bm;
+          } else {
+            wp0 = tr[0];
+            wp1 = tr[1];
+            wp2 = tr[2];
+            bp = tr[3];
+          }
+        } else {
+          face_normal(fy & EF_NBR_FACE_MASK, tr[4], tr[5], nx, ny, js);
+          wm0 = tr[0];
+          wm1 = tr[1];
+          wm2 = tr[2];
+          bm = tr[3];
+          wp0 = h[k];
+          wp1 = hu[k];
+          wp2 = hv[k];
+          bp = bb[k];
+          sgn = -1.0;
+        }
+        double f0, f1, f2;
+        es_flux_fast(wm0, wm1, wm2, wp0, wp1, wp2, bm, bp, nx, ny, g, inv2g, h_des, f0, f1, f2);
+        const double c = sgn * js * iw0;
+        r0[k] += c * f0;
+        r1[k] += c * f1;
+        r2[k] += c * f2;
+      }
+    }
+    // xi-lines hand their accumulators to the eta-line owners of the nodes
+    if (xi) {
+#pragma unroll
+      for (int k = 0; k < N1; ++k) {
+        const int q = el * NP + idx(k);
+        sm[P::ACC + 0 * P::GNP + q] = r0[k];
+        sm[P::ACC + 1 * P::GNP + q] = r1[k];
+        sm[P::ACC + 2 * P::GNP + q] = r2[k];
+      }
+    }
+    __syncthreads();
+    mbar_wait(bar_node, ph_node);
+    ph_node ^= 1;
+
+    // ---- node phase on the eta-line threads: node (li, k), k = 0..N
+    double* red = sm + P::RED + (el * T + lt) * 6;
+    const double* Nd = sm + P::NODE + el * NP;
+    if (!xi && active) {
+      double s_area = 0.0, s0 = 0.0, s1 = 0.0, s2 = 0.0, mmin = 1.0e300;
+      const double wi = O::w(li);
+#pragma unroll
+      for (int k = 0; k < N1; ++k) {
+        const int q = idx(k);
+        const long long n = (long long)e * NP + q;
+        const double jac = Nd[P::N_JAC * P::GNP + q];
+        const double ij = -1.0 / jac;
+        double rh = (sm[P::ACC + 0 * P::GNP + el * NP + q] + r0[k]) * ij;
+        double rhu = (sm[P::ACC + 1 * P::GNP + el * NP + q] + r1[k]) * ij;
+        double rhv = (sm[P::ACC + 2 * P::GNP + el * NP + q] + r2[k]) * ij;
+        if (FORCE) {
+          rh += A.fh[n];
+          rhu += A.fhu[n];
+          rhv += A.fhv[n];
+        }
+        if (A.rhs.h) {
+          A.rhs.h[n] = rh;
+          A.rhs.hu[n] = rhu;
+          A.rhs.hv[n] = rhv;
+        }
+        double sh = h[k] + A.dt * rh;
+        double shu = hu[k] + A.dt * rhu;
+        double shv = hv[k] + A.dt * rhv;
+        if (A.stage > 0 && A.update) {
+          sh = A.ca * Nd[P::N_WH * P::GNP + q] + A.cb * sh;
+          shu = A.ca * Nd[P::N_WHU * P::GNP + q] + A.cb * shu;
+          shv = A.ca * Nd[P::N_WHV * P::GNP + q] + A.cb * shv;
+        }
+        h[k] = sh;
+        hu[k] = shu;
+        hv[k] = shv;
+        const double wj = wi * O::w(k) * jac;
+        s_area += wj;
+        s0 += wj * sh;
+        s1 += wj * shu;
+        s2 += wj * shv;
+        mmin = smin(mmin, sh);
+      }
+      red[0] = s_area;
+      red[1] = s0;
+      red[2] = s1;
+      red[3] = s2;
+      red[4] = mmin;
+    }
+    __syncthreads();
+
+    // ---- limiter (limit_element, limiter.hpp:43-84) and write-out
+    bool lim = active && A.update;
+    double area = 0.0, a0 = 0.0, a1 = 0.0, a2 = 0.0, mmin = 1.0e300;
+    const double* red0 = sm + P::RED + el * T * 6;
+    if (lim) {
+#pragma unroll
+      for (int q = N1; q < T; ++q) {
+        area += red0[q * 6 + 0];
+        a0 += red0[q * 6 + 1];
+        a1 += red0[q * 6 + 2];
+        a2 += red0[q * 6 + 3];
+        mmin = smin(mmin, red0[q * 6 + 4]);
+      }
+    }
+    const double inv = 1.0 / area;
+    const double avg0 = inv * a0, avg1 = inv * a1, avg2 = inv * a2;
+    if (lim && avg0 < 0.0) {
+      if (lt == 0) {
+        atomicExch(&F->reject, 1);
+        if (!Ph.limiter) atomicExch(&F->abort, 1);
+      }
+      lim = false;
+    }
+    double theta = 1.0;
+    if (lim && Ph.limiter && mmin < 0.0) {
+      const double denom = avg0 - mmin;
+      theta = denom < 1e-14 ? 1.0 : smin(1.0, avg0 / denom);
+    }
+    if (lim && !Ph.limiter && mmin < 0.0 && lt == 0) atomicExch(&F->abort, 1);
+    double mine = 1.0e300;
+    if (lim && !xi) {
+      const long long nb0 = (long long)e * NP + li * N1;
+#pragma unroll
+      for (int k = 0; k < N1; ++k) {
+        double sh = h[k], shu = hu[k], shv = hv[k];
+        if (theta < 1.0) {
+          sh = smax(theta * (sh - avg0) + avg0, 0.0);
+          shu = theta * (shu - avg1) + avg1;
+          shv = theta * (shv - avg2) + avg2;
+        }
+        if (Ph.limiter && sh < Ph.h_tol) {
+          shu = 0.0;
+          shv = 0.0;
+        }
+        A.out.h[nb0 + k] = sh;
+        A.out.hu[nb0 + k] = shu;
+        A.out.hv[nb0 + k] = shv;
+        mine = smin(mine, sh);
+      }
+    }
+    red[5] = mine;
+    __syncthreads();
+    if (lim && lt == 0) {
+      double m = red0[N1 * 6 + 5];
+      for (int q = N1 + 1; q < T; ++q) m = smin(m, red0[q * 6 + 5]);
+      atomicMin(&F->min_h_key, order_key(m));
+      if (theta < 1.0) atomicAdd(&F->n_limited, 1);
+    }
   }
 }
 
+// ===========================================================================
+// Half-line variant (N+1 >= 5).  Every line is split into A = nodes [0,H) and
+// B = [H,N+1); the A halves of 32 consecutive lines form one warp ("X"), their
+// B halves the next warp ("Y"), so the two code paths never diverge inside a
+// warp and each thread holds half a line: ~half the registers of the
+// full-line kernel, twice the resident warps.  X evaluates the A-A pairs and
+// the A x B0 cross pairs (streaming B0 nodes from shared memory), Y the B-B
+// pairs and the A x B1 cross pairs (streaming A); the cross contributions for
+// the streamed nodes go back through shared memory.  The line data lands in a
+// row-padded layout (stride N+2) via 8-byte cp.async, so both the xi-line
+// (column) and eta-line (row) reads are bank-conflict free.  The node phase
+// runs on the xi-line threads, whose nodes (k, j) make coalesced rows.
+template <int N1>
+struct HL {
+  static constexpr int NP = N1 * N1, LE = 2 * N1;
+  static constexpr int H = (N1 + 1) / 2, NB = N1 - H;
+  static constexpr int work_x(int b0) { return H * (H - 1) / 2 + H * b0; }
+  static constexpr int work_y(int b0) { return NB * (NB - 1) / 2 + H * (NB - b0); }
+  static constexpr int best_b0() {
+    int best = 0, bd = 1 << 30;
+    for (int b0 = 0; b0 <= NB; ++b0) {
+      const int d = work_x(b0) > work_y(b0) ? work_x(b0) - work_y(b0) : work_y(b0) - work_x(b0);
+      if (d < bd) {
+        bd = d;
+        best = b0;
+      }
+    }
+    return best;
+  }
+  static constexpr int NB0 = best_b0();
+  static constexpr int E0 = (64 / LE) > 1 ? (64 / LE) : 1;
+  static constexpr int E = (N1 & 1) ? ((E0 & ~1) > 2 ? (E0 & ~1) : 2) : (E0 > 2 ? E0 : 2);
+  static constexpr int L = E * LE;        // lines per CTA
+  static constexpr int WP = (L + 31) / 32;  // warps per part
+  static constexpr int THREADS = 64 * WP;
+  static constexpr int PAD = N1 + 1;       // padded row stride
+  static constexpr int EPAD = N1 * PAD;    // one padded element field
+  static constexpr int GPAD = E * EPAD;
+  static constexpr int GNP = (E * NP + 1) & ~1;
+  enum { F_H, F_HU, F_HV, F_YE, F_XE, F_YX, F_XX, kLineFields };
+  enum { N_JAC, N_SX, N_SY, N_WH, N_WHU, N_WHV, kNodeFields };
+  static constexpr int XS = 3 * (NB0 + H);  // exchange slots per line
+  static constexpr int LP = 32 * WP;        // lane slots per part (>= L; tail lanes idle)
+  // shared-memory plan, in doubles
+  static constexpr int LINE = 0;
+  static constexpr int ACC = LINE + kLineFields * GPAD;
+  static constexpr int XCH = ACC + 3 * GPAD;
+  static constexpr int NODE = XCH + LP * XS;
+  static constexpr int TR = NODE + kNodeFields * GNP;  // [E][4][N1][8]
+  static constexpr int EFO = TR + E * 4 * N1 * 8;       // int4 [E][4]
+  static constexpr int RED = EFO + E * 4 * 2;          // [2][LP][6]
+  static constexpr int BAR = RED + LP * 2 * 6;
+  static constexpr int TOTAL = BAR + 2;
+  static constexpr size_t bytes = TOTAL * sizeof(double);
+};
+
+// symmetric two-point contravariant flux of one pair, scaled (4F0, 8F1, 8F2)
+__device__ __forceinline__ void pair_flux(double ha, double ua, double va, double hua,
+                                          double hva, double Aa, double Ba, double hb,
+                                          double ub, double vb, double hub, double hvb,
+                                          double Ab, double Bb, double g2, double& F0,
+                                          double& T1, double& T2) {
+  const double Shu = hua + hub, Shv = hva + hvb, Su = ua + ub, Sv = va + vb;
+  const double SA = Aa + Ab, SB = Ba + Bb;
+  F0 = SA * Shu - SB * Shv;
+  const double Q = g2 * ha * hb;
+  T1 = Su * F0 + Q * SA;
+  T2 = Sv * F0 - Q * SB;
+}
+
+template <int N1>
+using HArr = double[HL<N1>::H];
+
+template <int N1, int PART>
+__device__ __forceinline__ void hl_intra(const HArr<N1>& h, const HArr<N1>& u,
+                                         const HArr<N1>& v, const HArr<N1>& hu,
+                                         const HArr<N1>& hv, const HArr<N1>& Am,
+                                         const HArr<N1>& Bm, HArr<N1>& r0, HArr<N1>& r1,
+                                         HArr<N1>& r2, double g2) {
+  using O = Ops<N1>;
+  constexpr int H = HL<N1>::H, NK = PART ? N1 - H : H, OFF = PART ? H : 0;
+  constexpr int CORNER = PART ? NK - 1 : 0;  // node 0 (X) / node N (Y): Dtilde(i,i) != 0
+#pragma unroll
+  for (int a = 0; a < NK; ++a) {
+#pragma unroll
+    for (int b = a; b < NK; ++b) {
+      if (a == b && a != CORNER) continue;
+      double F0, T1, T2;
+      pair_flux(h[a], u[a], v[a], hu[a], hv[a], Am[a], Bm[a], h[b], u[b], v[b], hu[b], hv[b],
+                Am[b], Bm[b], g2, F0, T1, T2);
+      r0[a] += O::D4(OFF + a, OFF + b) * F0;
+      r1[a] += O::D8(OFF + a, OFF + b) * T1;
+      r2[a] += O::D8(OFF + a, OFF + b) * T2;
+      if (a != b) {
+        r0[b] += O::D4(OFF + b, OFF + a) * F0;
+        r1[b] += O::D8(OFF + b, OFF + a) * T1;
+        r2[b] += O::D8(OFF + b, OFF + a) * T2;
+      }
+    }
+  }
+}
+
+template <int N1>
+__device__ __forceinline__ void hl_prefetch_line(double* sm, const Mesh& M, const CState& in,
+                                                 int g, int tid) {
+  using P = HL<N1>;
+  const int e0 = g * P::E, ne = min(P::E, M.n_owned - e0);
+  const long long base = (long long)e0 * P::NP;
+  const int cnt = ne * P::NP;
+  // one node per iteration, all 7 fields; divisions by compile-time constants
+  for (int r = tid; r < cnt; r += P::THREADS) {
+    const int el = r / P::NP, q = r - el * P::NP;
+    const int i = q / N1, j = q - i * N1;
+    double* d = sm + P::LINE + el * P::EPAD + i * P::PAD + j;
+    const long long s = base + r;
+    cp_async8(d + P::F_H * P::GPAD, in.h + s);
+    cp_async8(d + P::F_HU * P::GPAD, in.hu + s);
+    cp_async8(d + P::F_HV * P::GPAD, in.hv + s);
+    cp_async8(d + P::F_YE * P::GPAD, M.ye + s);
+    cp_async8(d + P::F_XE * P::GPAD, M.xe + s);
+    cp_async8(d + P::F_YX * P::GPAD, M.yx + s);
+    cp_async8(d + P::F_XX * P::GPAD, M.xx + s);
+  }
+  const int4* ef = M.ef + (long long)e0 * 4;
+  int4* dst = reinterpret_cast<int4*>(sm + P::EFO);
+  for (int idx = tid; idx < ne * 4; idx += P::THREADS)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst + idx)),
+                 "l"(ef + idx)
+                 : "memory");
+}
+
+template <int N1>
+__device__ __forceinline__ void hl_issue_node(double* sm, const Mesh& M, const StageArgs& A,
+                                              int g, uint64_t* bar) {
+  using P = HL<N1>;
+  const int e0 = g * P::E, ne = min(P::E, M.n_owned - e0);
+  const uint32_t fb = round16((size_t)ne * P::NP * sizeof(double));
+  const bool wn = A.update && A.stage > 0;
+  mbar_expect_tx(bar, (wn ? 6 : 3) * fb);
+  const long long off = (long long)e0 * P::NP;
+  bulk_g2s(sm + P::NODE + P::N_JAC * P::GNP, M.jac + off, fb, bar);
+  bulk_g2s(sm + P::NODE + P::N_SX * P::GNP, M.sx + off, fb, bar);
+  bulk_g2s(sm + P::NODE + P::N_SY * P::GNP, M.sy + off, fb, bar);
+  if (wn) {
+    bulk_g2s(sm + P::NODE + P::N_WH * P::GNP, A.wn.h + off, fb, bar);
+    bulk_g2s(sm + P::NODE + P::N_WHU * P::GNP, A.wn.hu + off, fb, bar);
+    bulk_g2s(sm + P::NODE + P::N_WHV * P::GNP, A.wn.hv + off, fb, bar);
+  }
+}
+
+template <int N1, bool FORCE>
+__global__ void __launch_bounds__(HL<N1>::THREADS)
+    k_stage_hl(Mesh M, Phys Ph, StageArgs A, Flags* F) {
+  using P = HL<N1>;
+  using O = Ops<N1>;
+  constexpr int NP = N1 * N1, H = P::H, NB0 = P::NB0, PAD = P::PAD;
+  constexpr int S = (H > N1 - H) ? H : N1 - H;  // register slots per thread
+  extern __shared__ __align__(16) double sm[];
+  uint64_t* bar_node = reinterpret_cast<uint64_t*>(sm + P::BAR);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int part = warp & 1;                   // 0: X (A half), 1: Y (B half)
+  const int line = (warp >> 1) * 32 + lane;    // line index inside the CTA
+  const bool line_ok = line < P::L;
+  const int el = line / P::LE, r = line - el * P::LE;
+  const bool xi = r < N1;
+  const int li = xi ? r : r - N1;
+  const int k0 = part ? H : 0;                  // first node of this thread's half
+  const int nk = part ? N1 - H : H;             // nodes held
+  const int ngroups = (M.n_owned + P::E - 1) / P::E;
+  const double g = Ph.g, h_des = Ph.h_des, inv2g = 1.0 / (2.0 * g), iw0 = 1.0 / M.w0;
+  const double g2 = 2.0 * g;
+
+  if (tid == 0) {
+    mbar_init(bar_node, 1);
+    fence_mbar_init();
+  }
+  if ((int)blockIdx.x >= ngroups) return;
+  hl_prefetch_line<N1>(sm, M, A.in, blockIdx.x, tid);
+  cp_async_commit();
+  uint32_t ph_node = 0;
+
+  // padded in-element offset of node k of this line
+  auto pidx = [&](int k) { return xi ? k * PAD + li : li * PAD + k; };
+
+  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    const int e0 = grp * P::E, ne = min(P::E, M.n_owned - e0);
+    const bool active = line_ok && el < ne;
+    const int e = e0 + el;
+    cp_async_wait_all();
+    __syncthreads();  // line(g) and connectivity(g) resident for every thread
+    if (tid == 0) {
+      fence_proxy_async();
+      hl_issue_node<N1>(sm, M, A, grp, bar_node);
+    }
+
+    // ---- own half -> registers, gathers for the own endpoint
+    double h[S], u[S], v[S], hu[S], hv[S], Am[S], Bm[S], r0[S], r1[S], r2[S];
+    const double* Lb = sm + P::LINE + el * P::EPAD;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      r0[s] = r1[s] = r2[s] = 0.0;
+      h[s] = hu[s] = hv[s] = Am[s] = Bm[s] = u[s] = v[s] = 0.0;
+      if (s < nk && active) {
+        const int q = pidx(k0 + s);
+        h[s] = Lb[P::F_H * P::GPAD + q];
+        hu[s] = Lb[P::F_HU * P::GPAD + q];
+        hv[s] = Lb[P::F_HV * P::GPAD + q];
+        Am[s] = xi ? Lb[P::F_YE * P::GPAD + q] : -Lb[P::F_YX * P::GPAD + q];
+        Bm[s] = xi ? Lb[P::F_XE * P::GPAD + q] : -Lb[P::F_XX * P::GPAD + q];
+        vel(h[s], hu[s], hv[s], h_des, u[s], v[s]);
+      }
+    }
+    const int face = xi ? (part ? 1 : 3) : (part ? 2 : 0);
+    int efy = 0;
+    // trace slots are component-major ([8][E][4][N+1]): consecutive lanes hit
+    // consecutive words (no bank conflicts)
+    constexpr int TRS = P::E * 4 * N1;
+    double* tr = sm + P::TR + (el * 4 + face) * N1 + li;
+    if (active) {
+      const int4 ef = reinterpret_cast<const int4*>(sm + P::EFO)[el * 4 + face];
+      efy = ef.y;
+      const long long own = (long long)e * NP + face_node(N1, face, li);
+      cp_async8(tr + 6 * TRS, M.b + own);
+      if ((ef.y & EF_PRESENT) && !(ef.y & EF_WALL)) {
+        const int nf = ef.y & EF_NBR_FACE_MASK;
+        const int tp = (ef.y & EF_REVERSED) ? N1 - 1 - li : li;
+        const long long nb = (long long)ef.x * NP + face_node(N1, nf, tp);
+        cp_async8(tr + 0 * TRS, A.in.h + nb);
+        cp_async8(tr + 1 * TRS, A.in.hu + nb);
+        cp_async8(tr + 2 * TRS, A.in.hv + nb);
+        cp_async8(tr + 3 * TRS, M.b + nb);
+        if (!(ef.y & EF_MINUS)) {
+          const bool ew = nf == 1 || nf == 3;
+          cp_async8(tr + 4 * TRS, (ew ? M.ye : M.yx) + nb);
+          cp_async8(tr + 5 * TRS, (ew ? M.xe : M.xx) + nb);
+        }
+      }
+    }
+    cp_async_commit();
+
+    // ---- volume: pairs inside the own half (+ the corner diagonal); part is
+    // warp-uniform, so each warp runs one fully unrolled, constant-operand body
+    if (part == 0)
+      hl_intra<N1, 0>(h, u, v, hu, hv, Am, Bm, r0, r1, r2, g2);
+    else
+      hl_intra<N1, 1>(h, u, v, hu, hv, Am, Bm, r0, r1, r2, g2);
+    // ---- cross pairs: X streams B0 = [H, H+NB0), Y streams A = [0, H)
+    // exchange slots are slot-major ([XS][LP]): consecutive lanes, consecutive words
+    double* xch_base = sm + P::XCH + line;
+    auto xch = [&](int slot) -> double& { return xch_base[slot * P::LP]; };
+    if (part == 0) {
+#pragma unroll
+      for (int s = 0; s < NB0; ++s) {
+        const int q = pidx(H + s);
+        const double hb = Lb[P::F_H * P::GPAD + q], hub = Lb[P::F_HU * P::GPAD + q],
+                     hvb = Lb[P::F_HV * P::GPAD + q];
+        const double Ab = xi ? Lb[P::F_YE * P::GPAD + q] : -Lb[P::F_YX * P::GPAD + q];
+        const double Bb = xi ? Lb[P::F_XE * P::GPAD + q] : -Lb[P::F_XX * P::GPAD + q];
+        double ub, vb;
+        vel(hb, hub, hvb, h_des, ub, vb);
+        double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+#pragma unroll
+        for (int a = 0; a < H; ++a) {
+          double F0, T1, T2;
+          pair_flux(h[a], u[a], v[a], hu[a], hv[a], Am[a], Bm[a], hb, ub, vb, hub, hvb, Ab, Bb,
+                    g2, F0, T1, T2);
+          r0[a] += O::D4(a, H + s) * F0;
+          r1[a] += O::D8(a, H + s) * T1;
+          r2[a] += O::D8(a, H + s) * T2;
+          c0 += O::D4(H + s, a) * F0;
+          c1 += O::D8(H + s, a) * T1;
+          c2 += O::D8(H + s, a) * T2;
+        }
+        xch(3 * s + 0) = c0;
+        xch(3 * s + 1) = c1;
+        xch(3 * s + 2) = c2;
+      }
+    } else {
+#pragma unroll
+      for (int a = 0; a < H; ++a) {
+        const int q = pidx(a);
+        const double ha = Lb[P::F_H * P::GPAD + q], hua = Lb[P::F_HU * P::GPAD + q],
+                     hva = Lb[P::F_HV * P::GPAD + q];
+        const double Aa = xi ? Lb[P::F_YE * P::GPAD + q] : -Lb[P::F_YX * P::GPAD + q];
+        const double Ba = xi ? Lb[P::F_XE * P::GPAD + q] : -Lb[P::F_XX * P::GPAD + q];
+        double ua, va;
+        vel(ha, hua, hva, h_des, ua, va);
+        double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+#pragma unroll
+        for (int s = NB0; s < N1 - H; ++s) {
+          double F0, T1, T2;
+          pair_flux(ha, ua, va, hua, hva, Aa, Ba, h[s], u[s], v[s], hu[s], hv[s], Am[s], Bm[s],
+                    g2, F0, T1, T2);
+          r0[s] += O::D4(H + s, a) * F0;
+          r1[s] += O::D8(H + s, a) * T1;
+          r2[s] += O::D8(H + s, a) * T2;
+          c0 += O::D4(a, H + s) * F0;
+          c1 += O::D8(a, H + s) * T1;
+          c2 += O::D8(a, H + s) * T2;
+        }
+        xch(3 * NB0 + 3 * a + 0) = c0;
+        xch(3 * NB0 + 3 * a + 1) = c1;
+        xch(3 * NB0 + 3 * a + 2) = c2;
+      }
+    }
+    __syncthreads();  // cross contributions published; line buffer free
+    // the partner half's exchange slots: X (line's A) gets Y's, Y gets X's
+    if (part == 0) {
+#pragma unroll
+      for (int a = 0; a < H; ++a) {
+        r0[a] += xch(3 * NB0 + 3 * a + 0);
+        r1[a] += xch(3 * NB0 + 3 * a + 1);
+        r2[a] += xch(3 * NB0 + 3 * a + 2);
+      }
+    } else {
+#pragma unroll
+      for (int s = 0; s < NB0; ++s) {
+        r0[s] += xch(3 * s + 0);
+        r1[s] += xch(3 * s + 1);
+        r2[s] += xch(3 * s + 2);
+      }
+    }
+    {  // prefetch the next group's line data behind the rest of this group
+      const int gn = grp + gridDim.x;
+      if (gn < ngroups) hl_prefetch_line<N1>(sm, M, A.in, gn, tid);
+      cp_async_commit();
+    }
+
+    // ---- interface flux at the own endpoint (dg_rhs.hpp:202-252)
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // gathers(g); line(g+1) may fly
+    if (active && (efy & EF_PRESENT)) {
+      constexpr int SY = (N1 - H) - 1;  // Y's endpoint slot (node N); X's is slot 0
+      const double hs = part ? h[SY] : h[0], hus = part ? hu[SY] : hu[0];
+      const double hvs = part ? hv[SY] : hv[0];
+      const double As = part ? Am[SY] : Am[0], Bs = part ? Bm[SY] : Bm[0];
+      const double om0 = xi ? As : -As, om1 = xi ? Bs : -Bs;
+      const double bo = tr[6 * TRS];
+      double wm0, wm1, wm2, wp0, wp1, wp2, bm, bp, nx, ny, js, sgn = 1.0;
+      if (efy & EF_MINUS) {
+        face_normal(face, om0, om1, nx, ny, js);
+        wm0 = hs;
+        wm1 = hus;
+        wm2 = hvs;
+        bm = bo;
+        if (efy & EF_WALL) {
+          const double mn = wm1 * nx + wm2 * ny;
+          wp0 = wm0;
+          wp1 = wm1 - 2.0 * mn * nx;
+          wp2 = wm2 - 2.0 * mn * ny;
+          bp = bm;
+        } else {
+          wp0 = tr[0 * TRS];
+          wp1 = tr[1 * TRS];
+          wp2 = tr[2 * TRS];
+          bp = tr[3 * TRS];
+        }
+      } else {
+        face_normal(efy & EF_NBR_FACE_MASK, tr[4 * TRS], tr[5 * TRS], nx, ny, js);
+        wm0 = tr[0 * TRS];
+        wm1 = tr[1 * TRS];
+        wm2 = tr[2 * TRS];
+        bm = tr[3 * TRS];
+        wp0 = hs;
+        wp1 = hus;
+        wp2 = hvs;
+        bp = bo;
+        sgn = -1.0;
+      }
+      double f0, f1, f2;
+      es_flux_fast(wm0, wm1, wm2, wp0, wp1, wp2, bm, bp, nx, ny, g, inv2g, h_des, f0, f1, f2);
+      const double c = sgn * js * iw0;
+      if (part) {
+        r0[SY] += c * f0;
+        r1[SY] += c * f1;
+        r2[SY] += c * f2;
+      } else {
+        r0[0] += c * f0;
+        r1[0] += c * f1;
+        r2[0] += c * f2;
+      }
+    }
+    // eta-line threads hand their accumulators to the xi-line owners
+    if (!xi && active) {
+      double* acc = sm + P::ACC + el * P::EPAD;
+#pragma unroll
+      for (int s = 0; s < S; ++s)
+        if (s < nk) {
+          const int q = pidx(k0 + s);
+          acc[0 * P::GPAD + q] = r0[s];
+          acc[1 * P::GPAD + q] = r1[s];
+          acc[2 * P::GPAD + q] = r2[s];
+        }
+    }
+    __syncthreads();
+    mbar_wait(bar_node, ph_node);
+    ph_node ^= 1;
+
+    // ---- node phase on the xi-line threads: nodes (k, li), k in the own half
+    double* red = sm + P::RED + (part * P::LP + line) * 6;
+    if (xi && active) {
+      const double* acc = sm + P::ACC + el * P::EPAD;
+      const double* Nd = sm + P::NODE + el * NP;
+      double s_area = 0.0, s0 = 0.0, s1 = 0.0, s2 = 0.0, mmin = 1.0e300;
+      const double wj = O::w(li);
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        if (s >= nk) continue;
+        const int k = k0 + s, q = k * N1 + li, qp = k * PAD + li;
+        const long long n = (long long)e * NP + q;
+        const double jac = Nd[P::N_JAC * P::GNP + q];
+        const double ij = -1.0 / jac, hg2 = 0.5 * g * h[s];
+        double rh = (acc[0 * P::GPAD + qp] + r0[s]) * ij;
+        double rhu = (acc[1 * P::GPAD + qp] + r1[s] + hg2 * Nd[P::N_SX * P::GNP + q]) * ij;
+        double rhv = (acc[2 * P::GPAD + qp] + r2[s] + hg2 * Nd[P::N_SY * P::GNP + q]) * ij;
+        if (FORCE) {
+          rh += A.fh[n];
+          rhu += A.fhu[n];
+          rhv += A.fhv[n];
+        }
+        if (A.rhs.h) {
+          A.rhs.h[n] = rh;
+          A.rhs.hu[n] = rhu;
+          A.rhs.hv[n] = rhv;
+        }
+        double sh = h[s] + A.dt * rh;
+        double shu = hu[s] + A.dt * rhu;
+        double shv = hv[s] + A.dt * rhv;
+        if (A.stage > 0 && A.update) {
+          sh = A.ca * Nd[P::N_WH * P::GNP + q] + A.cb * sh;
+          shu = A.ca * Nd[P::N_WHU * P::GNP + q] + A.cb * shu;
+          shv = A.ca * Nd[P::N_WHV * P::GNP + q] + A.cb * shv;
+        }
+        h[s] = sh;
+        hu[s] = shu;
+        hv[s] = shv;
+        const double wq = O::w(k) * wj * jac;
+        s_area += wq;
+        s0 += wq * sh;
+        s1 += wq * shu;
+        s2 += wq * shv;
+        mmin = smin(mmin, sh);
+      }
+      red[0] = s_area;
+      red[1] = s0;
+      red[2] = s1;
+      red[3] = s2;
+      red[4] = mmin;
+    }
+    __syncthreads();
+
+    // ---- limiter (limit_element, limiter.hpp:43-84) and write-out
+    bool lim = active && A.update;
+    double area = 0.0, a0 = 0.0, a1 = 0.0, a2 = 0.0, mmin = 1.0e300;
+    if (lim) {
+#pragma unroll
+      for (int pp = 0; pp < 2; ++pp)
+#pragma unroll
+        for (int l = 0; l < N1; ++l) {
+          const double* rr = sm + P::RED + (pp * P::LP + el * P::LE + l) * 6;
+          area += rr[0];
+          a0 += rr[1];
+          a1 += rr[2];
+          a2 += rr[3];
+          mmin = smin(mmin, rr[4]);
+        }
+    }
+    const double inv = 1.0 / area;
+    const double avg0 = inv * a0, avg1 = inv * a1, avg2 = inv * a2;
+    const bool lead = part == 0 && r == 0;  // one thread per element
+    if (lim && avg0 < 0.0) {
+      if (lead) {
+        atomicExch(&F->reject, 1);
+        if (!Ph.limiter) atomicExch(&F->abort, 1);
+      }
+      lim = false;
+    }
+    double theta = 1.0;
+    if (lim && Ph.limiter && mmin < 0.0) {
+      const double denom = avg0 - mmin;
+      theta = denom < 1e-14 ? 1.0 : smin(1.0, avg0 / denom);
+    }
+    if (lim && !Ph.limiter && mmin < 0.0 && lead) atomicExch(&F->abort, 1);
+    double mine = 1.0e300;
+    if (lim && xi) {
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        if (s >= nk) continue;
+        const long long n = (long long)e * NP + (k0 + s) * N1 + li;
+        double sh = h[s], shu = hu[s], shv = hv[s];
+        if (theta < 1.0) {
+          sh = smax(theta * (sh - avg0) + avg0, 0.0);
+          shu = theta * (shu - avg1) + avg1;
+          shv = theta * (shv - avg2) + avg2;
+        }
+        if (Ph.limiter && sh < Ph.h_tol) {
+          shu = 0.0;
+          shv = 0.0;
+        }
+        A.out.h[n] = sh;
+        A.out.hu[n] = shu;
+        A.out.hv[n] = shv;
+        mine = smin(mine, sh);
+      }
+    }
+    red[5] = mine;
+    __syncthreads();
+    if (lim && lead) {
+      double m = 1.0e300;
+      for (int pp = 0; pp < 2; ++pp)
+        for (int l = 0; l < N1; ++l) m = smin(m, sm[P::RED + (pp * P::LP + el * P::LE + l) * 6 + 5]);
+      atomicMin(&F->min_h_key, order_key(m));
+      if (theta < 1.0) atomicAdd(&F->n_limited, 1);
+    }
+  }
+  cp_async_wait_all();
+}
+
+// geometry-only split-source coefficients (dg_rhs.hpp:159-176), one thread per node
+__global__ void k_source_geometry(Mesh M, double* sx, double* sy) {
+  const long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (n >= (long long)M.K * M.np) return;
+  const int n1 = M.n1, np = M.np;
+  const int loc = (int)(n % np), i = loc / n1, j = loc % n1;
+  const long long base = n - loc;
+  double db_xi = 0.0, db_eta = 0.0, dye = 0.0, dyx = 0.0, dxe = 0.0, dxx = 0.0;
+  for (int m = 0; m < n1; ++m) {
+    const double di = M.D[i * n1 + m], dj = M.D[j * n1 + m];
+    const long long qx = base + m * n1 + j, qe = base + i * n1 + m;
+    db_xi += di * M.b[qx];
+    db_eta += dj * M.b[qe];
+    dye += di * (M.ye[qx] * M.b[qx]);
+    dxe += di * (M.xe[qx] * M.b[qx]);
+    dyx += dj * (M.yx[qe] * M.b[qe]);
+    dxx += dj * (M.xx[qe] * M.b[qe]);
+  }
+  sx[n] = M.ye[n] * db_xi + dye - M.yx[n] * db_eta - dyx;
+  sy[n] = M.xx[n] * db_eta + dxx - M.xe[n] * db_xi - dxe;
+}
+
 }  // namespace
+
+int launch_source_geometry(const Mesh& M, double* sx, double* sy, cudaStream_t st) {
+  const long long nn = (long long)M.K * M.np;
+  k_source_geometry<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(M, sx, sy);
+  return 1;
+}
 
 // ---------------------------------------------------------------------------
 static bool g_ops_set[17];
@@ -425,35 +1074,94 @@ int upload_fast_ops(int n1, const double* D, const double* Dt, const double* Dh,
   return 0;
 }
 
+template <class KERN>
+static int grid_for(KERN kern, int threads, size_t bytes, int groups, int& cache) {
+  if (cache == 0) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, bytes);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cache = (per_sm > 0 ? per_sm : 1) * sms;
+  }
+  return groups < cache ? groups : cache;
+}
+
+// full-line kernel (N+1 <= 4 by default)
+template <int N1, bool FORCE>
+static void launch_full(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
+                        cudaStream_t st) {
+  using PL = Plan<N1>;
+  static int cache = 0;
+  auto kern = k_stage<N1, FORCE>;
+  const int grid = grid_for(kern, PL::THREADS, PL::bytes, (M.n_owned + PL::E - 1) / PL::E, cache);
+  kern<<<grid, PL::THREADS, PL::bytes, st>>>(M, P, A, F);
+}
+
+// half-line kernel (N+1 >= 5)
+template <int N1, bool FORCE>
+static void launch_half(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
+                        cudaStream_t st) {
+  using PL = HL<N1>;
+  static int cache = 0;
+  auto kern = k_stage_hl<N1, FORCE>;
+  const int grid = grid_for(kern, PL::THREADS, PL::bytes, (M.n_owned + PL::E - 1) / PL::E, cache);
+  kern<<<grid, PL::THREADS, PL::bytes, st>>>(M, P, A, F);
+}
+
+static int variant_override() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("SWDG_FAST_VARIANT");  // "full" / "half" (experiments)
+    v = !s ? 0 : (s[0] == 'f' ? 1 : (s[0] == 'h' ? 2 : 0));
+  }
+  return v;
+}
+
 template <int N1>
-static void launch_lines(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
-                         cudaStream_t st) {
-  constexpr int E = elems_per_block<N1>(), T = 2 * N1;
-  const size_t smem = (size_t)E * Smem<N1>::per_elem * sizeof(double);
-  const unsigned grid = (unsigned)((M.n_owned + E - 1) / E);
-  if (A.fh) {
-    cudaFuncSetAttribute(k_stage_lines<N1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    k_stage_lines<N1, true><<<grid, E * T, smem, st>>>(M, P, A, F);
-  } else {
-    cudaFuncSetAttribute(k_stage_lines<N1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    k_stage_lines<N1, false><<<grid, E * T, smem, st>>>(M, P, A, F);
+static void launch_n(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
+                     cudaStream_t st) {
+  const int ov = variant_override();
+  bool half = N1 >= 5;
+  if constexpr (N1 <= 8) {
+    if (ov == 1) half = false;
+  }
+  if constexpr (N1 >= 5) {
+    if (ov == 2) half = true;
+  }
+  if constexpr (N1 <= 8) {
+    if (!half) {
+      if (A.fh) launch_full<N1, true>(M, P, A, F, st);
+      else launch_full<N1, false>(M, P, A, F, st);
+      return;
+    }
+  }
+  if constexpr (N1 >= 5) {
+    if (A.fh) launch_half<N1, true>(M, P, A, F, st);
+    else launch_half<N1, false>(M, P, A, F, st);
   }
 }
 
-bool fast_stage_supported(int n1) { return n1 >= 2 && n1 <= 8; }
+bool fast_stage_supported(int n1) { return n1 >= 2 && n1 <= 16; }
 
 int launch_fast_stage(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
                       cudaStream_t st) {
   switch (M.n1) {
-    case 2: launch_lines<2>(M, P, A, F, st); break;
-    case 3: launch_lines<3>(M, P, A, F, st); break;
-    case 4: launch_lines<4>(M, P, A, F, st); break;
-    case 5: launch_lines<5>(M, P, A, F, st); break;
-    case 6: launch_lines<6>(M, P, A, F, st); break;
-    case 7: launch_lines<7>(M, P, A, F, st); break;
-    case 8: launch_lines<8>(M, P, A, F, st); break;
+    case 2: launch_n<2>(M, P, A, F, st); break;
+    case 3: launch_n<3>(M, P, A, F, st); break;
+    case 4: launch_n<4>(M, P, A, F, st); break;
+    case 5: launch_n<5>(M, P, A, F, st); break;
+    case 6: launch_n<6>(M, P, A, F, st); break;
+    case 7: launch_n<7>(M, P, A, F, st); break;
+    case 8: launch_n<8>(M, P, A, F, st); break;
+    case 9: launch_n<9>(M, P, A, F, st); break;
+    case 10: launch_n<10>(M, P, A, F, st); break;
+    case 11: launch_n<11>(M, P, A, F, st); break;
+    case 12: launch_n<12>(M, P, A, F, st); break;
+    case 13: launch_n<13>(M, P, A, F, st); break;
+    case 14: launch_n<14>(M, P, A, F, st); break;
+    case 15: launch_n<15>(M, P, A, F, st); break;
+    case 16: launch_n<16>(M, P, A, F, st); break;
     default: return 0;
   }
   return 1;

@@ -37,6 +37,10 @@ struct Mesh {
   const double *len_xi, *len_eta;
   const double *fnx, *fny, *fjs, *fa;
   const int4* ef;  // [K*4]
+  // fast mode: geometry-only part of the split source (dg_rhs.hpp:171-176),
+  // S_x = y_eta D_xi b + D_xi(y_eta b) - y_xi D_eta b - D_eta(y_xi b) and S_y
+  // likewise, so the stage adds (g h / 2) (S_x, S_y)
+  const double *sx, *sy;
 };
 
 struct State {

@@ -273,7 +273,10 @@ void allocate(swdg_gpu* c, int K, int n_owned, int N, const std::vector<int4>& e
   const long long nn = (long long)K * np, nf = (long long)K * 4 * n1;
   c->nn = nn;
   c->nf = nf;
-  c->geo = c->dalloc<double>(8 * nn + 4 * nf);
+  // nodal arrays sit at a padded stride: every array starts 16-byte aligned
+  // and a bulk copy of the last partial element group may round up by 8 bytes
+  const long long nnp = ((nn + 1) & ~1ll) + 2;
+  c->geo = c->dalloc<double>(10 * nnp + 4 * nf);
   double* ops = c->dalloc<double>(n1 + 4 * np);
   upload(ops, ops_w, n1, "weights");
   upload(ops + n1, ops_d, np, "deriv");
@@ -297,14 +300,16 @@ void allocate(swdg_gpu* c, int K, int n_owned, int N, const std::vector<int4>& e
   M.Vinv = ops + n1 + 3 * np;
   double* geo = c->geo;
   M.ye = geo;
-  M.xe = geo + nn;
-  M.yx = geo + 2 * nn;
-  M.xx = geo + 3 * nn;
-  M.jac = geo + 4 * nn;
-  M.b = geo + 5 * nn;
-  M.len_xi = geo + 6 * nn;
-  M.len_eta = geo + 7 * nn;
-  double* fgeo = geo + 8 * nn;
+  M.xe = geo + nnp;
+  M.yx = geo + 2 * nnp;
+  M.xx = geo + 3 * nnp;
+  M.jac = geo + 4 * nnp;
+  M.b = geo + 5 * nnp;
+  M.len_xi = geo + 6 * nnp;
+  M.len_eta = geo + 7 * nnp;
+  M.sx = geo + 8 * nnp;
+  M.sy = geo + 9 * nnp;
+  double* fgeo = geo + 10 * nnp;
   M.fnx = fgeo;
   M.fny = fgeo + nf;
   M.fjs = fgeo + 2 * nf;
@@ -318,14 +323,14 @@ void allocate(swdg_gpu* c, int K, int n_owned, int N, const std::vector<int4>& e
     c->fast = fast_stage_supported(n1);
   }
 
-  double* sbuf = c->dalloc<double>(12 * nn);
+  double* sbuf = c->dalloc<double>(12 * nnp);
   for (int k = 0; k < 3; ++k) {
-    c->W[k] = sbuf + k * nn;
-    c->A[k] = sbuf + (3 + k) * nn;
-    c->B[k] = sbuf + (6 + k) * nn;
-    c->R[k] = sbuf + (9 + k) * nn;
+    c->W[k] = sbuf + k * nnp;
+    c->A[k] = sbuf + (3 + k) * nnp;
+    c->B[k] = sbuf + (6 + k) * nnp;
+    c->R[k] = sbuf + (9 + k) * nnp;
   }
-  ck(cudaMemset(sbuf, 0, 12 * nn * sizeof(double)), "memset state");
+  ck(cudaMemset(sbuf, 0, 12 * nnp * sizeof(double)), "memset state");
   c->eps = c->dalloc<double>(K);
   c->r_ind = c->dalloc<double>(K);
   ck(cudaMemset(c->eps, 0, K * sizeof(double)), "memset eps");
@@ -367,6 +372,10 @@ template <class F>
 int create_guarded(swdg_gpu* c, swdg_gpu** out, F&& body) {
   try {
     body();
+    // fast mode: geometry-only split-source coefficients, once per mesh
+    if (c->params.mode == SWDG_MODE_FAST)
+      c->launches += launch_source_geometry(c->M, const_cast<double*>(c->M.sx),
+                                            const_cast<double*>(c->M.sy), c->stream);
     ck(cudaDeviceSynchronize(), "create sync");
   } catch (const CudaError& e) {
     g_create_error = std::string(e.where) + ": " + cudaGetErrorString(e.e);
@@ -416,13 +425,13 @@ int swdg_gpu_create(const swdg_mesh_view* mv, const swdg_params* p, int device,
     allocate(c, K, n_owned, N, ef, mv->weights, mv->deriv, mv->deriv_modified, mv->deriv_weak,
              mv->vandermonde_inv);
     const long long nn = (long long)K * np, nf = (long long)K * 4 * n1;
-    double* geo = c->geo;
-    upload(geo + 0 * nn, mv->y_eta, nn, "y_eta");
-    upload(geo + 1 * nn, mv->x_eta, nn, "x_eta");
-    upload(geo + 2 * nn, mv->y_xi, nn, "y_xi");
-    upload(geo + 3 * nn, mv->x_xi, nn, "x_xi");
-    upload(geo + 4 * nn, mv->jac, nn, "jac");
-    upload(geo + 5 * nn, mv->b, nn, "b");
+    Mesh& M = c->M;
+    upload(const_cast<double*>(M.ye), mv->y_eta, nn, "y_eta");
+    upload(const_cast<double*>(M.xe), mv->x_eta, nn, "x_eta");
+    upload(const_cast<double*>(M.yx), mv->y_xi, nn, "y_xi");
+    upload(const_cast<double*>(M.xx), mv->x_xi, nn, "x_xi");
+    upload(const_cast<double*>(M.jac), mv->jac, nn, "jac");
+    upload(const_cast<double*>(M.b), mv->b, nn, "b");
     {
       // compute_dt lengths 2J/|(x_eta,y_eta)|, 2J/|(x_xi,y_xi)| (timeloop.hpp:62-65),
       // geometry-only: evaluated once with the reference's libm hypot
@@ -431,14 +440,13 @@ int swdg_gpu_create(const swdg_mesh_view* mv, const swdg_params* p, int device,
         lx[n] = 2.0 * mv->jac[n] / std::hypot(mv->x_eta[n], mv->y_eta[n]);
         le[n] = 2.0 * mv->jac[n] / std::hypot(mv->x_xi[n], mv->y_xi[n]);
       }
-      upload(geo + 6 * nn, lx.data(), nn, "len_xi");
-      upload(geo + 7 * nn, le.data(), nn, "len_eta");
+      upload(const_cast<double*>(M.len_xi), lx.data(), nn, "len_xi");
+      upload(const_cast<double*>(M.len_eta), le.data(), nn, "len_eta");
     }
-    double* fgeo = geo + 8 * nn;
-    upload(fgeo + 0 * nf, mv->face_nx, nf, "face_nx");
-    upload(fgeo + 1 * nf, mv->face_ny, nf, "face_ny");
-    upload(fgeo + 2 * nf, mv->face_jsurf, nf, "face_jsurf");
-    upload(fgeo + 3 * nf, mv->face_a, nf, "face_a");
+    upload(const_cast<double*>(M.fnx), mv->face_nx, nf, "face_nx");
+    upload(const_cast<double*>(M.fny), mv->face_ny, nf, "face_ny");
+    upload(const_cast<double*>(M.fjs), mv->face_jsurf, nf, "face_jsurf");
+    upload(const_cast<double*>(M.fa), mv->face_a, nf, "face_a");
     if (mv->x && mv->y) {
       c->x.assign(mv->x, mv->x + nn);
       c->y.assign(mv->y, mv->y + nn);
@@ -469,7 +477,7 @@ int swdg_gpu_create_structured(const swdg_structured_spec* s, const swdg_params*
     std::vector<double> nodes(n1), w(n1), D(np), Dt(np), Dh(np), V(np), Vi(np);
     swdg_operators(N, nodes.data(), w.data(), D.data(), Dt.data(), Dh.data(), V.data(), Vi.data());
     allocate(c, K, K, N, ef, w.data(), D.data(), Dt.data(), Dh.data(), Vi.data());
-    const long long nn = c->nn, nf = c->nf;
+    const long long nn = c->nn;
     c->xy = c->dalloc<double>(2 * nn);
     double* dnodes = c->dalloc<double>(n1);
     ck(cudaMemcpy(dnodes, nodes.data(), n1 * sizeof(double), cudaMemcpyHostToDevice), "nodes");
@@ -477,11 +485,10 @@ int swdg_gpu_create_structured(const swdg_structured_spec* s, const swdg_params*
     ck(cudaMemset(bad, 0, sizeof(int)), "memset");
     MeshSpecDev sd{s->kind, s->kx, s->ky, s->bathy_kind, s->x0, s->x1, s->y0, s->y1, s->extra,
                    {s->bathy[0], s->bathy[1], s->bathy[2], s->bathy[3]}};
-    double* geo = c->geo;
-    double* fgeo = geo + 8 * nn;
-    MeshOut o{c->xy, c->xy + nn, geo + 3 * nn, geo + 1 * nn, geo + 2 * nn, geo + 0 * nn,
-              geo + 4 * nn, geo + 5 * nn, geo + 6 * nn, geo + 7 * nn,
-              fgeo, fgeo + nf, fgeo + 2 * nf, fgeo + 3 * nf, bad};
+    const Mesh& M = c->M;
+    auto wr = [](const double* p) { return const_cast<double*>(p); };
+    MeshOut o{c->xy, c->xy + nn, wr(M.xx), wr(M.xe), wr(M.yx), wr(M.ye), wr(M.jac), wr(M.b),
+              wr(M.len_xi), wr(M.len_eta), wr(M.fnx), wr(M.fny), wr(M.fjs), wr(M.fa), bad};
     c->launches += launch_structured_mesh(sd, dnodes, c->M.D, n1, o, c->stream);
     int hbad = 0;
     ck(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "bad D2H");

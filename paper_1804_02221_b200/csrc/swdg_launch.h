@@ -34,6 +34,7 @@ int launch_exact_dt(const Mesh& M, const Phys& P, CState S, Flags* F, cudaStream
 int upload_fast_ops(int n1, const double* D, const double* Dt, const double* Dh,
                     const double* Vinv, const double* w);
 bool fast_stage_supported(int n1);
+int launch_source_geometry(const Mesh& M, double* sx, double* sy, cudaStream_t st);
 int launch_fast_stage(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
                       cudaStream_t st);
 
