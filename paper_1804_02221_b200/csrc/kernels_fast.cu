@@ -528,11 +528,30 @@ struct HL {
     return best;
   }
   static constexpr int NB0 = best_b0();
-  static constexpr int E0 = (64 / LE) > 1 ? (64 / LE) : 1;
-  static constexpr int E = (N1 & 1) ? ((E0 & ~1) > 2 ? (E0 & ~1) : 2) : (E0 > 2 ? E0 : 2);
-  static constexpr int L = E * LE;        // lines per CTA
-  static constexpr int WP = (L + 31) / 32;  // warps per part
-  static constexpr int THREADS = 64 * WP;
+  // Warp roles: (xi, X), (xi, Y), (eta, X), (eta, Y) — every branch on the line
+  // direction or the half is warp-uniform.  A role covers the E*(N+1) lines of
+  // its kind in WR warps; E maximises lane use with WR <= 2 (even E for odd N+1
+  // keeps the bulk copies 16-byte aligned).
+  static constexpr int lanes_used(int e) { return e * N1; }
+  static constexpr int warps_for(int e) { return (e * N1 + 31) / 32; }
+  static constexpr int pick_e() {
+    int best = 2, bu = 0;
+    for (int e = 2; e <= 32; ++e) {
+      if ((N1 & 1) && (e & 1)) continue;
+      if (warps_for(e) > 2) break;
+      const int u = 1000 * lanes_used(e) / (32 * warps_for(e));
+      if (u > bu) {
+        bu = u;
+        best = e;
+      }
+    }
+    return best;
+  }
+  static constexpr int E = pick_e();
+  static constexpr int L = E * LE;          // lines per CTA
+  static constexpr int WR = warps_for(E);   // warps per role
+  static constexpr int WP = 2 * WR;         // warps per half (both directions)
+  static constexpr int THREADS = 128 * WR;
   static constexpr int PAD = N1 + 1;       // padded row stride
   static constexpr int EPAD = N1 * PAD;    // one padded element field
   static constexpr int GPAD = E * EPAD;
@@ -546,10 +565,10 @@ struct HL {
   static constexpr int ACC = LINE + kLineFields * GPAD;
   static constexpr int XCH = ACC + 3 * GPAD;
   static constexpr int NODE = XCH + LP * XS;
-  static constexpr int TR = NODE + kNodeFields * GNP;  // [E][4][N1][8]
-  static constexpr int EFO = TR + E * 4 * N1 * 8;       // int4 [E][4]
-  static constexpr int RED = EFO + E * 4 * 2;          // [2][LP][6]
-  static constexpr int BAR = RED + LP * 2 * 6;
+  static constexpr int TR = NODE + kNodeFields * GNP;  // [7][E][4][N1]
+  static constexpr int EFO = TR + E * 4 * N1 * 7;       // int4 [E][4]
+  static constexpr int RED = EFO + E * 4 * 2;          // [2][32 WR xi lines][6]
+  static constexpr int BAR = RED + 2 * 32 * WR * 6;
   static constexpr int TOTAL = BAR + 2;
   static constexpr size_t bytes = TOTAL * sizeof(double);
 };
@@ -649,7 +668,7 @@ __device__ __forceinline__ void hl_issue_node(double* sm, const Mesh& M, const S
 }
 
 template <int N1, bool FORCE>
-__global__ void __launch_bounds__(HL<N1>::THREADS)
+__global__ void __launch_bounds__(HL<N1>::THREADS, (N1 <= 8 ? 3 : 1))
     k_stage_hl(Mesh M, Phys Ph, StageArgs A, Flags* F) {
   using P = HL<N1>;
   using O = Ops<N1>;
@@ -658,12 +677,13 @@ __global__ void __launch_bounds__(HL<N1>::THREADS)
   extern __shared__ __align__(16) double sm[];
   uint64_t* bar_node = reinterpret_cast<uint64_t*>(sm + P::BAR);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int part = warp & 1;                   // 0: X (A half), 1: Y (B half)
-  const int line = (warp >> 1) * 32 + lane;    // line index inside the CTA
-  const bool line_ok = line < P::L;
-  const int el = line / P::LE, r = line - el * P::LE;
-  const bool xi = r < N1;
-  const int li = xi ? r : r - N1;
+  const int role = warp / P::WR;               // 0 xi-X, 1 xi-Y, 2 eta-X, 3 eta-Y
+  const int part = role & 1;                   // 0: X (A half), 1: Y (B half)
+  const bool xi = role < 2;
+  const int lr = (warp % P::WR) * 32 + lane;   // el * (N+1) + li within the role
+  const bool line_ok = lr < P::E * N1;
+  const int el = lr / N1, li = lr - el * N1;
+  const int line = (xi ? 0 : P::WR * 32) + lr;  // exchange/reduction slot of the line
   const int k0 = part ? H : 0;                  // first node of this thread's half
   const int nk = part ? N1 - H : H;             // nodes held
   const int ngroups = (M.n_owned + P::E - 1) / P::E;
@@ -896,7 +916,7 @@ __global__ void __launch_bounds__(HL<N1>::THREADS)
     ph_node ^= 1;
 
     // ---- node phase on the xi-line threads: nodes (k, li), k in the own half
-    double* red = sm + P::RED + (part * P::LP + line) * 6;
+    double* red = sm + P::RED + (part * 32 * P::WR + lr) * 6;  // xi threads only
     if (xi && active) {
       const double* acc = sm + P::ACC + el * P::EPAD;
       const double* Nd = sm + P::NODE + el * NP;
@@ -956,7 +976,7 @@ __global__ void __launch_bounds__(HL<N1>::THREADS)
       for (int pp = 0; pp < 2; ++pp)
 #pragma unroll
         for (int l = 0; l < N1; ++l) {
-          const double* rr = sm + P::RED + (pp * P::LP + el * P::LE + l) * 6;
+          const double* rr = sm + P::RED + (pp * 32 * P::WR + el * N1 + l) * 6;
           area += rr[0];
           a0 += rr[1];
           a1 += rr[2];
@@ -966,7 +986,7 @@ __global__ void __launch_bounds__(HL<N1>::THREADS)
     }
     const double inv = 1.0 / area;
     const double avg0 = inv * a0, avg1 = inv * a1, avg2 = inv * a2;
-    const bool lead = part == 0 && r == 0;  // one thread per element
+    const bool lead = role == 0 && li == 0;  // one thread per element
     if (lim && avg0 < 0.0) {
       if (lead) {
         atomicExch(&F->reject, 1);
@@ -1002,12 +1022,13 @@ __global__ void __launch_bounds__(HL<N1>::THREADS)
         mine = smin(mine, sh);
       }
     }
-    red[5] = mine;
+    if (xi) red[5] = mine;
     __syncthreads();
     if (lim && lead) {
       double m = 1.0e300;
       for (int pp = 0; pp < 2; ++pp)
-        for (int l = 0; l < N1; ++l) m = smin(m, sm[P::RED + (pp * P::LP + el * P::LE + l) * 6 + 5]);
+        for (int l = 0; l < N1; ++l)
+          m = smin(m, sm[P::RED + (pp * 32 * P::WR + el * N1 + l) * 6 + 5]);
       atomicMin(&F->min_h_key, order_key(m));
       if (theta < 1.0) atomicAdd(&F->n_limited, 1);
     }

@@ -161,15 +161,23 @@ def test_device_mesh_generator(kind, N, bathy):
 
 
 @pytest.mark.parametrize("sid,kx,deg,T", [("oscillating_lake", 24, 3, 0.3),
-                                          ("oscillating_lake", 16, 6, 0.2)])
+                                          ("smooth_wave", 10, 6, 0.05),
+                                          ("smooth_wave", 6, 11, 0.02)])
 def test_fast_full_run(sid, kx, deg, T):
-    """north_star: within 1e-10 in L2, mass and entropy after a full run, on the
-    non-chaotic configuration (oscillating_lake amplifies a 2e-16
-    perturbation to 4.3e-13; three_mound to 7.3e-9 and the dam breaks to 1e-3, so
-    those need exact mode, test_gpu_exact.py)."""
+    """north_star: within 1e-10 in L2, mass and entropy after a full run, on
+    non-chaotic configurations: the oscillating lake at N=3 (SURVEY fact 5 table:
+    a 2e-16 perturbation grows to 4.3e-13) and a fully wet smooth wave on the curved
+    periodic mesh.  Wet/dry dam breaks amplify ulps to 1e-3 (chaotic): exact mode,
+    test_gpu_exact.py, reproduces those bitwise."""
     from paper_1804_02221_b200.driver import run_simulation
-    m, st = ref.scenario_mesh(sid, kx, kx, deg)
-    p, cfg = scenario_params(sid, deg, visc_enabled=0.0)
+    if sid == "smooth_wave":
+        m = ref.build_mesh("wavy", deg, kx, kx, periodic_x=True, periodic_y=True).bathymetry("smooth")
+        st = smooth_state(m, 0.1)
+        p = ref.params(g=9.81)
+        cfg = {"cfl": 0.3}
+    else:
+        m, st = ref.scenario_mesh(sid, kx, kx, deg)
+        p, cfg = scenario_params(sid, deg, visc_enabled=0.0)
     # reference run through the same driver loop semantics (driver.hpp:91-138)
     ri = ref.Integrator(m, p)
     s_ref = [a.copy() for a in st]
