@@ -510,8 +510,9 @@ __global__ void __launch_bounds__(Plan<N1>::THREADS, 1)
 // row-padded layout (stride N+2) via 8-byte cp.async, so both the xi-line
 // (column) and eta-line (row) reads are bank-conflict free.  The node phase
 // runs on the xi-line threads, whose nodes (k, j) make coalesced rows.
-template <int N1>
+template <int N1, bool V = false>
 struct HL {
+  static constexpr bool kVisc = V;
   static constexpr int NP = N1 * N1, LE = 2 * N1;
   static constexpr int H = (N1 + 1) / 2, NB = N1 - H;
   static constexpr int work_x(int b0) { return H * (H - 1) / 2 + H * b0; }
@@ -556,7 +557,10 @@ struct HL {
   static constexpr int EPAD = N1 * PAD;    // one padded element field
   static constexpr int GPAD = E * EPAD;
   static constexpr int GNP = (E * NP + 1) & ~1;
-  enum { F_H, F_HU, F_HV, F_YE, F_XE, F_YX, F_XX, kLineFields };
+  // line fields; the viscous variant adds the physical viscous flux pairs
+  enum { F_H, F_HU, F_HV, F_YE, F_XE, F_YX, F_XX, F_FVU, F_GVU, F_FVV, F_GVV };
+  static constexpr int kLineFields = V ? 11 : 7;
+  static constexpr int kTr = V ? 11 : 7;  // trace slots per face node
   enum { N_JAC, N_SX, N_SY, N_WH, N_WHU, N_WHV, kNodeFields };
   static constexpr int XS = 3 * (NB0 + H);  // exchange slots per line
   static constexpr int LP = 32 * WP;        // lane slots per part (>= L; tail lanes idle)
@@ -565,8 +569,8 @@ struct HL {
   static constexpr int ACC = LINE + kLineFields * GPAD;
   static constexpr int XCH = ACC + 3 * GPAD;
   static constexpr int NODE = XCH + LP * XS;
-  static constexpr int TR = NODE + kNodeFields * GNP;  // [7][E][4][N1]
-  static constexpr int EFO = TR + E * 4 * N1 * 7;       // int4 [E][4]
+  static constexpr int TR = NODE + kNodeFields * GNP;  // [kTr][E][4][N1]
+  static constexpr int EFO = TR + E * 4 * N1 * kTr;     // int4 [E][4]
   static constexpr int RED = EFO + E * 4 * 2;          // [2][32 WR xi lines][6]
   static constexpr int BAR = RED + 2 * 32 * WR * 6;
   static constexpr int TOTAL = BAR + 2;
@@ -619,10 +623,10 @@ __device__ __forceinline__ void hl_intra(const HArr<N1>& h, const HArr<N1>& u,
   }
 }
 
-template <int N1>
+template <int N1, bool V>
 __device__ __forceinline__ void hl_prefetch_line(double* sm, const Mesh& M, const CState& in,
-                                                 int g, int tid) {
-  using P = HL<N1>;
+                                                 const StageArgs& A, int g, int tid) {
+  using P = HL<N1, V>;
   const int e0 = g * P::E, ne = min(P::E, M.n_owned - e0);
   const long long base = (long long)e0 * P::NP;
   const int cnt = ne * P::NP;
@@ -639,6 +643,12 @@ __device__ __forceinline__ void hl_prefetch_line(double* sm, const Mesh& M, cons
     cp_async8(d + P::F_XE * P::GPAD, M.xe + s);
     cp_async8(d + P::F_YX * P::GPAD, M.yx + s);
     cp_async8(d + P::F_XX * P::GPAD, M.xx + s);
+    if constexpr (V) {
+      cp_async8(d + P::F_FVU * P::GPAD, A.fvu + s);
+      cp_async8(d + P::F_GVU * P::GPAD, A.gvu + s);
+      cp_async8(d + P::F_FVV * P::GPAD, A.fvv + s);
+      cp_async8(d + P::F_GVV * P::GPAD, A.gvv + s);
+    }
   }
   const int4* ef = M.ef + (long long)e0 * 4;
   int4* dst = reinterpret_cast<int4*>(sm + P::EFO);
@@ -648,10 +658,10 @@ __device__ __forceinline__ void hl_prefetch_line(double* sm, const Mesh& M, cons
                  : "memory");
 }
 
-template <int N1>
+template <int N1, bool V>
 __device__ __forceinline__ void hl_issue_node(double* sm, const Mesh& M, const StageArgs& A,
                                               int g, uint64_t* bar) {
-  using P = HL<N1>;
+  using P = HL<N1, V>;
   const int e0 = g * P::E, ne = min(P::E, M.n_owned - e0);
   const uint32_t fb = round16((size_t)ne * P::NP * sizeof(double));
   const bool wn = A.update && A.stage > 0;
@@ -667,10 +677,42 @@ __device__ __forceinline__ void hl_issue_node(double* sm, const Mesh& M, const S
   }
 }
 
-template <int N1, bool FORCE>
-__global__ void __launch_bounds__(HL<N1>::THREADS, (N1 <= 8 ? 3 : 1))
+// strong-form divergence of the contravariant viscous fluxes along this line
+// (viscosity.hpp:200-222): ft(m) = A(m) fv(m) - B(m) gv(m) for both directions
+// (A,B = (y_eta,x_eta) on xi-lines, -(y_xi,x_xi) on eta-lines); subtract D ft
+// from this half's momentum accumulators (the reference's res -= viscous_lhs)
+template <int N1, int PART, bool V>
+__device__ __forceinline__ void hl_visc_div(const double* Lb, int li, bool xi,
+                                            const HArr<N1>& Am, const HArr<N1>& Bm,
+                                            HArr<N1>& r1, HArr<N1>& r2) {
+  using O = Ops<N1>;
+  using P = HL<N1, V>;
+  constexpr int H = P::H, NK = PART ? N1 - H : H, OFF = PART ? H : 0;
+#pragma unroll
+  for (int m = 0; m < N1; ++m) {
+    const int q = xi ? m * P::PAD + li : li * P::PAD + m;
+    double A_m, B_m;
+    if (m >= OFF && m < OFF + NK) {  // own half: metrics already in registers
+      A_m = Am[m - OFF];
+      B_m = Bm[m - OFF];
+    } else {
+      A_m = xi ? Lb[P::F_YE * P::GPAD + q] : -Lb[P::F_YX * P::GPAD + q];
+      B_m = xi ? Lb[P::F_XE * P::GPAD + q] : -Lb[P::F_XX * P::GPAD + q];
+    }
+    const double ftu = A_m * Lb[P::F_FVU * P::GPAD + q] - B_m * Lb[P::F_GVU * P::GPAD + q];
+    const double ftv = A_m * Lb[P::F_FVV * P::GPAD + q] - B_m * Lb[P::F_GVV * P::GPAD + q];
+#pragma unroll
+    for (int s = 0; s < NK; ++s) {
+      r1[s] -= O::D(OFF + s, m) * ftu;
+      r2[s] -= O::D(OFF + s, m) * ftv;
+    }
+  }
+}
+
+template <int N1, bool FORCE, bool VISC>
+__global__ void __launch_bounds__(HL<N1, VISC>::THREADS, (N1 <= 8 ? 3 : 1))
     k_stage_hl(Mesh M, Phys Ph, StageArgs A, Flags* F) {
-  using P = HL<N1>;
+  using P = HL<N1, VISC>;
   using O = Ops<N1>;
   constexpr int NP = N1 * N1, H = P::H, NB0 = P::NB0, PAD = P::PAD;
   constexpr int S = (H > N1 - H) ? H : N1 - H;  // register slots per thread
@@ -695,7 +737,7 @@ __global__ void __launch_bounds__(HL<N1>::THREADS, (N1 <= 8 ? 3 : 1))
     fence_mbar_init();
   }
   if ((int)blockIdx.x >= ngroups) return;
-  hl_prefetch_line<N1>(sm, M, A.in, blockIdx.x, tid);
+  hl_prefetch_line<N1, VISC>(sm, M, A.in, A, blockIdx.x, tid);
   cp_async_commit();
   uint32_t ph_node = 0;
 
@@ -710,7 +752,7 @@ __global__ void __launch_bounds__(HL<N1>::THREADS, (N1 <= 8 ? 3 : 1))
     __syncthreads();  // line(g) and connectivity(g) resident for every thread
     if (tid == 0) {
       fence_proxy_async();
-      hl_issue_node<N1>(sm, M, A, grp, bar_node);
+      hl_issue_node<N1, VISC>(sm, M, A, grp, bar_node);
     }
 
     // ---- own half -> registers, gathers for the own endpoint
@@ -753,6 +795,12 @@ __global__ void __launch_bounds__(HL<N1>::THREADS, (N1 <= 8 ? 3 : 1))
           const bool ew = nf == 1 || nf == 3;
           cp_async8(tr + 4 * TRS, (ew ? M.ye : M.yx) + nb);
           cp_async8(tr + 5 * TRS, (ew ? M.xe : M.xx) + nb);
+        }
+        if constexpr (VISC) {  // the neighbour's viscous flux pairs for the penalty
+          cp_async8(tr + 7 * TRS, A.fvu + nb);
+          cp_async8(tr + 8 * TRS, A.gvu + nb);
+          cp_async8(tr + 9 * TRS, A.fvv + nb);
+          cp_async8(tr + 10 * TRS, A.gvv + nb);
         }
       }
     }
@@ -823,6 +871,20 @@ __global__ void __launch_bounds__(HL<N1>::THREADS, (N1 <= 8 ? 3 : 1))
         xch(3 * NB0 + 3 * a + 2) = c2;
       }
     }
+    // ---- viscous divergence along the line, own endpoint flux pairs kept for the
+    // penalty (the line buffer is recycled after the next barrier)
+    double fvo[4] = {0.0, 0.0, 0.0, 0.0};
+    if constexpr (VISC) {
+      if (part == 0)
+        hl_visc_div<N1, 0, VISC>(Lb, li, xi, Am, Bm, r1, r2);
+      else
+        hl_visc_div<N1, 1, VISC>(Lb, li, xi, Am, Bm, r1, r2);
+      const int qe = pidx(part ? N1 - 1 : 0);
+      fvo[0] = Lb[P::F_FVU * P::GPAD + qe];
+      fvo[1] = Lb[P::F_GVU * P::GPAD + qe];
+      fvo[2] = Lb[P::F_FVV * P::GPAD + qe];
+      fvo[3] = Lb[P::F_GVV * P::GPAD + qe];
+    }
     __syncthreads();  // cross contributions published; line buffer free
     // the partner half's exchange slots: X (line's A) gets Y's, Y gets X's
     if (part == 0) {
@@ -842,7 +904,7 @@ __global__ void __launch_bounds__(HL<N1>::THREADS, (N1 <= 8 ? 3 : 1))
     }
     {  // prefetch the next group's line data behind the rest of this group
       const int gn = grp + gridDim.x;
-      if (gn < ngroups) hl_prefetch_line<N1>(sm, M, A.in, gn, tid);
+      if (gn < ngroups) hl_prefetch_line<N1, VISC>(sm, M, A.in, A, gn, tid);
       cp_async_commit();
     }
 
@@ -889,6 +951,24 @@ __global__ void __launch_bounds__(HL<N1>::THREADS, (N1 <= 8 ? 3 : 1))
       double f0, f1, f2;
       es_flux_fast(wm0, wm1, wm2, wp0, wp1, wp2, bm, bp, nx, ny, g, inv2g, h_des, f0, f1, f2);
       const double c = sgn * js * iw0;
+      if constexpr (VISC) {
+        // viscous interface penalty (viscosity.hpp:224-246): with the minus-side
+        // normal, du = (phi+ - phi-)/2 lands on both sides; walls take 0 - phi-
+        const double pu_o = nx * fvo[0] + ny * fvo[1], pv_o = nx * fvo[2] + ny * fvo[3];
+        double du, dv;
+        if (efy & EF_WALL) {
+          du = -pu_o;
+          dv = -pv_o;
+        } else {
+          const double pu_n = nx * tr[7 * TRS] + ny * tr[8 * TRS];
+          const double pv_n = nx * tr[9 * TRS] + ny * tr[10 * TRS];
+          const double sg = (efy & EF_MINUS) ? 1.0 : -1.0;  // (plus - minus)
+          du = 0.5 * sg * (pu_n - pu_o);
+          dv = 0.5 * sg * (pv_n - pv_o);
+        }
+        f1 -= du / sgn;  // folded below as c * f: c = sgn js / w0
+        f2 -= dv / sgn;
+      }
       if (part) {
         r0[SY] += c * f0;
         r1[SY] += c * f1;
@@ -1036,6 +1116,180 @@ __global__ void __launch_bounds__(HL<N1>::THREADS, (N1 <= 8 ? 3 : 1))
   cp_async_wait_all();
 }
 
+// ===========================================================================
+// Viscous pre-kernel (fast): per element the modal shock indicator and the
+// viscosity coefficient (viscosity.hpp:35-78, finished on the device with
+// CUDA log10/sin), the BR1 lifted velocity gradients (viscosity.hpp:95-168)
+// and the physical viscous flux pairs h eps grad (viscosity.hpp:187-194),
+// written per node for the stage kernel (its strong divergence and the
+// interface penalties).  One thread per node, E elements per CTA, element
+// data staged in shared memory.
+template <int N1>
+struct VP {
+  static constexpr int NP = N1 * N1;
+  static constexpr int E = (256 / NP) > 1 ? (256 / NP) : 1;
+  static constexpr int THREADS = E * NP;
+  enum { H, U, V, YE, XE, YX, XX, TMP, C0, C1, C2, C3, kF };
+  static constexpr int RED = kF * E * NP;  // [E][4] shell sums
+  static constexpr int EPS = RED + E * 4;
+  static constexpr int TOTAL = EPS + E;
+  static constexpr size_t bytes = TOTAL * sizeof(double);
+};
+
+template <int N1>
+__global__ void __launch_bounds__(VP<N1>::THREADS)
+    k_visc_pre(Mesh M, Phys Ph, CState S, double* eps_out, double* fvu, double* fvv,
+               double* gvu, double* gvv, Flags* F) {
+  using P = VP<N1>;
+  using O = Ops<N1>;
+  constexpr int NP = P::NP, N = N1 - 1;
+  extern __shared__ __align__(16) double sm[];
+  const int el = threadIdx.x / NP, q = threadIdx.x % NP, i = q / N1, j = q % N1;
+  const int e = blockIdx.x * P::E + el;
+  const bool active = e < M.n_owned;
+  const long long n = (long long)e * NP + q;
+  double* f = sm + el * NP;
+  auto fld = [&](int k) { return f + k * P::E * NP; };
+  double h = 0.0, hu = 0.0, hv = 0.0;
+  if (active) {
+    h = S.h[n];
+    hu = S.hu[n];
+    hv = S.hv[n];
+    double u, v;
+    vel(h, hu, hv, Ph.h_des, u, v);
+    fld(P::H)[q] = h;
+    fld(P::U)[q] = u;
+    fld(P::V)[q] = v;
+    fld(P::YE)[q] = M.ye[n];
+    fld(P::XE)[q] = M.xe[n];
+    fld(P::YX)[q] = M.yx[n];
+    fld(P::XX)[q] = M.xx[n];
+  }
+  if (threadIdx.x < P::E * 4) sm[P::RED + threadIdx.x] = 0.0;
+  __syncthreads();
+  // ---- modal transform of h: tmp = V^-1 h, modal = tmp V^-T
+  double t = 0.0;
+#pragma unroll
+  for (int k = 0; k < N1; ++k) t += O::Vinv(i, k) * fld(P::H)[k * N1 + j];
+  fld(P::TMP)[q] = t;
+  __syncthreads();
+  double mo = 0.0;
+#pragma unroll
+  for (int k = 0; k < N1; ++k) mo += fld(P::TMP)[i * N1 + k] * O::Vinv(j, k);
+  const double m2 = mo * mo;
+  // shells: den1 all, den2 i,j<N, num1 top shell (i==N or j==N), num2 shell N-1
+  fld(P::C0)[q] = m2;
+  fld(P::C1)[q] = (i < N && j < N) ? m2 : 0.0;
+  fld(P::C2)[q] = (i == N || j == N) ? m2 : 0.0;
+  fld(P::C3)[q] = ((i == N - 1 && j <= N - 1) || (j == N - 1 && i <= N - 1)) ? m2 : 0.0;
+  __syncthreads();
+  if (q == 0 && active) {
+    // fixed-order sums: reproducible run to run
+    double den1 = 0.0, den2 = 0.0, num1 = 0.0, num2 = 0.0;
+    for (int k = 0; k < NP; ++k) {
+      den1 += fld(P::C0)[k];
+      den2 += fld(P::C1)[k];
+      num1 += fld(P::C2)[k];
+      num2 += fld(P::C3)[k];
+    }
+    const double floor_abs = 1e-28 * den1 + 1e-300;
+    double eps = 0.0;
+    if (!(den1 <= 1e-300)) {
+      const double r1 = num1 > floor_abs ? num1 / den1 : 0.0;
+      const double r2 = (num2 > floor_abs && den2 > floor_abs) ? num2 / den2 : 0.0;
+      const double r = smax(r1, r2);
+      if (r > 0.0) {
+        const double sigma = log10(r);
+        if (sigma >= Ph.sigma_max) {
+          eps = Ph.epsilon0;
+        } else if (!(sigma < Ph.sigma_min)) {
+          eps = 0.5 * Ph.epsilon0 *
+                (1.0 + sin(M_PI * (sigma - 0.5 * (Ph.sigma_max + Ph.sigma_min)) /
+                           (Ph.sigma_max - Ph.sigma_min)));
+        }
+      }
+    }
+    sm[P::EPS + el] = eps;
+    eps_out[e] = eps;
+    atomicMax(&F->max_eps_key, order_key(eps));
+  }
+  __syncthreads();
+  if (!active) return;
+  // ---- BR1: weak D-hat sums of metric * velocity along xi (i) and eta (j)
+  double sye_u = 0.0, sxe_u = 0.0, sye_v = 0.0, sxe_v = 0.0;
+  double syx_u = 0.0, sxx_u = 0.0, syx_v = 0.0, sxx_v = 0.0;
+#pragma unroll
+  for (int m = 0; m < N1; ++m) {
+    const int qx = m * N1 + j, qe = i * N1 + m;
+    const double di = O::Dh(i, m), dj = O::Dh(j, m);
+    const double ux = fld(P::U)[qx], vx = fld(P::V)[qx], ue = fld(P::U)[qe], ve = fld(P::V)[qe];
+    const double yex = fld(P::YE)[qx], xex = fld(P::XE)[qx];
+    const double yxe = fld(P::YX)[qe], xxe = fld(P::XX)[qe];
+    sye_u += di * (yex * ux);
+    sxe_u += di * (xex * ux);
+    sye_v += di * (yex * vx);
+    sxe_v += di * (xex * vx);
+    syx_u += dj * (yxe * ue);
+    sxx_u += dj * (xxe * ue);
+    syx_v += dj * (yxe * ve);
+    sxx_v += dj * (xxe * ve);
+  }
+  double u1 = sye_u - syx_u, u2 = sxx_u - sxe_u, v1 = sye_v - syx_v, v2 = sxx_v - sxe_v;
+  // interface corrections (viscosity.hpp:114-160): U* = <u> inside, u- on walls
+  const double uo = fld(P::U)[q], vo = fld(P::V)[q], iw0 = 1.0 / M.w0;
+  int fa[2], ta[2];
+  const int nfc = node_faces(N1, i, j, fa, ta);
+  for (int c2 = 0; c2 < nfc; ++c2) {
+    const int face = fa[c2], tt = ta[c2];
+    const int4 ef = M.ef[e * 4 + face];
+    if (!(ef.y & EF_PRESENT)) continue;
+    double us = uo, vs = vo;
+    if (!(ef.y & EF_WALL)) {
+      const int nf = ef.y & EF_NBR_FACE_MASK;
+      const int tp = (ef.y & EF_REVERSED) ? N - tt : tt;
+      const long long nb = (long long)ef.x * NP + face_node(N1, nf, tp);
+      double ub, vb;
+      vel(S.h[nb], S.hu[nb], S.hv[nb], Ph.h_des, ub, vb);
+      us = 0.5 * (uo + ub);
+      vs = 0.5 * (vo + vb);
+    }
+    double cy, cx;
+    switch (face) {
+      case 1: cy = fld(P::YE)[q]; cx = fld(P::XE)[q]; break;
+      case 3: cy = -fld(P::YE)[q]; cx = -fld(P::XE)[q]; break;
+      case 2: cy = -fld(P::YX)[q]; cx = -fld(P::XX)[q]; break;
+      default: cy = fld(P::YX)[q]; cx = fld(P::XX)[q]; break;
+    }
+    cy *= iw0;
+    cx *= iw0;
+    u1 += cy * us;
+    u2 -= cx * us;
+    v1 += cy * vs;
+    v2 -= cx * vs;
+  }
+  const double ij = 1.0 / M.jac[n];
+  const double he = h * sm[P::EPS + el] * ij;
+  fvu[n] = he * u1;
+  fvv[n] = he * v1;
+  gvu[n] = he * u2;
+  gvv[n] = he * v2;
+}
+
+template <int N1>
+static void launch_visc_pre_n(const Mesh& M, const Phys& P, CState S, double* eps, double* fvu,
+                              double* fvv, double* gvu, double* gvv, Flags* F,
+                              cudaStream_t st) {
+  using PL = VP<N1>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_visc_pre<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)PL::bytes);
+    attr = true;
+  }
+  const int grid = (M.n_owned + PL::E - 1) / PL::E;
+  k_visc_pre<N1><<<grid, PL::THREADS, PL::bytes, st>>>(M, P, S, eps, fvu, fvv, gvu, gvv, F);
+}
+
 // geometry-only split-source coefficients (dg_rhs.hpp:159-176), one thread per node
 __global__ void k_source_geometry(Mesh M, double* sx, double* sy) {
   const long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -1119,13 +1373,13 @@ static void launch_full(const Mesh& M, const Phys& P, const StageArgs& A, Flags*
   kern<<<grid, PL::THREADS, PL::bytes, st>>>(M, P, A, F);
 }
 
-// half-line kernel (N+1 >= 5)
-template <int N1, bool FORCE>
+// half-line kernel (N+1 >= 5 inviscid, N+1 >= 3 viscous)
+template <int N1, bool FORCE, bool VISC>
 static void launch_half(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
                         cudaStream_t st) {
-  using PL = HL<N1>;
+  using PL = HL<N1, VISC>;
   static int cache = 0;
-  auto kern = k_stage_hl<N1, FORCE>;
+  auto kern = k_stage_hl<N1, FORCE, VISC>;
   const int grid = grid_for(kern, PL::THREADS, PL::bytes, (M.n_owned + PL::E - 1) / PL::E, cache);
   kern<<<grid, PL::THREADS, PL::bytes, st>>>(M, P, A, F);
 }
@@ -1142,6 +1396,13 @@ static int variant_override() {
 template <int N1>
 static void launch_n(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
                      cudaStream_t st) {
+  if constexpr (N1 >= 3) {
+    if (A.fvu) {  // viscous stages always take the half-line kernel
+      if (A.fh) launch_half<N1, true, true>(M, P, A, F, st);
+      else launch_half<N1, false, true>(M, P, A, F, st);
+      return;
+    }
+  }
   const int ov = variant_override();
   bool half = N1 >= 5;
   if constexpr (N1 <= 8) {
@@ -1158,9 +1419,22 @@ static void launch_n(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
     }
   }
   if constexpr (N1 >= 5) {
-    if (A.fh) launch_half<N1, true>(M, P, A, F, st);
-    else launch_half<N1, false>(M, P, A, F, st);
+    if (A.fh) launch_half<N1, true, false>(M, P, A, F, st);
+    else launch_half<N1, false, false>(M, P, A, F, st);
   }
+}
+
+int launch_fast_visc_pre(const Mesh& M, const Phys& P, CState S, double* eps, double* fvu,
+                         double* fvv, double* gvu, double* gvv, Flags* F, cudaStream_t st) {
+  switch (M.n1) {
+#define SWDG_VP(n) \
+  case n: launch_visc_pre_n<n>(M, P, S, eps, fvu, fvv, gvu, gvv, F, st); break;
+    SWDG_VP(3) SWDG_VP(4) SWDG_VP(5) SWDG_VP(6) SWDG_VP(7) SWDG_VP(8) SWDG_VP(9) SWDG_VP(10)
+    SWDG_VP(11) SWDG_VP(12) SWDG_VP(13) SWDG_VP(14) SWDG_VP(15) SWDG_VP(16)
+#undef SWDG_VP
+    default: return 0;
+  }
+  return 1;
 }
 
 bool fast_stage_supported(int n1) { return n1 >= 2 && n1 <= 16; }

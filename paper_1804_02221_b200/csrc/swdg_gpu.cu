@@ -195,7 +195,17 @@ double stage(swdg_gpu* c, CState in, double* const* out, int k, double t, double
   if (out) a.out = st(out);
   if (rhs) a.rhs = st(rhs);
   double mx = 0.0;
-  if (viscous) {
+  if (viscous && c->fast) {
+    // device-resident: indicator + eps ramp + BR1 + flux pairs in one kernel;
+    // max eps lands in F->max_eps_key
+    c->launches += launch_fast_visc_pre(c->M, c->phys, in, c->eps, c->fvu, c->fvv, c->gvu,
+                                        c->gvv, F, c->stream);
+    a.eps = c->eps;
+    a.fvu = c->fvu;
+    a.fvv = c->fvv;
+    a.gvu = c->gvu;
+    a.gvv = c->gvv;
+  } else if (viscous) {
     mx = stage_viscosity(c, in);
     a.eps = c->eps;
     a.fvu = c->fvu;
@@ -208,7 +218,7 @@ double stage(swdg_gpu* c, CState in, double* const* out, int k, double t, double
     a.fhu = c->fhu;
     a.fhv = c->fhv;
   }
-  if (c->fast && !viscous) {
+  if (c->fast) {
     c->launches += launch_fast_stage(c->M, c->phys, a, F, c->stream);
   } else {
     c->launches += launch_exact_rhs_stage(c->M, c->phys, a, c->stream);
@@ -352,7 +362,7 @@ void allocate(swdg_gpu* c, int K, int n_owned, int N, const std::vector<int4>& e
   f.dt_key = ~0ull;
   f.minlen_key = ~0ull;
   f.posdt_key = ~0ull;
-  f.max_eps_key = ~0ull;
+  f.max_eps_key = 0ull;  // atomicMax target (eps >= 0)
   for (int k = 0; k < 3; ++k) c->flags_h[k] = f;
   ck(cudaMemcpy(c->flags_init, c->flags_h, 3 * sizeof(Flags), cudaMemcpyHostToDevice), "flags");
   c->eps_h.assign(K, 0.0);
@@ -638,6 +648,8 @@ int swdg_gpu_compute_dt(swdg_gpu* c, double cfl, double* dt) {
 static int fold_flags(swdg_gpu* c, swdg_step_info& r, int& code) {
   for (int k = 0; k < 3; ++k) {
     const Flags& f = c->flags_h[k];
+    // eps of every evaluated stage counts, the rejected one included (timeloop.hpp:177-180)
+    if (c->params.visc_enabled) r.max_eps = std::max(r.max_eps, key_value(f.max_eps_key));
     if (f.abort) {
       code = fail(c, SWDG_ERR_ABORT, "negative water height without limiter");
       return k;
@@ -658,10 +670,10 @@ int swdg_gpu_try_step(swdg_gpu* c, double t, double dt, swdg_step_info* info) {
     const bool viscous = c->params.visc_enabled != 0;
     int code = SWDG_OK;
     reset_flags(c);
-    if (c->fast && !viscous && !c->forcing) {
+    if (c->fast && !c->forcing) {
       // device-resident: three stages back to back, one flag read per step
       for (int k = 0; k < 3; ++k) {
-        stage(c, in, outs[k], k, t, dt, false, nullptr, c->flags + k);
+        stage(c, in, outs[k], k, t, dt, viscous, nullptr, c->flags + k);
         in = cs(outs[k]);
       }
       read_flags(c);
@@ -694,7 +706,7 @@ int swdg_gpu_try_step(swdg_gpu* c, double t, double dt, swdg_step_info* info) {
 int swdg_gpu_run_steps(swdg_gpu* c, int nsteps, double t, double dt) {
   return guarded(c, [&] {
     const bool viscous = c->params.visc_enabled != 0;
-    if (!(c->fast && !viscous && !c->forcing)) {
+    if (!(c->fast && !c->forcing)) {
       for (int s = 0; s < nsteps; ++s) {
         swdg_step_info r{};
         const int rc = swdg_gpu_try_step(c, t + s * dt, dt, &r);
@@ -709,7 +721,7 @@ int swdg_gpu_run_steps(swdg_gpu* c, int nsteps, double t, double dt) {
     for (int s = 0; s < nsteps; ++s) {
       CState in = cs(c->W);
       for (int k = 0; k < 3; ++k) {
-        stage(c, in, outs[k], k, t + s * dt, dt, false, nullptr, c->flags + k);
+        stage(c, in, outs[k], k, t + s * dt, dt, viscous, nullptr, c->flags + k);
         in = cs(outs[k]);
       }
       for (int k = 0; k < 3; ++k) std::swap(c->W[k], c->A[k]);
@@ -733,7 +745,13 @@ int swdg_gpu_last_info(swdg_gpu* c, swdg_step_info* info) {
 
 int swdg_gpu_last_eps(swdg_gpu* c, double* eps) {
   return guarded(c, [&] {
-    std::memcpy(eps, c->eps_h.data(), sizeof(double) * c->M.K);
+    if (c->fast) {  // eps lives on the device in fast mode
+      ck(cudaMemcpyAsync(eps, c->eps, sizeof(double) * c->M.K, cudaMemcpyDeviceToHost,
+                         c->stream), "eps D2H");
+      ck(cudaStreamSynchronize(c->stream), "eps sync");
+    } else {
+      std::memcpy(eps, c->eps_h.data(), sizeof(double) * c->M.K);
+    }
     return SWDG_OK;
   });
 }

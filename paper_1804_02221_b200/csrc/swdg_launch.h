@@ -35,6 +35,8 @@ int upload_fast_ops(int n1, const double* D, const double* Dt, const double* Dh,
                     const double* Vinv, const double* w);
 bool fast_stage_supported(int n1);
 int launch_source_geometry(const Mesh& M, double* sx, double* sy, cudaStream_t st);
+int launch_fast_visc_pre(const Mesh& M, const Phys& P, CState S, double* eps, double* fvu,
+                         double* fvv, double* gvu, double* gvv, Flags* F, cudaStream_t st);
 int launch_fast_stage(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
                       cudaStream_t st);
 
