@@ -138,8 +138,10 @@ const char* swdg_gpu_create_error(void);
 void swdg_gpu_destroy(swdg_gpu* ctx);
 const char* swdg_gpu_last_error(const swdg_gpu* ctx);
 
-/* Run every launch of this context on `stream` (a cudaStream_t); NULL = the
- * context's own stream. */
+/* Run every launch and copy of this context on `stream` (a cudaStream_t; NULL
+ * is the legacy default stream).  A new context uses its own non-blocking
+ * stream; callers that order the context against their own work (CUDA events,
+ * NCCL, torch) pass their stream here. */
 int swdg_gpu_set_stream(swdg_gpu* ctx, void* stream);
 int swdg_gpu_synchronize(swdg_gpu* ctx);
 
@@ -217,6 +219,31 @@ int swdg_gpu_create_structured(const swdg_structured_spec* spec, const swdg_para
 
 /* Copy a device geometry array ("y_eta", "jac", "b", "face_nx", "x", ...) to host. */
 int swdg_gpu_download_geometry(swdg_gpu* ctx, const char* name, double* out);
+
+/* ---- partitioned (multi-GPU) runs ----------------------------------------
+ * The reference has no decomposition; a partition is a mesh view whose
+ * elements [n_owned, n_elem) are ghost copies of off-rank neighbours
+ * (paper_1804_02221_b200/partition.py builds them).  Between stages the caller
+ * moves face-node data between ranks (NCCL): pack -> send/recv -> unpack.
+ *
+ * halo_setup: local node ids to send (owner side) and to fill (ghost side),
+ * concatenated over peers in the partition plan's order.
+ * halo_pack/unpack: what 0 = stage k's input state (3 doubles per node,
+ * node-major), what 1 = the viscous flux pairs (4 doubles per node); buffers
+ * are device memory owned by the caller.
+ * The split step: step_begin; for k in 0..2 { [exchange state]; stage_visc;
+ * [exchange flux pairs]; stage_run }; step_flags (local reject/abort, sync);
+ * the caller reduces them over ranks; step_commit(accept). */
+int swdg_gpu_halo_setup(swdg_gpu* ctx, int64_t n_send, const int32_t* send_idx, int64_t n_recv,
+                        const int32_t* recv_idx);
+int swdg_gpu_halo_pack(swdg_gpu* ctx, int what, int stage, double* send_buf);
+int swdg_gpu_halo_unpack(swdg_gpu* ctx, int what, int stage, const double* recv_buf);
+int swdg_gpu_dt_candidates(swdg_gpu* ctx, double* dt_min, double* min_len);
+int swdg_gpu_step_begin(swdg_gpu* ctx);
+int swdg_gpu_stage_visc(swdg_gpu* ctx, int stage, double t, double dt);
+int swdg_gpu_stage_run(swdg_gpu* ctx, int stage, double t, double dt);
+int swdg_gpu_step_flags(swdg_gpu* ctx, int32_t* reject, int32_t* abort);
+int swdg_gpu_step_commit(swdg_gpu* ctx, int accept, swdg_step_info* info);
 
 #ifdef __cplusplus
 }

@@ -26,9 +26,19 @@ __device__ __forceinline__ void velocity(double h, double hu, double hv, double 
   }
 }
 
+__device__ __forceinline__ double elem_sums(const Mesh& M, const Phys& P, const CState& S,
+                                            double* partial, int e);
+
 __global__ void k_elem_sums(Mesh M, Phys P, CState S, double* partial, Flags* F) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= M.n_owned) return;
+  unsigned long long key = ~0ull;
+  if (e < M.n_owned) key = order_key(elem_sums(M, P, S, partial, e));
+  key = warp_min_key(key);
+  if ((threadIdx.x & 31) == 0) atomicMin(&F->min_h_key, key);
+}
+
+__device__ __forceinline__ double elem_sums(const Mesh& M, const Phys& P, const CState& S,
+                                            double* partial, int e) {
   const int n1 = M.n1;
   const long long b = (long long)e * M.np;
   double mass = 0.0, ent = 0.0, mn = S.h[b];
@@ -46,7 +56,7 @@ __global__ void k_elem_sums(Mesh M, Phys P, CState S, double* partial, Flags* F)
     }
   partial[2 * e] = mass;
   partial[2 * e + 1] = ent;
-  atomicMin(&F->min_h_key, order_key(mn));
+  return mn;
 }
 
 __global__ void k_sum_partials(const double* partial, int K, double* out2) {
@@ -76,15 +86,26 @@ __global__ void k_sum_partials(const double* partial, int K, double* out2) {
 // positivity_dt_bounds (limiter.hpp:107-130) evaluated by every owned
 // element-face node from its own side (the reference evaluates the minus side
 // and, for interior faces, the plus side with the plus normal: the same set).
+__device__ __forceinline__ double posdt_bound(const Mesh& M, const Phys& P, const CState& S,
+                                               long long idx);
+
 __global__ void k_posdt(Mesh M, Phys P, CState S, Flags* F) {
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  unsigned long long key = ~0ull;
+  if (idx < (long long)M.n_owned * 4 * M.n1) key = order_key(posdt_bound(M, P, S, idx));
+  key = warp_min_key(key);  // one atomic per warp
+  if ((threadIdx.x & 31) == 0) atomicMin(&F->posdt_key, key);
+}
+
+__device__ __forceinline__ double posdt_bound(const Mesh& M, const Phys& P, const CState& S,
+                                               long long idx) {
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
   const int n1 = M.n1;
-  if (idx >= (long long)M.n_owned * 4 * n1) return;
   const int t = (int)(idx % n1);
   const int face = (int)((idx / n1) % 4);
   const int e = (int)(idx / (4 * n1));
   const int4 ef = M.ef[e * 4 + face];
-  if (!(ef.y & EF_PRESENT)) return;
+  if (!(ef.y & EF_PRESENT)) return inf;
   const long long n = (long long)e * M.np + face_node(n1, face, t);
   const double nx = M.fnx[idx], ny = M.fny[idx], a_scale = M.fa[idx];
   const double hm = S.h[n], hum = S.hu[n], hvm = S.hv[n];
@@ -111,15 +132,53 @@ __global__ void k_posdt(Mesh M, Phys P, CState S, Flags* F) {
   const double a = fabs(uavg + cavg) + fabs(uavg - cavg);
   const double bb = fabs(uavg + cavg) - fabs(uavg - cavg);
   const double den1 = a + 2.0 * uavg;
-  const double inf = __longlong_as_double(0x7ff0000000000000ll);
   double bound = den1 > 1e-300 ? M.w0 * a_scale / den1 : inf;
   const double jump = unp - unm;
   if (hm > 0.0 && bb * jump < 0.0)
     bound = smin(bound, fabs(M.w0 * a_scale * P.g * hm / (cavg * bb * jump)));
-  atomicMin(&F->posdt_key, order_key(bound));
+  return bound;
+}
+
+// halo pack/unpack: node-major [i][field] so each peer's block is contiguous
+__global__ void k_halo_pack(const int* idx, long long n, int nf, const double* f0,
+                            const double* f1, const double* f2, const double* f3, double* buf) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long k = idx[i];
+  buf[i * nf + 0] = f0[k];
+  buf[i * nf + 1] = f1[k];
+  buf[i * nf + 2] = f2[k];
+  if (nf > 3) buf[i * nf + 3] = f3[k];
+}
+
+__global__ void k_halo_unpack(const int* idx, long long n, int nf, double* f0, double* f1,
+                              double* f2, double* f3, const double* buf) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long k = idx[i];
+  f0[k] = buf[i * nf + 0];
+  f1[k] = buf[i * nf + 1];
+  f2[k] = buf[i * nf + 2];
+  if (nf > 3) f3[k] = buf[i * nf + 3];
 }
 
 }  // namespace
+
+int launch_halo_pack(const int* idx, long long n, int nf, const double* const* f, double* buf,
+                     cudaStream_t st) {
+  if (n == 0) return 0;
+  k_halo_pack<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(idx, n, nf, f[0], f[1], f[2],
+                                                          nf > 3 ? f[3] : f[0], buf);
+  return 1;
+}
+
+int launch_halo_unpack(const int* idx, long long n, int nf, double* const* f, const double* buf,
+                       cudaStream_t st) {
+  if (n == 0) return 0;
+  k_halo_unpack<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(idx, n, nf, f[0], f[1], f[2],
+                                                            nf > 3 ? f[3] : f[0], buf);
+  return 1;
+}
 
 int launch_diagnostics(const Mesh& M, const Phys& P, CState S, double* partial, double* out2,
                        Flags* F, cudaStream_t st) {

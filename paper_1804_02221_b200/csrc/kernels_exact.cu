@@ -514,18 +514,27 @@ __global__ void k_limit(Mesh M, Phys P, State S, Flags* F) {
 // the lengths 2J/hypot(.) come precomputed by the host with std::hypot.
 __global__ void k_dt(Mesh M, Phys P, CState S, Flags* F) {
   const long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (n >= (long long)M.n_owned * M.np) return;
-  const double order = 2.0 * M.degree + 1.0;
-  double u, v;
-  velocity(S.h[n], S.hu[n], S.hv[n], P.h_des, u, v);
-  const double c = sqrt(P.g * smax(S.h[n], 0.0));
-  const double lxi = M.len_xi[n], leta = M.len_eta[n];
-  double dt = __longlong_as_double(0x7ff0000000000000ll);
-  const double lx = fabs(u) + c, ly = fabs(v) + c;
-  if (lx > 1e-14) dt = smin(dt, lxi / (order * lx));
-  if (ly > 1e-14) dt = smin(dt, leta / (order * ly));
-  atomicMin(&F->dt_key, order_key(dt));
-  atomicMin(&F->minlen_key, order_key(smin(lxi, leta)));
+  unsigned long long kdt = ~0ull, klen = ~0ull;
+  if (n < (long long)M.n_owned * M.np) {
+    const double order = 2.0 * M.degree + 1.0;
+    double u, v;
+    velocity(S.h[n], S.hu[n], S.hv[n], P.h_des, u, v);
+    const double c = sqrt(P.g * smax(S.h[n], 0.0));
+    const double lxi = M.len_xi[n], leta = M.len_eta[n];
+    double dt = __longlong_as_double(0x7ff0000000000000ll);
+    const double lx = fabs(u) + c, ly = fabs(v) + c;
+    if (lx > 1e-14) dt = smin(dt, lxi / (order * lx));
+    if (ly > 1e-14) dt = smin(dt, leta / (order * ly));
+    kdt = order_key(dt);
+    klen = order_key(smin(lxi, leta));
+  }
+  // min is exact: reduce per warp, one atomic per warp
+  kdt = warp_min_key(kdt);
+  klen = warp_min_key(klen);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&F->dt_key, kdt);
+    atomicMin(&F->minlen_key, klen);
+  }
 }
 
 }  // namespace

@@ -1183,15 +1183,21 @@ __global__ void __launch_bounds__(VP<N1>::THREADS)
   fld(P::C2)[q] = (i == N || j == N) ? m2 : 0.0;
   fld(P::C3)[q] = ((i == N - 1 && j <= N - 1) || (j == N - 1 && i <= N - 1)) ? m2 : 0.0;
   __syncthreads();
-  if (q == 0 && active) {
-    // fixed-order sums: reproducible run to run
-    double den1 = 0.0, den2 = 0.0, num1 = 0.0, num2 = 0.0;
-    for (int k = 0; k < NP; ++k) {
-      den1 += fld(P::C0)[k];
-      den2 += fld(P::C1)[k];
-      num1 += fld(P::C2)[k];
-      num2 += fld(P::C3)[k];
+  // fixed-shape tree over the element's nodes: parallel and reproducible
+  constexpr int P2 = NP <= 4 ? 4 : NP <= 16 ? 16 : NP <= 64 ? 64 : NP <= 128 ? 128 : 256;
+#pragma unroll
+  for (int s = P2 / 2; s > 0; s >>= 1) {
+    if (q < s && q + s < NP) {
+      fld(P::C0)[q] += fld(P::C0)[q + s];
+      fld(P::C1)[q] += fld(P::C1)[q + s];
+      fld(P::C2)[q] += fld(P::C2)[q + s];
+      fld(P::C3)[q] += fld(P::C3)[q + s];
     }
+    __syncthreads();
+  }
+  if (q == 0 && active) {
+    const double den1 = fld(P::C0)[0], den2 = fld(P::C1)[0];
+    const double num1 = fld(P::C2)[0], num2 = fld(P::C3)[0];
     const double floor_abs = 1e-28 * den1 + 1e-300;
     double eps = 0.0;
     if (!(den1 <= 1e-300)) {

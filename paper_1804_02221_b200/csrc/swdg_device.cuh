@@ -74,6 +74,18 @@ __host__ __device__ inline double key_value(unsigned long long k) {
   return *reinterpret_cast<const double*>(&b);
 }
 
+#ifdef __CUDACC__
+// warp-level min of order keys: one atomic per warp instead of one per thread
+// (min is exact and order-independent)
+__device__ __forceinline__ unsigned long long warp_min_key(unsigned long long k) {
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long other = __shfl_xor_sync(0xffffffffu, k, o);
+    k = other < k ? other : k;
+  }
+  return k;
+}
+#endif
+
 // node (i,j) of local face `face` at position t (core.hpp:53-61)
 __host__ __device__ inline int face_node(int n1, int face, int t) {
   switch (face) {

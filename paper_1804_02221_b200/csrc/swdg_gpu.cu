@@ -76,6 +76,12 @@ struct swdg_gpu {
   void* forcing_user = nullptr;
   swdg_step_info last{};
 
+  // partitioned runs: halo node lists (device) and the split-step state
+  int* send_idx = nullptr;
+  int* recv_idx = nullptr;
+  long long n_send = 0, n_recv = 0;
+  double split_max_eps = 0.0;
+
   template <class T>
   T* dalloc(size_t count) {
     void* p = nullptr;
@@ -181,8 +187,22 @@ bool stage_forcing(swdg_gpu* c, double ts) {
 
 // dW/dt of `in` (+ optional stage update into `out`, limiter into flags[k]).
 // Returns max eps.
-double stage(swdg_gpu* c, CState in, double* const* out, int k, double t, double dt,
-             bool viscous, double* const* rhs, Flags* F) {
+// Viscous pre-pass of a stage input: eps, BR1 gradients and the flux pairs into
+// c->fvu.. (fast: one device kernel, max eps into F; exact: indicator on the
+// device, ramp on the host).  Returns the host-side max eps (exact mode).
+double stage_visc(swdg_gpu* c, CState in, Flags* F) {
+  if (c->fast) {
+    c->launches += launch_fast_visc_pre(c->M, c->phys, in, c->eps, c->fvu, c->fvv, c->gvu,
+                                        c->gvv, F, c->stream);
+    return 0.0;
+  }
+  return stage_viscosity(c, in);
+}
+
+// The stage proper: dW/dt of `in` (+ update into `out` and the limiter/reject
+// flags in F), consuming the flux pairs of a preceding stage_visc.
+void stage_main(swdg_gpu* c, CState in, double* const* out, int k, double t, double dt,
+                bool viscous, double* const* rhs, Flags* F) {
   StageArgs a{};
   a.in = in;
   a.wn = cs(c->W);
@@ -194,19 +214,7 @@ double stage(swdg_gpu* c, CState in, double* const* out, int k, double t, double
   a.update = out != nullptr;
   if (out) a.out = st(out);
   if (rhs) a.rhs = st(rhs);
-  double mx = 0.0;
-  if (viscous && c->fast) {
-    // device-resident: indicator + eps ramp + BR1 + flux pairs in one kernel;
-    // max eps lands in F->max_eps_key
-    c->launches += launch_fast_visc_pre(c->M, c->phys, in, c->eps, c->fvu, c->fvv, c->gvu,
-                                        c->gvv, F, c->stream);
-    a.eps = c->eps;
-    a.fvu = c->fvu;
-    a.fvv = c->fvv;
-    a.gvu = c->gvu;
-    a.gvv = c->gvv;
-  } else if (viscous) {
-    mx = stage_viscosity(c, in);
+  if (viscous) {
     a.eps = c->eps;
     a.fvu = c->fvu;
     a.fvv = c->fvv;
@@ -224,6 +232,12 @@ double stage(swdg_gpu* c, CState in, double* const* out, int k, double t, double
     c->launches += launch_exact_rhs_stage(c->M, c->phys, a, c->stream);
     if (out) c->launches += launch_exact_limit(c->M, c->phys, st(out), F, c->stream);
   }
+}
+
+double stage(swdg_gpu* c, CState in, double* const* out, int k, double t, double dt,
+             bool viscous, double* const* rhs, Flags* F) {
+  const double mx = viscous ? stage_visc(c, in, F) : 0.0;
+  stage_main(c, in, out, k, t, dt, viscous, rhs, F);
   return mx;
 }
 
@@ -524,12 +538,9 @@ int swdg_gpu_set_stream(swdg_gpu* c, void* stream) {
       c->own_stream = false;
       c->stream = nullptr;
     }
-    if (stream) {
-      c->stream = static_cast<cudaStream_t>(stream);
-    } else {
-      ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
-      c->own_stream = true;
-    }
+    // the caller's stream, NULL included (the legacy default stream): kernels,
+    // copies and the caller's own work (NCCL, events) are then stream-ordered
+    c->stream = static_cast<cudaStream_t>(stream);
     return SWDG_OK;
   });
 }
@@ -790,5 +801,147 @@ int swdg_gpu_set_forcing(swdg_gpu* c, swdg_forcing_fn fn, void* user) {
 }
 
 int64_t swdg_gpu_launch_count(const swdg_gpu* c) { return c ? c->launches : 0; }
+
+// ---- partitioned runs: halo exchange hooks and the split SSPRK3 step -------
+
+int swdg_gpu_halo_setup(swdg_gpu* c, int64_t n_send, const int32_t* send_idx, int64_t n_recv,
+                        const int32_t* recv_idx) {
+  return guarded(c, [&] {
+    const long long lim = c->nn;
+    for (int64_t i = 0; i < n_send; ++i)
+      if (send_idx[i] < 0 || send_idx[i] >= lim) throw InputError{"halo: send index out of range"};
+    for (int64_t i = 0; i < n_recv; ++i)
+      if (recv_idx[i] < 0 || recv_idx[i] >= lim) throw InputError{"halo: recv index out of range"};
+    c->send_idx = c->dalloc<int>(n_send);
+    c->recv_idx = c->dalloc<int>(n_recv);
+    if (n_send)
+      ck(cudaMemcpy(c->send_idx, send_idx, n_send * sizeof(int), cudaMemcpyHostToDevice), "send idx");
+    if (n_recv)
+      ck(cudaMemcpy(c->recv_idx, recv_idx, n_recv * sizeof(int), cudaMemcpyHostToDevice), "recv idx");
+    c->n_send = n_send;
+    c->n_recv = n_recv;
+    return SWDG_OK;
+  });
+}
+
+static double* const* stage_input(swdg_gpu* c, int k) {
+  return k == 0 ? c->W : (k == 1 ? c->A : c->B);
+}
+static double* const* stage_output(swdg_gpu* c, int k) { return k == 1 ? c->B : c->A; }
+
+// what: 0 = state of stage k's input (3 fields), 1 = viscous flux pairs (4 fields)
+int swdg_gpu_halo_pack(swdg_gpu* c, int what, int k, double* send_buf) {
+  return guarded(c, [&] {
+    if (k < 0 || k > 2 || what < 0 || what > 1) throw InputError{"halo_pack: bad stage/what"};
+    if (what == 1 && !c->fvu) throw InputError{"halo_pack: viscosity is off"};
+    double* const* in = stage_input(c, k);
+    const double* f[4] = {in[0], in[1], in[2], nullptr};
+    if (what == 1) {
+      f[0] = c->fvu;
+      f[1] = c->fvv;
+      f[2] = c->gvu;
+      f[3] = c->gvv;
+    }
+    c->launches += launch_halo_pack(c->send_idx, c->n_send, what ? 4 : 3, f, send_buf, c->stream);
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_halo_unpack(swdg_gpu* c, int what, int k, const double* recv_buf) {
+  return guarded(c, [&] {
+    if (k < 0 || k > 2 || what < 0 || what > 1) throw InputError{"halo_unpack: bad stage/what"};
+    if (what == 1 && !c->fvu) throw InputError{"halo_unpack: viscosity is off"};
+    double* const* in = stage_input(c, k);
+    double* f[4] = {in[0], in[1], in[2], nullptr};
+    if (what == 1) {
+      f[0] = c->fvu;
+      f[1] = c->fvv;
+      f[2] = c->gvu;
+      f[3] = c->gvv;
+    }
+    c->launches += launch_halo_unpack(c->recv_idx, c->n_recv, what ? 4 : 3, f, recv_buf,
+                                      c->stream);
+    return SWDG_OK;
+  });
+}
+
+// compute_dt's two reductions before the cross-rank min (timeloop.hpp:57-74):
+// min over owned nodes of the CFL candidates (inf if none) and of the lengths
+int swdg_gpu_dt_candidates(swdg_gpu* c, double* dt_min, double* min_len) {
+  return guarded(c, [&] {
+    reset_flags(c);
+    c->launches += launch_exact_dt(c->M, c->phys, cs(c->W), c->flags, c->stream);
+    read_flags(c);
+    *dt_min = key_value(c->flags_h[0].dt_key);
+    *min_len = key_value(c->flags_h[0].minlen_key);
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_step_begin(swdg_gpu* c) {
+  return guarded(c, [&] {
+    reset_flags(c);
+    c->split_max_eps = 0.0;
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_stage_visc(swdg_gpu* c, int k, double t, double dt) {
+  (void)t;
+  (void)dt;
+  return guarded(c, [&] {
+    if (k < 0 || k > 2) throw InputError{"stage_visc: bad stage"};
+    if (!c->params.visc_enabled) return SWDG_OK;
+    const double mx = stage_visc(c, cs(stage_input(c, k)), c->flags + k);
+    c->split_max_eps = std::max(c->split_max_eps, mx);
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_stage_run(swdg_gpu* c, int k, double t, double dt) {
+  return guarded(c, [&] {
+    if (k < 0 || k > 2) throw InputError{"stage_run: bad stage"};
+    stage_main(c, cs(stage_input(c, k)), stage_output(c, k), k, t, dt,
+               c->params.visc_enabled != 0, nullptr, c->flags + k);
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_step_flags(swdg_gpu* c, int32_t* reject, int32_t* abort) {
+  return guarded(c, [&] {
+    read_flags(c);
+    *reject = 0;
+    *abort = 0;
+    // stage order, stopping at the first signal: the reference never evaluates
+    // the stages after a reject (ssprk3_step timeloop.hpp:97-105)
+    for (int k = 0; k < 3; ++k) {
+      if (c->flags_h[k].abort) {
+        *abort = 1;
+        break;
+      }
+      if (c->flags_h[k].reject) {
+        *reject = 1;
+        break;
+      }
+    }
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_step_commit(swdg_gpu* c, int accept, swdg_step_info* info) {
+  return guarded(c, [&] {
+    swdg_step_info r{};
+    r.min_stage_h = std::numeric_limits<double>::infinity();
+    int code = SWDG_OK;
+    fold_flags(c, r, code);
+    if (!c->fast) r.max_eps = std::max(r.max_eps, c->split_max_eps);
+    r.accepted = accept ? 1 : 0;
+    if (accept)
+      for (int k = 0; k < 3; ++k) std::swap(c->W[k], c->A[k]);
+    c->last = r;
+    if (info) *info = r;
+    return SWDG_OK;
+  });
+}
 
 }  // extern "C"

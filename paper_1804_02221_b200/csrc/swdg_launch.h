@@ -41,6 +41,10 @@ int launch_fast_stage(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F
                       cudaStream_t st);
 
 // mode-independent (kernels_common.cu)
+int launch_halo_pack(const int* idx, long long n, int nf, const double* const* f, double* buf,
+                     cudaStream_t st);
+int launch_halo_unpack(const int* idx, long long n, int nf, double* const* f, const double* buf,
+                       cudaStream_t st);
 int launch_diagnostics(const Mesh& M, const Phys& P, CState S, double* partial, double* out2,
                        Flags* F, cudaStream_t st);
 

@@ -1,0 +1,246 @@
+"""Partitioned SSPRK3 stepping across ranks: one element partition per
+GPU, face-trace halos exchanged between stages, one flag reduction per step.
+
+    step_begin
+    for k in 0..2:
+        exchange stage-k input state at the halo face nodes      (3 doubles / node)
+        stage_visc k            (viscosity on: eps, BR1, flux pairs)
+        exchange the viscous flux pairs at the halo face nodes   (4 doubles / node)
+        stage_run k             (fused stage kernel, limiter, reject flags)
+    all-reduce (reject, abort) -> step_commit(accept)
+
+The stepping logic is backend-agnostic: `GpuPartition` drives the sm_100a kernels
+through the split-step C ABI; tests drive the same loop with the CPU oracle.  The
+exchanger is torch.distributed (NCCL between GPUs, gloo on CPU) or an in-process
+loopback for several partitions in one process.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+
+from . import swdg
+from .partition import LocalMesh
+
+
+class Backend:
+    """Interface of one rank's partition."""
+    visc: bool
+    plan = None  # HaloPlan
+
+    def step_begin(self): ...
+    def pack(self, what: int, k: int, buf): ...
+    def unpack(self, what: int, k: int, buf): ...
+    def stage_visc(self, k: int, t: float, dt: float): ...
+    def stage_run(self, k: int, t: float, dt: float): ...
+    def step_flags(self): ...
+    def step_commit(self, accept: bool): ...
+    def dt_candidates(self): ...
+
+
+def _offsets(plan, which):
+    off, out = 0, {}
+    for p in plan.peers:
+        n = len(getattr(plan, which)[p])
+        out[p] = (off, n)
+        off += n
+    return out, off
+
+
+class TorchExchanger:
+    """Halo exchange with torch.distributed point-to-point ops (NCCL or gloo)."""
+
+    def __init__(self, backend: Backend, device):
+        import torch
+        self.torch = torch
+        self.b = backend
+        plan = backend.plan
+        self.soff, ns = _offsets(plan, "send_idx")
+        self.roff, nr = _offsets(plan, "recv_idx")
+        self.send = torch.zeros(max(ns, 1) * 4, dtype=torch.float64, device=device)
+        self.recv = torch.zeros(max(nr, 1) * 4, dtype=torch.float64, device=device)
+
+    def exchange(self, what: int, k: int):
+        dist = self.torch.distributed
+        nf = 4 if what else 3
+        self.b.pack(what, k, self.send)
+        ops = []
+        for p in self.b.plan.peers:
+            o, n = self.soff[p]
+            if n:
+                ops.append(dist.P2POp(dist.isend, self.send[o * nf:(o + n) * nf], p))
+            o, n = self.roff[p]
+            if n:
+                ops.append(dist.P2POp(dist.irecv, self.recv[o * nf:(o + n) * nf], p))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        self.b.unpack(what, k, self.recv)
+
+    def all_max(self, vals):
+        t = self.torch.tensor(vals, dtype=self.torch.float64, device=self.send.device)
+        self.torch.distributed.all_reduce(t, op=self.torch.distributed.ReduceOp.MAX)
+        return t.tolist()
+
+    def all_min(self, vals):
+        return [-v for v in self.all_max([-v for v in vals])]
+
+
+class LoopbackExchanger:
+    """Several partitions in one process: halo buffers copied directly."""
+
+    def __init__(self, backends, make_buffer):
+        self.bs = backends
+        self.bufs = []
+        for b in backends:
+            soff, ns = _offsets(b.plan, "send_idx")
+            roff, nr = _offsets(b.plan, "recv_idx")
+            self.bufs.append((soff, roff, make_buffer(max(ns, 1) * 4), make_buffer(max(nr, 1) * 4)))
+
+    def exchange_all(self, what: int, k: int):
+        nf = 4 if what else 3
+        for b, (_, _, send, _) in zip(self.bs, self.bufs):
+            b.pack(what, k, send)
+        for r, (b, (_, roff, _, recv)) in enumerate(zip(self.bs, self.bufs)):
+            for p in b.plan.peers:
+                o, n = roff[p]
+                so, sn = self.bufs[p][0][r]
+                assert sn == n, "halo plans disagree between ranks"
+                recv[o * nf:(o + n) * nf] = self.bufs[p][2][so * nf:(so + n) * nf]
+        for b, (_, _, _, recv) in zip(self.bs, self.bufs):
+            b.unpack(what, k, recv)
+
+
+def try_step_distributed(b: Backend, ex, t: float, dt: float) -> bool:
+    """One SSPRK3 step of this rank's partition, in lock step with the other ranks."""
+    b.step_begin()
+    for k in range(3):
+        ex.exchange(0, k)
+        if b.visc:
+            b.stage_visc(k, t, dt)
+            ex.exchange(1, k)
+        b.stage_run(k, t, dt)
+    rej, ab = b.step_flags()
+    rej, ab = ex.all_max([float(rej), float(ab)])
+    if ab:
+        raise swdg.NumericalAbort("negative water height without limiter")
+    accept = not rej
+    b.step_commit(accept)
+    return accept
+
+
+def try_step_loopback(bs, ex: LoopbackExchanger, t: float, dt: float) -> bool:
+    """All partitions of one process, one SSPRK3 step (the same schedule)."""
+    for b in bs:
+        b.step_begin()
+    for k in range(3):
+        ex.exchange_all(0, k)
+        if bs[0].visc:
+            for b in bs:
+                b.stage_visc(k, t, dt)
+            ex.exchange_all(1, k)
+        for b in bs:
+            b.stage_run(k, t, dt)
+    flags = [b.step_flags() for b in bs]
+    if any(a for _, a in flags):
+        raise swdg.NumericalAbort("negative water height without limiter")
+    accept = not any(r for r, _ in flags)
+    for b in bs:
+        b.step_commit(accept)
+    return accept
+
+
+def compute_dt_distributed(b: Backend, ex, cfl: float, degree: int, phys) -> float:
+    """compute_dt (timeloop.hpp:53-75) over all ranks: min of both reductions, then
+    the all-dry fallback, exactly as on one device."""
+    if not (cfl > 0.0) or cfl > 1.0:
+        raise swdg.SwdgError("compute_dt: cfl must be in (0, 1]")
+    d, ml = b.dt_candidates()
+    d, ml = ex.all_min([d, ml])
+    if not math.isfinite(d):
+        order = 2.0 * degree + 1.0
+        d = ml / (order * math.sqrt(phys.g * max(phys.h_ref, 1e-12)))
+    return cfl * d
+
+
+class GpuPartition(Backend):
+    """One rank's partition on the GPU through the split-step C ABI."""
+
+    def __init__(self, lm: LocalMesh, cfg: swdg.RunConfig, device: int = 0):
+        self.lm = lm
+        self.plan = lm.halo
+        self.visc = bool(cfg.visc.enabled)
+        mesh = swdg.Mesh(lm.degree, lm.n_elem, lm.arrays, lm.faces, n_owned=lm.n_owned)
+        self.integ = swdg.TimeIntegrator(mesh, cfg, device=device)
+        L = swdg.lib()
+        vp, i32p = C.c_void_p, C.POINTER(C.c_int32)
+        for name, args in (("swdg_gpu_halo_setup", [vp, C.c_int64, i32p, C.c_int64, i32p]),
+                           ("swdg_gpu_halo_pack", [vp, C.c_int, C.c_int, C.c_void_p]),
+                           ("swdg_gpu_halo_unpack", [vp, C.c_int, C.c_int, C.c_void_p]),
+                           ("swdg_gpu_step_begin", [vp]),
+                           ("swdg_gpu_stage_visc", [vp, C.c_int, C.c_double, C.c_double]),
+                           ("swdg_gpu_stage_run", [vp, C.c_int, C.c_double, C.c_double]),
+                           ("swdg_gpu_step_flags", [vp, i32p, i32p]),
+                           ("swdg_gpu_step_commit", [vp, C.c_int, C.POINTER(swdg.StepInfoC)]),
+                           ("swdg_gpu_dt_candidates", [vp, C.POINTER(C.c_double),
+                                                       C.POINTER(C.c_double)])):
+            f = getattr(L, name)
+            f.restype = C.c_int
+            f.argtypes = args
+        self.L = L
+        send = np.concatenate([self.plan.send_idx[p] for p in self.plan.peers] or
+                              [np.zeros(0, np.int32)]).astype(np.int32)
+        recv = np.concatenate([self.plan.recv_idx[p] for p in self.plan.peers] or
+                              [np.zeros(0, np.int32)]).astype(np.int32)
+        self._keep = (send, recv)
+        self._chk(L.swdg_gpu_halo_setup(self.integ._h, len(send), send.ctypes.data_as(i32p),
+                                        len(recv), recv.ctypes.data_as(i32p)))
+        self.info = swdg.StepInfoC()
+        # halo buffers are torch tensors moved by torch (NCCL / copies): order the
+        # context's kernels on torch's current stream
+        import torch
+        self.integ.set_stream(torch.cuda.current_stream().cuda_stream)
+
+    def _chk(self, rc):
+        self.integ._check(rc)
+
+    def set_stream(self, handle):
+        self.integ.set_stream(handle)
+
+    def upload(self, state):
+        self.integ.upload(swdg.State(*state))
+
+    def download(self):
+        out = [np.empty(self.lm.n_nodes) for _ in range(3)]
+        self.integ.download(swdg.State(*out))
+        return out
+
+    def step_begin(self):
+        self._chk(self.L.swdg_gpu_step_begin(self.integ._h))
+
+    def pack(self, what, k, buf):
+        self._chk(self.L.swdg_gpu_halo_pack(self.integ._h, what, k, C.c_void_p(buf.data_ptr())))
+
+    def unpack(self, what, k, buf):
+        self._chk(self.L.swdg_gpu_halo_unpack(self.integ._h, what, k, C.c_void_p(buf.data_ptr())))
+
+    def stage_visc(self, k, t, dt):
+        self._chk(self.L.swdg_gpu_stage_visc(self.integ._h, k, t, dt))
+
+    def stage_run(self, k, t, dt):
+        self._chk(self.L.swdg_gpu_stage_run(self.integ._h, k, t, dt))
+
+    def step_flags(self):
+        r, a = C.c_int32(), C.c_int32()
+        self._chk(self.L.swdg_gpu_step_flags(self.integ._h, C.byref(r), C.byref(a)))
+        return r.value, a.value
+
+    def step_commit(self, accept):
+        self._chk(self.L.swdg_gpu_step_commit(self.integ._h, int(accept), C.byref(self.info)))
+
+    def dt_candidates(self):
+        d, m = C.c_double(), C.c_double()
+        self._chk(self.L.swdg_gpu_dt_candidates(self.integ._h, C.byref(d), C.byref(m)))
+        return d.value, m.value

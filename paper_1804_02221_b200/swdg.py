@@ -463,7 +463,8 @@ class TimeIntegrator:
         return dt.value
 
     def set_stream(self, stream_handle: int | None):
-        """Launch on an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)."""
+        """Launch on an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream;
+        0 is the legacy default stream)."""
         self._check(lib().swdg_gpu_set_stream(self._h, C.c_void_p(stream_handle or None)))
 
     def synchronize(self):

@@ -1,0 +1,88 @@
+"""Partitioned stepping on the GPU: several element partitions (ghost elements, halo
+pack/unpack kernels, split-step C ABI) in one process on cuda:0, exchanged through
+the loopback exchanger, reproduce the unpartitioned run — bitwise in exact mode
+(hence the reference) and bitwise against the single-partition fast run."""
+import numpy as np
+import pytest
+
+from oracle import ref
+from paper_1804_02221_b200 import partition as part
+from paper_1804_02221_b200 import swdg
+from paper_1804_02221_b200.distributed import (GpuPartition, LoopbackExchanger,
+                                               compute_dt_distributed, try_step_loopback)
+from tests.conftest import gpu_available
+from tests.helpers import beq, build, random_state, scenario_params
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device"),
+              pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")]
+
+
+def cfg_from(p, mode):
+    return swdg.RunConfig(
+        phys=swdg.PhysicsParams(p.g, p.h_tol, p.h_des, p.h_ref),
+        visc=swdg.ViscosityConfig(bool(p.visc_enabled), p.epsilon0, p.sigma_min, p.sigma_max),
+        limiter_enabled=bool(p.limiter_enabled), mode=mode)
+
+
+def run_parts(m, cfg, st, P, dt, steps):
+    import torch
+    lms = [part.local_mesh(m, P, r) for r in range(P)]
+    bs = [GpuPartition(lm, cfg) for lm in lms]
+    for lm, b in zip(lms, bs):
+        b.upload(part.scatter_state(st, lm))
+    ex = LoopbackExchanger(bs, lambda n: torch.zeros(n, dtype=torch.float64, device="cuda"))
+    acc = []
+    for k in range(steps):
+        acc.append(try_step_loopback(bs, ex, k * dt, dt))
+    np_ = m.n1 * m.n1
+    out = [np.zeros(m.n_nodes) for _ in range(3)]
+    for lm, b in zip(lms, bs):
+        w = b.download()
+        sel = (lm.global_ids[: lm.n_owned, None] * np_ + np.arange(np_)).ravel()
+        for o, a in zip(out, w):
+            o[sel] = a[: lm.n_owned * np_]
+    return out, acc
+
+
+@pytest.mark.parametrize("mode", [swdg.MODE_EXACT, swdg.MODE_FAST])
+@pytest.mark.parametrize("sid,kx,deg,P", [("wetdry_dambreak", 8, 3, 2),
+                                          ("parabolic_dam_dry", 8, 3, 3),
+                                          ("oscillating_lake", 10, 4, 4)])
+def test_partitioned_equals_single(mode, sid, kx, deg, P):
+    m, st = ref.scenario_mesh(sid, kx, kx, deg)
+    p, cfg = scenario_params(sid, deg)
+    dt = ref.compute_dt(m, p, st, cfg["cfl"])
+    single = swdg.TimeIntegrator(m, cfg_from(p, mode))
+    want = swdg.State(*[a.copy() for a in st])
+    acc_ref = [single.try_step(want, k * dt, dt) for k in range(4)]
+    got, acc = run_parts(m, cfg_from(p, mode), st, P, dt, 4)
+    assert acc == acc_ref
+    assert beq(got, want.arrays())
+    if mode == swdg.MODE_EXACT:  # and therefore the reference itself
+        ri = ref.Integrator(m, p)
+        s = [a.copy() for a in st]
+        for k in range(4):
+            ri.try_step(s, k * dt, dt)
+        assert beq(got, s)
+
+
+def test_distributed_dt_matches():
+    m = build("wavy_N4")
+    p = ref.params(g=9.81)
+    st = random_state(m.n_nodes, np.random.default_rng(4), h=(0.5, 1.5))
+    cfg = cfg_from(p, swdg.MODE_EXACT)
+    lms = [part.local_mesh(m, 3, r) for r in range(3)]
+    bs = [GpuPartition(lm, cfg) for lm in lms]
+    for lm, b in zip(lms, bs):
+        b.upload(part.scatter_state(st, lm))
+
+    class MinEx:  # all-min over the in-process partitions
+        def __init__(self, bs):
+            self.vals = [b.dt_candidates() for b in bs]
+
+        def all_min(self, v):
+            return [min(x[0] for x in self.vals), min(x[1] for x in self.vals)]
+
+    dt = compute_dt_distributed(bs[0], MinEx(bs), 0.5, m.degree, cfg.phys)
+    assert dt == ref.compute_dt(m, p, st, 0.5)
