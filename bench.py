@@ -183,6 +183,68 @@ def measure_gpu(N: int, steps: int, warmup: int, viscous: bool, rank: int, world
     return res
 
 
+def measure_gpu_distributed(N: int, steps: int, warmup: int, viscous: bool, rank: int,
+                            world: int, e2e_steps: int = 2):
+    """Strong scaling over `world` ranks (one GPU each) of the same 1M-element mesh:
+    rank r owns a band of element rows, generates its owned + ghost geometry on its
+    device, and exchanges face-trace halos with NCCL between stages."""
+    import numpy as np
+    import torch
+    from paper_1804_02221_b200 import swdg
+    from paper_1804_02221_b200.distributed import (GpuPartition, TorchExchanger,
+                                                   compute_dt_distributed, try_step_distributed)
+
+    spec = spec_for(N)
+    cfg = run_config(N, viscous)
+    dev = torch.cuda.current_device()
+    b = GpuPartition.structured(spec, cfg, world, rank, dev)
+    integ = b.integ
+    stream = torch.cuda.current_stream()
+    nn_local = integ.mesh.n_nodes
+    x, y = integ.geometry("x"), integ.geometry("y")
+    host = [torch.empty(nn_local, dtype=torch.float64).pin_memory() for _ in range(3)]
+    for hbuf, val in zip(host, smooth_state(x, y)):
+        hbuf.numpy()[:] = val
+    st = swdg.State(*(hb.numpy() for hb in host))
+    integ.upload(st)
+    ex = TorchExchanger(b, "cuda")
+    dt = 0.1 * compute_dt_distributed(b, ex, 0.5, N, cfg.phys)
+    for s in range(warmup):
+        try_step_distributed(b, ex, s * dt, dt)
+    torch.distributed.barrier()
+    torch.cuda.synchronize()
+    l0 = integ.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ok = True
+    with ClockSampler(dev) as clk:
+        ev0.record(stream)
+        for s in range(steps):
+            ok &= try_step_distributed(b, ex, (warmup + s) * dt, dt)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if not ok:
+        raise RuntimeError("a step was rejected during the timed run (invalid measurement)")
+    launches = integ.launch_count() - l0
+    t = torch.tensor([ev0.elapsed_time(ev1)], device="cuda", dtype=torch.float64)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t.item())
+    # e2e: every rank uploads its partition from pinned host memory, steps, downloads
+    torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for s in range(e2e_steps):
+        integ.upload(st)
+        try_step_distributed(b, ex, s * dt, dt)
+        integ.download(st)
+    torch.cuda.synchronize()
+    e2e = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    torch.distributed.all_reduce(e2e, op=torch.distributed.ReduceOp.MAX)
+    np1 = (N + 1) ** 2
+    return dict(ms=ms, dofs=3 * spec.kx * spec.ky * np1, nn=b.lm.n_owned * np1,
+                launches=launches, clocks=clk.summary(), e2e_s=float(e2e.item()) / e2e_steps,
+                h2d=3 * nn_local * 8, d2h=3 * nn_local * 8, halo_peers=len(b.plan.peers))
+
+
 def cpu_reference(N: int, viscous: bool, budget_s: float = 15.0, kx: int = 64, steps=None):
     """The reference's own try_step (oracle/_ref, single-threaded like the reference) on
     a bounded sample of the C5 workload: the same mesh family, state and params on a
@@ -231,7 +293,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--degree", type=int, default=7)
     ap.add_argument("--viscous", action="store_true")
-    ap.add_argument("--sweep", action="store_true", help="also time N=1..7")
+    ap.add_argument("--sweep", action="store_true", help="also time N=1..15 (single GPU)")
+    ap.add_argument("--distributed", action="store_true",
+                    help="use the partitioned (NCCL halo) path even on one GPU")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -266,12 +330,22 @@ def main():
         return
 
     import torch
-    if world > 1:
-        torch.distributed.init_process_group("nccl")
+    distributed = world > 1 or args.distributed
+    if distributed:
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
-    r = measure_gpu(N, args.steps, args.warmup, args.viscous, rank, world)
+        if not torch.distributed.is_initialized():
+            if "MASTER_ADDR" not in os.environ:  # single-process check of the path
+                os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29531", RANK="0",
+                                  WORLD_SIZE="1")
+            torch.distributed.init_process_group("nccl")
+        r = measure_gpu_distributed(N, args.steps, args.warmup, args.viscous, rank, world)
+        config.update(parallelism=f"element partition over {world} GPU(s), NCCL halos",
+                      scaling="strong: the same 1M-element mesh for every N")
+    else:
+        r = measure_gpu(N, args.steps, args.warmup, args.viscous, rank, world)
     stage_s = r["ms"] * 1e-3 / (3 * args.steps)
-    value = world * r["dofs"] / stage_s
+    # value: DOF-updates of the whole job per second
+    value = (r["dofs"] if distributed else world * r["dofs"]) / stage_s
     bytes_node, flops_node = frozen_counts(N, args.viscous)
     pk = peaks()
     achieved_gbs = bytes_node * r["nn"] / stage_s / 1e9
@@ -283,7 +357,8 @@ def main():
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": r["ms"] / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if distributed else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
         "config": config,
         "roofline": {
             "bound": bound,
@@ -301,10 +376,14 @@ def main():
         },
         "clocks": r["clocks"],
         "gpu_launches": r["launches"],
-        "e2e": {"value": world * 3 * r["dofs"] / r["e2e_s"], "unit": UNIT,
+        "e2e": {"value": (1 if distributed else world) * 3 * r["dofs"] / r["e2e_s"], "unit": UNIT,
                 "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"],
-                "path": "TimeIntegrator.try_step via swdg_gpu_upload/try_step/download (pinned)"},
+                "path": ("per rank: swdg_gpu_upload_state + split-step C ABI with NCCL halos + "
+                         "download (pinned)") if distributed else
+                        "TimeIntegrator.try_step via swdg_gpu_upload/try_step/download (pinned)"},
     }
+    if distributed:
+        out["halo_peers_rank0"] = r.get("halo_peers")
     if rank == 0:
         cb = cpu_reference(N, args.viscous, budget_s=args.cpu_budget)
         out["cpu_baseline"] = {
@@ -312,17 +391,20 @@ def main():
             "sample": f"oracle/_ref TimeIntegrator::try_step, {cb['kx']}x{cb['kx']} patch of the "
                       f"same mesh family, {cb['steps']} steps in {cb['seconds']:.1f} s, "
                       f"{cpu_model()}"}
-        if args.sweep:
+        if args.sweep and not distributed:
             sweep = {}
-            for n in range(1, 8):
+            for n in range(1, 16):
                 if n == N:
-                    sweep[n] = value / world
+                    sweep[n] = value
                     continue
-                rr = measure_gpu(n, max(5, args.steps // 2), 3, args.viscous, rank, 1, e2e_steps=0)
-                sweep[n] = rr["dofs"] / (rr["ms"] * 1e-3 / (3 * max(5, args.steps // 2)))
+                if args.viscous and n < 2:
+                    continue
+                ks = max(3, args.steps // 4)
+                rr = measure_gpu(n, ks, 3, args.viscous, rank, 1, e2e_steps=0)
+                sweep[n] = rr["dofs"] / (rr["ms"] * 1e-3 / (3 * ks))
             out["sweep_dof_per_s_by_degree"] = sweep
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if distributed:
         torch.distributed.destroy_process_group()
 
 

@@ -217,6 +217,15 @@ typedef struct swdg_structured_spec {
 int swdg_gpu_create_structured(const swdg_structured_spec* spec, const swdg_params* params,
                                int device, swdg_gpu** out);
 
+/* One partition of a structured mesh generated on the device: local element i
+ * is global element local_to_global[i]; [0, n_owned) are owned, the rest are
+ * halo (ghost) copies; local_faces is the partition's face list in local ids
+ * (paper_1804_02221_b200/partition.py build_plan). */
+int swdg_gpu_create_structured_part(const swdg_structured_spec* spec, const swdg_params* params,
+                                    int device, int32_t n_local, int32_t n_owned,
+                                    const int32_t* local_to_global, int32_t n_faces,
+                                    const swdg_face* local_faces, swdg_gpu** out);
+
 /* Copy a device geometry array ("y_eta", "jac", "b", "face_nx", "x", ...) to host. */
 int swdg_gpu_download_geometry(swdg_gpu* ctx, const char* name, double* out);
 

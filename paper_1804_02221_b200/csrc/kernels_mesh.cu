@@ -69,7 +69,8 @@ __global__ void k_coords(MeshSpecDev s, const double* nodes, int n1, long long n
   if (n >= nn) return;
   const int np = n1 * n1;
   const int e = (int)(n / np), loc = (int)(n % np), i = loc / n1, j = loc % n1;
-  const int ex = e % s.kx, ey = e / s.kx;
+  const int eg = s.gid ? s.gid[e] : e;
+  const int ex = eg % s.kx, ey = eg / s.kx;
   const double u0 = (double)ex / s.kx, u1 = (double)(ex + 1) / s.kx;
   const double v0 = (double)ey / s.ky, v1 = (double)(ey + 1) / s.ky;
   const double xi = nodes[i], eta = nodes[j];
@@ -143,8 +144,8 @@ __global__ void k_faces(int n1, long long nfn, MeshOut o) {
 
 int launch_structured_mesh(const MeshSpecDev& s, const double* nodes, const double* D, int n1,
                            const MeshOut& o, cudaStream_t st) {
-  const long long nn = (long long)s.kx * s.ky * n1 * n1;
-  const long long nfn = (long long)s.kx * s.ky * 4 * n1;
+  const long long nn = s.n_elem * n1 * n1;
+  const long long nfn = s.n_elem * 4 * n1;
   k_coords<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(s, nodes, n1, nn, o.x, o.y);
   k_metrics<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(s, D, n1, nn, o.x, o.y, o);
   k_faces<<<(unsigned)((nfn + 255) / 256), 256, 0, st>>>(n1, nfn, o);

@@ -480,6 +480,13 @@ int swdg_gpu_create(const swdg_mesh_view* mv, const swdg_params* p, int device,
 
 int swdg_gpu_create_structured(const swdg_structured_spec* s, const swdg_params* p, int device,
                                swdg_gpu** out) {
+  return swdg_gpu_create_structured_part(s, p, device, 0, 0, nullptr, 0, nullptr, out);
+}
+
+int swdg_gpu_create_structured_part(const swdg_structured_spec* s, const swdg_params* p,
+                                    int device, int32_t n_local, int32_t n_owned,
+                                    const int32_t* local_to_global, int32_t n_faces,
+                                    const swdg_face* local_faces, swdg_gpu** out) {
   *out = nullptr;
   g_create_error.clear();
   if (!s || !p) {
@@ -492,23 +499,39 @@ int swdg_gpu_create_structured(const swdg_structured_spec* s, const swdg_params*
     validate_params(p, N);
     if (s->kx < 1 || s->ky < 1) throw InputError{"mesh: element counts must be >= 1"};
     if (s->kind < 0 || s->kind > 2) throw InputError{"unknown mesh kind"};
-    const long long Kl = (long long)s->kx * s->ky;
+    const long long Kg = (long long)s->kx * s->ky;
+    const bool part = local_to_global != nullptr;
+    const long long Kl = part ? n_local : Kg;
     if (Kl * np > (1ll << 31) - 1) throw InputError{"mesh too large for int32 node indices"};
     const int K = (int)Kl;
-    const std::vector<swdg_face> faces =
-        swdg_host::structured_faces(s->kx, s->ky, s->periodic_x != 0, s->periodic_y != 0);
+    std::vector<swdg_face> faces;
+    if (part) {
+      if (n_owned < 1 || n_owned > n_local) throw InputError{"partition: bad n_owned"};
+      for (int i = 0; i < n_local; ++i)
+        if (local_to_global[i] < 0 || local_to_global[i] >= Kg)
+          throw InputError{"partition: global id out of range"};
+      faces.assign(local_faces, local_faces + n_faces);
+    } else {
+      faces = swdg_host::structured_faces(s->kx, s->ky, s->periodic_x != 0, s->periodic_y != 0);
+    }
     const std::vector<int4> ef = connectivity(K, faces.data(), (int)faces.size());
     std::vector<double> nodes(n1), w(n1), D(np), Dt(np), Dh(np), V(np), Vi(np);
     swdg_operators(N, nodes.data(), w.data(), D.data(), Dt.data(), Dh.data(), V.data(), Vi.data());
-    allocate(c, K, K, N, ef, w.data(), D.data(), Dt.data(), Dh.data(), Vi.data());
+    allocate(c, K, part ? n_owned : K, N, ef, w.data(), D.data(), Dt.data(), Dh.data(),
+             Vi.data());
     const long long nn = c->nn;
     c->xy = c->dalloc<double>(2 * nn);
     double* dnodes = c->dalloc<double>(n1);
     ck(cudaMemcpy(dnodes, nodes.data(), n1 * sizeof(double), cudaMemcpyHostToDevice), "nodes");
     int* bad = c->dalloc<int>(1);
     ck(cudaMemset(bad, 0, sizeof(int)), "memset");
+    int* gid = nullptr;
+    if (part) {
+      gid = c->dalloc<int>(n_local);
+      ck(cudaMemcpy(gid, local_to_global, n_local * sizeof(int), cudaMemcpyHostToDevice), "gid");
+    }
     MeshSpecDev sd{s->kind, s->kx, s->ky, s->bathy_kind, s->x0, s->x1, s->y0, s->y1, s->extra,
-                   {s->bathy[0], s->bathy[1], s->bathy[2], s->bathy[3]}};
+                   {s->bathy[0], s->bathy[1], s->bathy[2], s->bathy[3]}, gid, Kl};
     const Mesh& M = c->M;
     auto wr = [](const double* p) { return const_cast<double*>(p); };
     MeshOut o{c->xy, c->xy + nn, wr(M.xx), wr(M.xe), wr(M.yx), wr(M.ye), wr(M.jac), wr(M.b),

@@ -9,6 +9,8 @@ struct MeshSpecDev {
   int kind, kx, ky, bathy_kind;
   double x0, x1, y0, y1, extra;
   double bathy[4];
+  const int* gid;  // local -> global element id (partitions), nullptr = identity
+  long long n_elem;  // elements generated
 };
 
 struct MeshOut {

@@ -168,12 +168,14 @@ def compute_dt_distributed(b: Backend, ex, cfl: float, degree: int, phys) -> flo
 class GpuPartition(Backend):
     """One rank's partition on the GPU through the split-step C ABI."""
 
-    def __init__(self, lm: LocalMesh, cfg: swdg.RunConfig, device: int = 0):
+    def __init__(self, lm: LocalMesh, cfg: swdg.RunConfig, device: int = 0, integ=None):
         self.lm = lm
         self.plan = lm.halo
         self.visc = bool(cfg.visc.enabled)
-        mesh = swdg.Mesh(lm.degree, lm.n_elem, lm.arrays, lm.faces, n_owned=lm.n_owned)
-        self.integ = swdg.TimeIntegrator(mesh, cfg, device=device)
+        if integ is None:
+            mesh = swdg.Mesh(lm.degree, lm.n_elem, lm.arrays, lm.faces, n_owned=lm.n_owned)
+            integ = swdg.TimeIntegrator(mesh, cfg, device=device)
+        self.integ = integ
         L = swdg.lib()
         vp, i32p = C.c_void_p, C.POINTER(C.c_int32)
         for name, args in (("swdg_gpu_halo_setup", [vp, C.c_int64, i32p, C.c_int64, i32p]),
@@ -202,6 +204,19 @@ class GpuPartition(Backend):
         # context's kernels on torch's current stream
         import torch
         self.integ.set_stream(torch.cuda.current_stream().cuda_stream)
+
+    @classmethod
+    def structured(cls, spec, cfg: swdg.RunConfig, P: int, rank: int, device: int = 0):
+        """Rank `rank` of P of a device-generated structured mesh: the host builds only
+        the face list and the partition plan; geometry is generated on the device for
+        the owned and ghost elements."""
+        from .partition import build_plan
+        K = spec.kx * spec.ky
+        faces = swdg.structured_faces(spec.kx, spec.ky, spec.periodic_x, spec.periodic_y)
+        gids, n_owned, lf, ords, plan = build_plan(faces, K, spec.degree, P, rank)
+        lm = LocalMesh(spec.degree, len(gids), n_owned, gids, lf, ords, {}, plan)
+        integ = swdg.TimeIntegrator.structured_part(spec, cfg, gids, n_owned, lf, device)
+        return cls(lm, cfg, device, integ=integ)
 
     def _chk(self, rc):
         self.integ._check(rc)

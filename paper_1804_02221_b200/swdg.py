@@ -361,6 +361,29 @@ class TimeIntegrator:
         integ.mesh.owner = integ
         return integ
 
+    @classmethod
+    def structured_part(cls, spec: StructuredSpecC, cfg: RunConfig, global_ids, n_owned: int,
+                        local_faces, device: int = 0):
+        """One partition of a device-generated structured mesh (owned + ghost elements)."""
+        L = lib()
+        f = L.swdg_gpu_create_structured_part
+        f.restype = C.c_int
+        f.argtypes = [C.POINTER(StructuredSpecC), C.POINTER(ParamsC), C.c_int, C.c_int32,
+                      C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(C.c_void_p)]
+        gids = np.ascontiguousarray(global_ids, np.int32)
+        faces = np.ascontiguousarray(local_faces, np.int32).reshape(-1, 6)
+        p = cfg.c_params()
+        h = C.c_void_p()
+        rc = f(C.byref(spec), C.byref(p), device, len(gids), n_owned, gids.ctypes.data,
+               len(faces), faces.ctypes.data, C.byref(h))
+        if rc != SWDG_OK:
+            _raise(rc, L.swdg_gpu_create_error().decode())
+        m = _DeviceMesh(spec.degree, len(gids))
+        m.n_owned = n_owned
+        integ = cls(m, cfg, device, _handle=h)
+        m.owner = integ
+        return integ
+
     def geometry(self, name: str) -> np.ndarray:
         """Device geometry array (nodal or face layout) copied to host."""
         n = self.mesh.n_nodes
