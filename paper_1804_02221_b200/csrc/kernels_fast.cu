@@ -1296,6 +1296,210 @@ static void launch_visc_pre_n(const Mesh& M, const Phys& P, CState S, double* ep
   k_visc_pre<N1><<<grid, PL::THREADS, PL::bytes, st>>>(M, P, S, eps, fvu, fvv, gvu, gvv, F);
 }
 
+// ===========================================================================
+// Element-per-thread kernel for the smallest degrees (N+1 <= 3, inviscid).  An
+// element is (N+1)^2 <= 9 nodes: one thread loads all of it (vectorised,
+// coalesced across the warp), its neighbours' face traces (L2 hits) and does the
+// whole stage in registers — volume pairs, source, the 4(N+1) interface
+// fluxes, -1/J, SSPRK3 update, element mean, limiter — with no shared memory
+// and no barriers.  At these degrees the stage is a stream (HBM bound); what
+// matters is many independent loads in flight, which this gives at full
+// occupancy.
+template <int N1, bool FORCE>
+__global__ void __launch_bounds__(128) k_stage_elem(Mesh M, Phys Ph, StageArgs A, Flags* F) {
+  using O = Ops<N1>;
+  constexpr int NP = N1 * N1;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = e < M.n_owned;
+  const long long base = (long long)(active ? e : 0) * NP;
+  const double g = Ph.g, h_des = Ph.h_des, inv2g = 1.0 / (2.0 * g), iw0 = 1.0 / M.w0;
+  double h[NP], hu[NP], hv[NP], u[NP], v[NP], ye[NP], xe[NP], yx[NP], xx[NP];
+  double r0[NP], r1[NP], r2[NP];
+#pragma unroll
+  for (int q = 0; q < NP; ++q) {
+    h[q] = A.in.h[base + q];
+    hu[q] = A.in.hu[base + q];
+    hv[q] = A.in.hv[base + q];
+    ye[q] = M.ye[base + q];
+    xe[q] = M.xe[base + q];
+    yx[q] = M.yx[base + q];
+    xx[q] = M.xx[base + q];
+    r0[q] = r1[q] = r2[q] = 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < NP; ++q) vel(h[q], hu[q], hv[q], h_des, u[q], v[q]);
+  const double g2 = 2.0 * g;
+  // volume: xi-lines (j fixed, metrics (y_eta, x_eta)) and eta-lines (i fixed, -(y_xi, x_xi))
+#pragma unroll
+  for (int dir = 0; dir < 2; ++dir)
+#pragma unroll
+    for (int l = 0; l < N1; ++l)
+#pragma unroll
+      for (int a = 0; a < N1; ++a)
+#pragma unroll
+        for (int b = a; b < N1; ++b) {
+          if (a == b && a != 0 && a != N1 - 1) continue;
+          const int qa = dir == 0 ? a * N1 + l : l * N1 + a;
+          const int qb = dir == 0 ? b * N1 + l : l * N1 + b;
+          const double Aa = dir == 0 ? ye[qa] : -yx[qa], Ba = dir == 0 ? xe[qa] : -xx[qa];
+          const double Ab = dir == 0 ? ye[qb] : -yx[qb], Bb = dir == 0 ? xe[qb] : -xx[qb];
+          double F0, T1, T2;
+          pair_flux(h[qa], u[qa], v[qa], hu[qa], hv[qa], Aa, Ba, h[qb], u[qb], v[qb], hu[qb],
+                    hv[qb], Ab, Bb, g2, F0, T1, T2);
+          r0[qa] += O::D4(a, b) * F0;
+          r1[qa] += O::D8(a, b) * T1;
+          r2[qa] += O::D8(a, b) * T2;
+          if (a != b) {
+            r0[qb] += O::D4(b, a) * F0;
+            r1[qb] += O::D8(b, a) * T1;
+            r2[qb] += O::D8(b, a) * T2;
+          }
+        }
+  // interface fluxes at the 4 (N+1) face nodes
+#pragma unroll
+  for (int face = 0; face < 4; ++face) {
+    const int4 ef = M.ef[(active ? e : 0) * 4 + face];
+    if (!active || !(ef.y & EF_PRESENT)) continue;
+    const int nf = ef.y & EF_NBR_FACE_MASK;
+#pragma unroll
+    for (int t = 0; t < N1; ++t) {
+      const int q = face == 0 ? t * N1 : face == 1 ? (N1 - 1) * N1 + t
+                  : face == 2 ? t * N1 + (N1 - 1) : t;
+      const bool ew = face == 1 || face == 3;
+      const double bo = M.b[base + q];
+      double wm0, wm1, wm2, wp0, wp1, wp2, bm, bp, nx, ny, js, sgn = 1.0;
+      if (ef.y & EF_MINUS) {
+        face_normal(face, ew ? ye[q] : yx[q], ew ? xe[q] : xx[q], nx, ny, js);
+        wm0 = h[q];
+        wm1 = hu[q];
+        wm2 = hv[q];
+        bm = bo;
+        if (ef.y & EF_WALL) {
+          const double mn = wm1 * nx + wm2 * ny;
+          wp0 = wm0;
+          wp1 = wm1 - 2.0 * mn * nx;
+          wp2 = wm2 - 2.0 * mn * ny;
+          bp = bm;
+        } else {
+          const int tp = (ef.y & EF_REVERSED) ? N1 - 1 - t : t;
+          const long long nb = (long long)ef.x * NP + face_node(N1, nf, tp);
+          wp0 = A.in.h[nb];
+          wp1 = A.in.hu[nb];
+          wp2 = A.in.hv[nb];
+          bp = M.b[nb];
+        }
+      } else {
+        const int tp = (ef.y & EF_REVERSED) ? N1 - 1 - t : t;
+        const long long nb = (long long)ef.x * NP + face_node(N1, nf, tp);
+        const bool new_ = nf == 1 || nf == 3;
+        face_normal(nf, new_ ? M.ye[nb] : M.yx[nb], new_ ? M.xe[nb] : M.xx[nb], nx, ny, js);
+        wm0 = A.in.h[nb];
+        wm1 = A.in.hu[nb];
+        wm2 = A.in.hv[nb];
+        bm = M.b[nb];
+        wp0 = h[q];
+        wp1 = hu[q];
+        wp2 = hv[q];
+        bp = bo;
+        sgn = -1.0;
+      }
+      double f0, f1, f2;
+      es_flux_fast(wm0, wm1, wm2, wp0, wp1, wp2, bm, bp, nx, ny, g, inv2g, h_des, f0, f1, f2);
+      const double c = sgn * js * iw0;
+      r0[q] += c * f0;
+      r1[q] += c * f1;
+      r2[q] += c * f2;
+    }
+  }
+  // node phase + element mean (no early returns: warp-collective reductions follow)
+  double area = 1.0, a0 = 0.0, a1 = 0.0, a2 = 0.0, mmin = 1.0e300;
+  if (active) {
+    area = 0.0;
+#pragma unroll
+  for (int q = 0; q < NP; ++q) {
+    const long long n = base + q;
+    const double jac = M.jac[n], ij = -1.0 / jac, hg2 = 0.5 * g * h[q];
+    double rh = r0[q] * ij;
+    double rhu = (r1[q] + hg2 * M.sx[n]) * ij;
+    double rhv = (r2[q] + hg2 * M.sy[n]) * ij;
+    if (FORCE) {
+      rh += A.fh[n];
+      rhu += A.fhu[n];
+      rhv += A.fhv[n];
+    }
+    if (A.rhs.h) {
+      A.rhs.h[n] = rh;
+      A.rhs.hu[n] = rhu;
+      A.rhs.hv[n] = rhv;
+    }
+    double sh = h[q] + A.dt * rh, shu = hu[q] + A.dt * rhu, shv = hv[q] + A.dt * rhv;
+    if (A.stage > 0 && A.update) {
+      sh = A.ca * A.wn.h[n] + A.cb * sh;
+      shu = A.ca * A.wn.hu[n] + A.cb * shu;
+      shv = A.ca * A.wn.hv[n] + A.cb * shv;
+    }
+    h[q] = sh;
+    hu[q] = shu;
+    hv[q] = shv;
+    const double wq = O::w(q / N1) * O::w(q % N1) * jac;
+    area += wq;
+    a0 += wq * sh;
+    a1 += wq * shu;
+    a2 += wq * shv;
+    mmin = smin(mmin, sh);
+  }
+  }
+  bool lim = active && A.update;
+  const double inv = 1.0 / area;
+  const double avg0 = inv * a0, avg1 = inv * a1, avg2 = inv * a2;
+  if (lim && avg0 < 0.0) {
+    atomicExch(&F->reject, 1);
+    if (!Ph.limiter) atomicExch(&F->abort, 1);
+    lim = false;
+  }
+  double theta = 1.0;
+  if (lim && Ph.limiter && mmin < 0.0) {
+    const double denom = avg0 - mmin;
+    theta = denom < 1e-14 ? 1.0 : smin(1.0, avg0 / denom);
+  }
+  if (lim && !Ph.limiter && mmin < 0.0) atomicExch(&F->abort, 1);
+  unsigned long long key = ~0ull;
+  if (lim) {
+    double mine = 1.0e300;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      double sh = h[q], shu = hu[q], shv = hv[q];
+      if (theta < 1.0) {
+        sh = smax(theta * (sh - avg0) + avg0, 0.0);
+        shu = theta * (shu - avg1) + avg1;
+        shv = theta * (shv - avg2) + avg2;
+      }
+      if (Ph.limiter && sh < Ph.h_tol) {
+        shu = 0.0;
+        shv = 0.0;
+      }
+      A.out.h[base + q] = sh;
+      A.out.hu[base + q] = shu;
+      A.out.hv[base + q] = shv;
+      mine = smin(mine, sh);
+    }
+    key = order_key(mine);
+  }
+  // one atomic per warp for the limited count and the min height
+  const unsigned limited = __ballot_sync(0xffffffffu, lim && theta < 1.0);
+  key = warp_min_key(key);
+  if ((threadIdx.x & 31) == 0) {
+    if (limited) atomicAdd(&F->n_limited, __popc(limited));
+    atomicMin(&F->min_h_key, key);
+  }
+}
+
+template <int N1, bool FORCE>
+static void launch_elem(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
+                        cudaStream_t st) {
+  k_stage_elem<N1, FORCE><<<(M.n_owned + 127) / 128, 128, 0, st>>>(M, P, A, F);
+}
+
 // geometry-only split-source coefficients (dg_rhs.hpp:159-176), one thread per node
 __global__ void k_source_geometry(Mesh M, double* sx, double* sy) {
   const long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -1393,8 +1597,8 @@ static void launch_half(const Mesh& M, const Phys& P, const StageArgs& A, Flags*
 static int variant_override() {
   static int v = -1;
   if (v < 0) {
-    const char* s = getenv("SWDG_FAST_VARIANT");  // "full" / "half" (experiments)
-    v = !s ? 0 : (s[0] == 'f' ? 1 : (s[0] == 'h' ? 2 : 0));
+    const char* s = getenv("SWDG_FAST_VARIANT");  // "elem" / "full" / "half" (experiments)
+    v = !s ? 0 : (s[0] == 'f' ? 1 : (s[0] == 'h' ? 2 : (s[0] == 'e' ? 3 : 0)));
   }
   return v;
 }
@@ -1409,22 +1613,31 @@ static void launch_n(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
       return;
     }
   }
+  // inviscid kernel choice: element-per-thread (N+1 <= 3), full-line (N+1 = 4),
+  // half-line (N+1 >= 5); SWDG_FAST_VARIANT=elem/full/half overrides where the
+  // variant exists for this degree
+  // measured on B200 (1M elements): full-line wins where the half split is
+  // unbalanced (odd N+1: 5, 7), half-line at even N+1 >= 6
+  int v = N1 <= 3 ? 3 : ((N1 == 4 || N1 == 5 || N1 == 7) ? 1 : 2);
   const int ov = variant_override();
-  bool half = N1 >= 5;
-  if constexpr (N1 <= 8) {
-    if (ov == 1) half = false;
+  if (ov == 3 && N1 <= 3) v = 3;
+  if (ov == 1 && N1 <= 8) v = 1;
+  if (ov == 2 && N1 >= 3) v = 2;
+  if constexpr (N1 <= 3) {
+    if (v == 3) {
+      if (A.fh) launch_elem<N1, true>(M, P, A, F, st);
+      else launch_elem<N1, false>(M, P, A, F, st);
+      return;
+    }
   }
-  if constexpr (N1 >= 5) {
-    if (ov == 2) half = true;
-  }
   if constexpr (N1 <= 8) {
-    if (!half) {
+    if (v == 1) {
       if (A.fh) launch_full<N1, true>(M, P, A, F, st);
       else launch_full<N1, false>(M, P, A, F, st);
       return;
     }
   }
-  if constexpr (N1 >= 5) {
+  if constexpr (N1 >= 3) {
     if (A.fh) launch_half<N1, true, false>(M, P, A, F, st);
     else launch_half<N1, false, false>(M, P, A, F, st);
   }

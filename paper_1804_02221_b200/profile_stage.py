@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--viscous", action="store_true")
     ap.add_argument("--exact", action="store_true")
+    ap.add_argument("--time", type=int, default=0, help="time this many extra steps")
     a = ap.parse_args()
     N = a.degree
     visc = swdg.ViscosityConfig(False)
@@ -37,7 +38,17 @@ def main():
     dt = 0.1 * integ.compute_dt_device(0.5)
     integ.run_steps(a.steps, 0.0, dt)
     integ.synchronize()
-    print("ok", integ.last_info().accepted, integ.launch_count())
+    if a.time:
+        import time
+        reps = a.time
+        t0 = time.perf_counter()
+        integ.run_steps(reps, 0.0, dt)  # ends with a flag read (host sync)
+        el = time.perf_counter() - t0
+        dofs = 3 * integ.mesh.n_nodes
+        print(f"N={N} kx={a.kx} visc={a.viscous} stage_ms={el / reps / 3 * 1e3:.3f} "
+              f"dof_per_s={dofs * reps * 3 / el:.4e} accepted={integ.last_info().accepted}")
+    else:
+        print("ok", integ.last_info().accepted, integ.launch_count())
 
 
 if __name__ == "__main__":
