@@ -28,6 +28,9 @@ SOURCES = {
     "kernels_exact.cu": ["--fmad=false"],
     "kernels_common.cu": [],
     "kernels_fast.cu": [],
+    "kernels_pl_a.cu": [],
+    "kernels_pl_b.cu": [],
+    "kernels_pl_c.cu": [],
     "kernels_mesh.cu": [],
     "host_mesh.cpp": [],
 }
@@ -47,8 +50,9 @@ def _stale(target, deps):
 
 
 def build(verbose: bool = False, force: bool = False, ptxas_v: bool = False) -> str:
+    from concurrent.futures import ThreadPoolExecutor
     os.makedirs(OBJ_DIR, exist_ok=True)
-    objs = []
+    objs, cmds = [], []
     hdrs = _headers()
     for src, extra in SOURCES.items():
         path = os.path.join(CSRC, src)
@@ -60,9 +64,15 @@ def build(verbose: bool = False, force: bool = False, ptxas_v: bool = False) -> 
             cmd = [NVCC, *ARCH, *COMMON, *extra, "-c", path, "-o", obj]
             if ptxas_v:
                 cmd.insert(1, "-Xptxas=-v")
-            if verbose:
-                print(" ".join(cmd), flush=True)
-            subprocess.run(cmd, check=True)
+            cmds.append(cmd)
+    # the translation units are independent: compile them in parallel
+    def run(cmd):
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        for f in [ex.submit(run, c) for c in cmds]:
+            f.result()
     if force or _stale(LIB, objs):
         cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs]
         if verbose:

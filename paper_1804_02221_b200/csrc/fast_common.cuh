@@ -1,0 +1,175 @@
+// fast_common.cuh — device helpers shared by the fast-mode translation units
+// (kernels_fast.cu and the kernels_pl_*.cu instantiations of stage_pl.cuh).
+// Every TU that includes this gets its own copy of the constant operator table
+// (internal linkage); upload_fast_ops fills all of them.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ptx_async.cuh"
+#include "swdg_device.cuh"
+#include "swdg_launch.h"
+
+namespace swdg_dev {
+namespace {
+
+// ---- constant operator tables --------------------------------------------
+// per n1 = 2..16: D, Dtilde/4, Dtilde/8, Dhat, Vinv (n1^2 each) and w (n1)
+__host__ __device__ constexpr int ops_offset(int n1) {
+  int off = 0;
+  for (int k = 2; k < n1; ++k) off += 5 * k * k + k;
+  return off;
+}
+constexpr int kOpsTotal = ops_offset(17);
+__constant__ double c_ops[kOpsTotal];  // per TU (anonymous namespace)
+
+template <int N1>
+struct Ops {
+  static constexpr int base = ops_offset(N1);
+  static __device__ __forceinline__ double D(int a, int b) { return c_ops[base + a * N1 + b]; }
+  static __device__ __forceinline__ double D4(int a, int b) {
+    return c_ops[base + N1 * N1 + a * N1 + b];
+  }
+  static __device__ __forceinline__ double D8(int a, int b) {
+    return c_ops[base + 2 * N1 * N1 + a * N1 + b];
+  }
+  static __device__ __forceinline__ double Dh(int a, int b) {
+    return c_ops[base + 3 * N1 * N1 + a * N1 + b];
+  }
+  static __device__ __forceinline__ double Vinv(int a, int b) {
+    return c_ops[base + 4 * N1 * N1 + a * N1 + b];
+  }
+  static __device__ __forceinline__ double w(int a) { return c_ops[base + 5 * N1 * N1 + a]; }
+};
+
+
+__device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
+__device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
+
+// Fast reciprocal and reciprocal square root: the MUFU seed (rcp/rsqrt.approx)
+// refined by two Newton steps in explicit round-to-nearest operations — within
+// an ulp of the IEEE result, branch-free (no slow path), and bitwise identical
+// at every call site (both sides of a face must see the same numbers).
+__device__ __forceinline__ double frcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = __fma_rn(-x, r, 1.0);
+  r = __fma_rn(r, e, r);
+  e = __fma_rn(-x, r, 1.0);
+  return __fma_rn(r, e, r);
+}
+__device__ __forceinline__ double frsqrt(double x) {  // x > 0
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = __fma_rn(-__dmul_rn(x, y), y, 1.0);
+  y = __fma_rn(__dmul_rn(0.5, y), e, y);
+  e = __fma_rn(-__dmul_rn(x, y), y, 1.0);
+  return __fma_rn(__dmul_rn(0.5, y), e, y);
+}
+// sqrt(max(x, 0))
+__device__ __forceinline__ double fsqrt0(double x) {
+  return x > 0.0 ? __dmul_rn(x, frsqrt(x)) : 0.0;
+}
+
+// velocity desingularisation (physics.hpp:23-36): hard cut below h_des
+__device__ __forceinline__ void vel(double h, double hu, double hv, double h_des, double& u,
+                                    double& v) {
+  if (h >= h_des) {
+    const double r = frcp(h);
+    u = __dmul_rn(hu, r);
+    v = __dmul_rn(hv, r);
+  } else {
+    u = 0.0;
+    v = 0.0;
+  }
+}
+
+// gravity wave speed sqrt(g max(h, 0)) (fluxes.hpp:150)
+__device__ __forceinline__ double wave_c(double g, double h) {
+  return fsqrt0(__dmul_rn(g, h));
+}
+
+// Minus-side outward normal and J_surf from the face metrics (compute_metrics,
+// mesh.hpp:192-218): E/W faces take (y_eta, x_eta), S/N faces (y_xi, x_xi).
+// One reciprocal square root; explicit _rn operations: bitwise the same on both
+// sides of the face.
+__device__ __forceinline__ void face_normal(int face, double m0, double m1, double& nx,
+                                            double& ny, double& js) {
+  const double m2 = __fma_rn(m0, m0, __dmul_rn(m1, m1));
+  const double ri = frsqrt(m2);
+  js = __dmul_rn(m2, ri);
+  const double s = (face == 1 || face == 0) ? 1.0 : -1.0;  // E,S: +(m0,-m1); W,N: -(m0,-m1)
+  nx = __dmul_rn(s * m0, ri);
+  ny = __dmul_rn(-s * m1, ri);
+}
+
+// entropy-stable normal flux (fluxes.hpp:136-166) from both sides' states,
+// velocities and wave speeds, algebraically simplified: R|Lambda|R^T applied
+// directly (the zero/one entries of R dropped).
+__device__ __forceinline__ void es_flux_pre(double hm, double um, double vm, double cm,
+                                            double hp, double up, double vp, double cp,
+                                            double bm, double bp, double nx, double ny,
+                                            double g, double inv2g, double& f0, double& f1,
+                                            double& f2) {
+  const double unm = nx * um + ny * vm, utm = nx * vm - ny * um;
+  const double unp = nx * up + ny * vp, utp = nx * vp - ny * up;
+  const double havg = 0.5 * (hm + hp);
+  const double h2avg = 0.5 * (hm * hm + hp * hp);
+  const double uavg = 0.5 * (unm + unp), vavg = 0.5 * (utm + utp);
+  const double cavg = 0.5 * (cm + cp);
+  const double hu_ = havg * uavg;
+  double a0 = hu_;
+  double a1 = hu_ * uavg + 0.5 * g * h2avg;
+  double a2 = hu_ * vavg;
+  const double x1 = unp - unm, x2 = utp - utm;
+  const double x0 = g * ((hp + bp) - (hm + bm)) - 0.5 * (x1 * (unp + unm)) -
+                    0.5 * (x2 * (utp + utm));
+  const double r10 = uavg + cavg, r12 = uavg - cavg;
+  const double y0 = inv2g * fabs(r10) * (x0 + r10 * x1 + vavg * x2);
+  const double y1 = fabs(hu_) * x2;
+  const double y2 = inv2g * fabs(r12) * (x0 + r12 * x1 + vavg * x2);
+  a0 -= 0.5 * (y0 + y2);
+  a1 -= 0.5 * (r10 * y0 + r12 * y2);
+  a2 -= 0.5 * (vavg * (y0 + y2) + y1);
+  f0 = a0;
+  f1 = nx * a1 - ny * a2;
+  f2 = ny * a1 + nx * a2;
+}
+
+__device__ __forceinline__ void es_flux_fast(double hm, double hum, double hvm, double hp,
+                                             double hup, double hvp, double bm, double bp,
+                                             double nx, double ny, double g, double inv2g,
+                                             double h_des, double& f0, double& f1,
+                                             double& f2) {
+  double um, vm, up, vp;
+  vel(hm, hum, hvm, h_des, um, vm);
+  vel(hp, hup, hvp, h_des, up, vp);
+  es_flux_pre(hm, um, vm, wave_c(g, hm), hp, up, vp, wave_c(g, hp), bm, bp, nx, ny, g, inv2g,
+              f0, f1, f2);
+}
+
+__device__ __forceinline__ uint32_t round16(size_t b) { return (uint32_t)((b + 15) & ~size_t(15)); }
+
+template <class KERN>
+int grid_for(KERN kern, int threads, size_t bytes, int groups, int& cache) {
+  if (cache == 0) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, bytes);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cache = (per_sm > 0 ? per_sm : 1) * sms;
+  }
+  return groups < cache ? groups : cache;
+}
+
+// this TU's copy of the operator tables
+inline int upload_ops_local(int base, const double* tab, int len) {
+  return cudaMemcpyToSymbol(c_ops, tab, len * sizeof(double), base * sizeof(double)) ==
+                 cudaSuccess ? 0 : -2;
+}
+
+}  // namespace
+}  // namespace swdg_dev

@@ -38,103 +38,11 @@
 #include <cstdlib>
 #include <cstring>
 
-#include "ptx_async.cuh"
-#include "swdg_device.cuh"
-#include "swdg_launch.h"
+#include "fast_common.cuh"
 
 namespace swdg_dev {
 
-// ---- constant operator tables --------------------------------------------
-// per n1 = 2..16: D, Dtilde/4, Dtilde/8, Dhat, Vinv (n1^2 each) and w (n1)
-__host__ __device__ constexpr int ops_offset(int n1) {
-  int off = 0;
-  for (int k = 2; k < n1; ++k) off += 5 * k * k + k;
-  return off;
-}
-constexpr int kOpsTotal = ops_offset(17);
-__constant__ double c_ops[kOpsTotal];
-
-template <int N1>
-struct Ops {
-  static constexpr int base = ops_offset(N1);
-  static __device__ __forceinline__ double D(int a, int b) { return c_ops[base + a * N1 + b]; }
-  static __device__ __forceinline__ double D4(int a, int b) {
-    return c_ops[base + N1 * N1 + a * N1 + b];
-  }
-  static __device__ __forceinline__ double D8(int a, int b) {
-    return c_ops[base + 2 * N1 * N1 + a * N1 + b];
-  }
-  static __device__ __forceinline__ double Dh(int a, int b) {
-    return c_ops[base + 3 * N1 * N1 + a * N1 + b];
-  }
-  static __device__ __forceinline__ double Vinv(int a, int b) {
-    return c_ops[base + 4 * N1 * N1 + a * N1 + b];
-  }
-  static __device__ __forceinline__ double w(int a) { return c_ops[base + 5 * N1 * N1 + a]; }
-};
-
 namespace {
-
-__device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
-__device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
-
-__device__ __forceinline__ void vel(double h, double hu, double hv, double h_des, double& u,
-                                    double& v) {
-  if (h >= h_des) {
-    const double r = 1.0 / h;
-    u = hu * r;
-    v = hv * r;
-  } else {
-    u = 0.0;
-    v = 0.0;
-  }
-}
-
-// Minus-side outward normal and J_surf from the face metrics (compute_metrics,
-// mesh.hpp:192-218): E/W faces take (y_eta, x_eta), S/N faces (y_xi, x_xi).
-// Explicit _rn intrinsics: bitwise the same on both sides of the face.
-__device__ __forceinline__ void face_normal(int face, double m0, double m1, double& nx,
-                                            double& ny, double& js) {
-  js = __dsqrt_rn(__fma_rn(m0, m0, __dmul_rn(m1, m1)));
-  const double s = (face == 1 || face == 0) ? 1.0 : -1.0;  // E,S: +(m0,-m1); W,N: -(m0,-m1)
-  nx = __ddiv_rn(s * m0, js);
-  ny = __ddiv_rn(-s * m1, js);
-}
-
-// entropy-stable normal flux (fluxes.hpp:136-166), algebraically simplified:
-// R|Lambda|R^T applied directly (the zero/one entries of R dropped).
-__device__ __forceinline__ void es_flux_fast(double hm, double hum, double hvm, double hp,
-                                             double hup, double hvp, double bm, double bp,
-                                             double nx, double ny, double g, double inv2g,
-                                             double h_des, double& f0, double& f1,
-                                             double& f2) {
-  double um, vm, up, vp;
-  vel(hm, hum, hvm, h_des, um, vm);
-  vel(hp, hup, hvp, h_des, up, vp);
-  const double unm = nx * um + ny * vm, utm = nx * vm - ny * um;
-  const double unp = nx * up + ny * vp, utp = nx * vp - ny * up;
-  const double havg = 0.5 * (hm + hp);
-  const double h2avg = 0.5 * (hm * hm + hp * hp);
-  const double uavg = 0.5 * (unm + unp), vavg = 0.5 * (utm + utp);
-  const double cavg = 0.5 * (sqrt(g * smax(hm, 0.0)) + sqrt(g * smax(hp, 0.0)));
-  const double hu_ = havg * uavg;
-  double a0 = hu_;
-  double a1 = hu_ * uavg + 0.5 * g * h2avg;
-  double a2 = hu_ * vavg;
-  const double x1 = unp - unm, x2 = utp - utm;
-  const double x0 = g * ((hp + bp) - (hm + bm)) - 0.5 * (x1 * (unp + unm)) -
-                    0.5 * (x2 * (utp + utm));
-  const double r10 = uavg + cavg, r12 = uavg - cavg;
-  const double y0 = inv2g * fabs(r10) * (x0 + r10 * x1 + vavg * x2);
-  const double y1 = fabs(hu_) * x2;
-  const double y2 = inv2g * fabs(r12) * (x0 + r12 * x1 + vavg * x2);
-  a0 -= 0.5 * (y0 + y2);
-  a1 -= 0.5 * (r10 * y0 + r12 * y2);
-  a2 -= 0.5 * (vavg * (y0 + y2) + y1);
-  f0 = a0;
-  f1 = nx * a1 - ny * a2;
-  f2 = ny * a1 + nx * a2;
-}
 
 // ---- shared-memory plan (in doubles) ---------------------------------------
 template <int N1>
@@ -157,7 +65,6 @@ struct Plan {
   static constexpr size_t bytes = TOTAL * sizeof(double);
 };
 
-__device__ __forceinline__ uint32_t round16(size_t b) { return (uint32_t)((b + 15) & ~size_t(15)); }
 
 // thread 0: stream one group's line data (8 fields + face connectivity)
 template <int N1>
@@ -553,7 +460,7 @@ struct HL {
   static constexpr int WR = warps_for(E);   // warps per role
   static constexpr int WP = 2 * WR;         // warps per half (both directions)
   static constexpr int THREADS = 128 * WR;
-  static constexpr int PAD = N1 + 1;       // padded row stride
+  static constexpr int PAD = N1 | 1;       // odd padded row stride: conflict-free rows and columns
   static constexpr int EPAD = N1 * PAD;    // one padded element field
   static constexpr int GPAD = E * EPAD;
   static constexpr int GNP = (E * NP + 1) & ~1;
@@ -1305,6 +1212,38 @@ static void launch_visc_pre_n(const Mesh& M, const Phys& P, CState S, double* ep
 // and no barriers.  At these degrees the stage is a stream (HBM bound); what
 // matters is many independent loads in flight, which this gives at full
 // occupancy.
+// element data of one field: NP consecutive doubles, 16-byte vectors when the
+// element block is 16-byte aligned (NP even)
+template <int NP>
+__device__ __forceinline__ void ld_elem(const double* __restrict__ p, long long base,
+                                        double (&o)[NP]) {
+  if constexpr ((NP & 1) == 0) {
+    const double2* v = reinterpret_cast<const double2*>(p + base);
+#pragma unroll
+    for (int k = 0; k < NP / 2; ++k) {
+      const double2 t = __ldg(v + k);
+      o[2 * k] = t.x;
+      o[2 * k + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < NP; ++k) o[k] = __ldg(p + base + k);
+  }
+}
+
+template <int NP>
+__device__ __forceinline__ void st_elem(double* __restrict__ p, long long base,
+                                        const double (&o)[NP]) {
+  if constexpr ((NP & 1) == 0) {
+    double2* v = reinterpret_cast<double2*>(p + base);
+#pragma unroll
+    for (int k = 0; k < NP / 2; ++k) v[k] = make_double2(o[2 * k], o[2 * k + 1]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < NP; ++k) p[base + k] = o[k];
+  }
+}
+
 template <int N1, bool FORCE>
 __global__ void __launch_bounds__(128) k_stage_elem(Mesh M, Phys Ph, StageArgs A, Flags* F) {
   using O = Ops<N1>;
@@ -1315,19 +1254,21 @@ __global__ void __launch_bounds__(128) k_stage_elem(Mesh M, Phys Ph, StageArgs A
   const double g = Ph.g, h_des = Ph.h_des, inv2g = 1.0 / (2.0 * g), iw0 = 1.0 / M.w0;
   double h[NP], hu[NP], hv[NP], u[NP], v[NP], ye[NP], xe[NP], yx[NP], xx[NP];
   double r0[NP], r1[NP], r2[NP];
+  ld_elem<NP>(A.in.h, base, h);
+  ld_elem<NP>(A.in.hu, base, hu);
+  ld_elem<NP>(A.in.hv, base, hv);
+  ld_elem<NP>(M.ye, base, ye);
+  ld_elem<NP>(M.xe, base, xe);
+  ld_elem<NP>(M.yx, base, yx);
+  ld_elem<NP>(M.xx, base, xx);
+  int4 efs[4];
+#pragma unroll
+  for (int face = 0; face < 4; ++face) efs[face] = M.ef[(active ? e : 0) * 4 + face];
 #pragma unroll
   for (int q = 0; q < NP; ++q) {
-    h[q] = A.in.h[base + q];
-    hu[q] = A.in.hu[base + q];
-    hv[q] = A.in.hv[base + q];
-    ye[q] = M.ye[base + q];
-    xe[q] = M.xe[base + q];
-    yx[q] = M.yx[base + q];
-    xx[q] = M.xx[base + q];
     r0[q] = r1[q] = r2[q] = 0.0;
+    vel(h[q], hu[q], hv[q], h_des, u[q], v[q]);
   }
-#pragma unroll
-  for (int q = 0; q < NP; ++q) vel(h[q], hu[q], hv[q], h_des, u[q], v[q]);
   const double g2 = 2.0 * g;
   // volume: xi-lines (j fixed, metrics (y_eta, x_eta)) and eta-lines (i fixed, -(y_xi, x_xi))
 #pragma unroll
@@ -1355,10 +1296,13 @@ __global__ void __launch_bounds__(128) k_stage_elem(Mesh M, Phys Ph, StageArgs A
             r2[qb] += O::D8(b, a) * T2;
           }
         }
-  // interface fluxes at the 4 (N+1) face nodes
+  // interface fluxes at the 4 (N+1) face nodes; own velocities reused, one
+  // reciprocal and one square root per neighbour trace node
+  double bo[NP];
+  ld_elem<NP>(M.b, base, bo);
 #pragma unroll
   for (int face = 0; face < 4; ++face) {
-    const int4 ef = M.ef[(active ? e : 0) * 4 + face];
+    const int4 ef = efs[face];
     if (!active || !(ef.y & EF_PRESENT)) continue;
     const int nf = ef.y & EF_NBR_FACE_MASK;
 #pragma unroll
@@ -1366,45 +1310,39 @@ __global__ void __launch_bounds__(128) k_stage_elem(Mesh M, Phys Ph, StageArgs A
       const int q = face == 0 ? t * N1 : face == 1 ? (N1 - 1) * N1 + t
                   : face == 2 ? t * N1 + (N1 - 1) : t;
       const bool ew = face == 1 || face == 3;
-      const double bo = M.b[base + q];
-      double wm0, wm1, wm2, wp0, wp1, wp2, bm, bp, nx, ny, js, sgn = 1.0;
-      if (ef.y & EF_MINUS) {
+      const double co = wave_c(g, h[q]);
+      double hn, hun, hvn, bn, un = 0.0, vn = 0.0, nx, ny, js, sgn = 1.0;
+      if ((ef.y & EF_MINUS) && (ef.y & EF_WALL)) {  // exterior_state (mesh.hpp:382-386)
         face_normal(face, ew ? ye[q] : yx[q], ew ? xe[q] : xx[q], nx, ny, js);
-        wm0 = h[q];
-        wm1 = hu[q];
-        wm2 = hv[q];
-        bm = bo;
-        if (ef.y & EF_WALL) {
-          const double mn = wm1 * nx + wm2 * ny;
-          wp0 = wm0;
-          wp1 = wm1 - 2.0 * mn * nx;
-          wp2 = wm2 - 2.0 * mn * ny;
-          bp = bm;
-        } else {
-          const int tp = (ef.y & EF_REVERSED) ? N1 - 1 - t : t;
-          const long long nb = (long long)ef.x * NP + face_node(N1, nf, tp);
-          wp0 = A.in.h[nb];
-          wp1 = A.in.hu[nb];
-          wp2 = A.in.hv[nb];
-          bp = M.b[nb];
-        }
+        const double mn = hu[q] * nx + hv[q] * ny;
+        hn = h[q];
+        hun = hu[q] - 2.0 * mn * nx;
+        hvn = hv[q] - 2.0 * mn * ny;
+        bn = bo[q];
+        vel(hn, hun, hvn, h_des, un, vn);
       } else {
         const int tp = (ef.y & EF_REVERSED) ? N1 - 1 - t : t;
         const long long nb = (long long)ef.x * NP + face_node(N1, nf, tp);
-        const bool new_ = nf == 1 || nf == 3;
-        face_normal(nf, new_ ? M.ye[nb] : M.yx[nb], new_ ? M.xe[nb] : M.xx[nb], nx, ny, js);
-        wm0 = A.in.h[nb];
-        wm1 = A.in.hu[nb];
-        wm2 = A.in.hv[nb];
-        bm = M.b[nb];
-        wp0 = h[q];
-        wp1 = hu[q];
-        wp2 = hv[q];
-        bp = bo;
-        sgn = -1.0;
+        hn = __ldg(A.in.h + nb);
+        hun = __ldg(A.in.hu + nb);
+        hvn = __ldg(A.in.hv + nb);
+        bn = __ldg(M.b + nb);
+        vel(hn, hun, hvn, h_des, un, vn);
+        if (ef.y & EF_MINUS) {
+          face_normal(face, ew ? ye[q] : yx[q], ew ? xe[q] : xx[q], nx, ny, js);
+        } else {
+          const bool new_ = nf == 1 || nf == 3;
+          face_normal(nf, __ldg((new_ ? M.ye : M.yx) + nb), __ldg((new_ ? M.xe : M.xx) + nb),
+                      nx, ny, js);
+          sgn = -1.0;
+        }
       }
+      const double cn = wave_c(g, hn);
       double f0, f1, f2;
-      es_flux_fast(wm0, wm1, wm2, wp0, wp1, wp2, bm, bp, nx, ny, g, inv2g, h_des, f0, f1, f2);
+      if (sgn > 0.0)
+        es_flux_pre(h[q], u[q], v[q], co, hn, un, vn, cn, bo[q], bn, nx, ny, g, inv2g, f0, f1, f2);
+      else
+        es_flux_pre(hn, un, vn, cn, h[q], u[q], v[q], co, bn, bo[q], nx, ny, g, inv2g, f0, f1, f2);
       const double c = sgn * js * iw0;
       r0[q] += c * f0;
       r1[q] += c * f1;
@@ -1412,45 +1350,59 @@ __global__ void __launch_bounds__(128) k_stage_elem(Mesh M, Phys Ph, StageArgs A
     }
   }
   // node phase + element mean (no early returns: warp-collective reductions follow)
+  double jac[NP], sxa[NP], sya[NP];
+  ld_elem<NP>(M.jac, base, jac);
+  ld_elem<NP>(M.sx, base, sxa);
+  ld_elem<NP>(M.sy, base, sya);
+  const bool comb = A.stage > 0 && A.update;
   double area = 1.0, a0 = 0.0, a1 = 0.0, a2 = 0.0, mmin = 1.0e300;
   if (active) {
     area = 0.0;
 #pragma unroll
-  for (int q = 0; q < NP; ++q) {
-    const long long n = base + q;
-    const double jac = M.jac[n], ij = -1.0 / jac, hg2 = 0.5 * g * h[q];
-    double rh = r0[q] * ij;
-    double rhu = (r1[q] + hg2 * M.sx[n]) * ij;
-    double rhv = (r2[q] + hg2 * M.sy[n]) * ij;
-    if (FORCE) {
-      rh += A.fh[n];
-      rhu += A.fhu[n];
-      rhv += A.fhv[n];
+    for (int q = 0; q < NP; ++q) {
+      const long long n = base + q;
+      const double ij = -frcp(jac[q]), hg2 = 0.5 * g * h[q];
+      double rh = r0[q] * ij;
+      double rhu = (r1[q] + hg2 * sxa[q]) * ij;
+      double rhv = (r2[q] + hg2 * sya[q]) * ij;
+      if (FORCE) {
+        rh += A.fh[n];
+        rhu += A.fhu[n];
+        rhv += A.fhv[n];
+      }
+      if (A.rhs.h) {
+        A.rhs.h[n] = rh;
+        A.rhs.hu[n] = rhu;
+        A.rhs.hv[n] = rhv;
+      }
+      h[q] = h[q] + A.dt * rh;
+      hu[q] = hu[q] + A.dt * rhu;
+      hv[q] = hv[q] + A.dt * rhv;
     }
-    if (A.rhs.h) {
-      A.rhs.h[n] = rh;
-      A.rhs.hu[n] = rhu;
-      A.rhs.hv[n] = rhv;
+    if (comb) {
+      double wh[NP], whu[NP], whv[NP];
+      ld_elem<NP>(A.wn.h, base, wh);
+      ld_elem<NP>(A.wn.hu, base, whu);
+      ld_elem<NP>(A.wn.hv, base, whv);
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+        h[q] = A.ca * wh[q] + A.cb * h[q];
+        hu[q] = A.ca * whu[q] + A.cb * hu[q];
+        hv[q] = A.ca * whv[q] + A.cb * hv[q];
+      }
     }
-    double sh = h[q] + A.dt * rh, shu = hu[q] + A.dt * rhu, shv = hv[q] + A.dt * rhv;
-    if (A.stage > 0 && A.update) {
-      sh = A.ca * A.wn.h[n] + A.cb * sh;
-      shu = A.ca * A.wn.hu[n] + A.cb * shu;
-      shv = A.ca * A.wn.hv[n] + A.cb * shv;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const double wq = O::w(q / N1) * O::w(q % N1) * jac[q];
+      area += wq;
+      a0 += wq * h[q];
+      a1 += wq * hu[q];
+      a2 += wq * hv[q];
+      mmin = smin(mmin, h[q]);
     }
-    h[q] = sh;
-    hu[q] = shu;
-    hv[q] = shv;
-    const double wq = O::w(q / N1) * O::w(q % N1) * jac;
-    area += wq;
-    a0 += wq * sh;
-    a1 += wq * shu;
-    a2 += wq * shv;
-    mmin = smin(mmin, sh);
-  }
   }
   bool lim = active && A.update;
-  const double inv = 1.0 / area;
+  const double inv = frcp(area);
   const double avg0 = inv * a0, avg1 = inv * a1, avg2 = inv * a2;
   if (lim && avg0 < 0.0) {
     atomicExch(&F->reject, 1);
@@ -1478,11 +1430,14 @@ __global__ void __launch_bounds__(128) k_stage_elem(Mesh M, Phys Ph, StageArgs A
         shu = 0.0;
         shv = 0.0;
       }
-      A.out.h[base + q] = sh;
-      A.out.hu[base + q] = shu;
-      A.out.hv[base + q] = shv;
+      h[q] = sh;
+      hu[q] = shu;
+      hv[q] = shv;
       mine = smin(mine, sh);
     }
+    st_elem<NP>(A.out.h, base, h);
+    st_elem<NP>(A.out.hu, base, hu);
+    st_elem<NP>(A.out.hv, base, hv);
     key = order_key(mine);
   }
   // one atomic per warp for the limited count and the min height
@@ -1551,26 +1506,14 @@ int upload_fast_ops(int n1, const double* D, const double* Dt, const double* Dh,
     if (std::memcmp(tab, g_ops_host + base, len * sizeof(double)) != 0) return -1;
     return 0;
   }
-  if (cudaMemcpyToSymbol(c_ops, tab, len * sizeof(double), base * sizeof(double)) !=
-      cudaSuccess)
-    return -2;
+  if (upload_ops_local(base, tab, len) != 0) return -2;
+  for (auto up : {pl_upload_ops_a, pl_upload_ops_b, pl_upload_ops_c})
+    if (up(base, tab, len) != 0) return -2;
   std::memcpy(g_ops_host + base, tab, len * sizeof(double));
   g_ops_set[n1] = true;
   return 0;
 }
 
-template <class KERN>
-static int grid_for(KERN kern, int threads, size_t bytes, int groups, int& cache) {
-  if (cache == 0) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    int per_sm = 0, dev = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, bytes);
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cache = (per_sm > 0 ? per_sm : 1) * sms;
-  }
-  return groups < cache ? groups : cache;
-}
 
 // full-line kernel (N+1 <= 4 by default)
 template <int N1, bool FORCE>
@@ -1598,7 +1541,7 @@ static int variant_override() {
   static int v = -1;
   if (v < 0) {
     const char* s = getenv("SWDG_FAST_VARIANT");  // "elem" / "full" / "half" (experiments)
-    v = !s ? 0 : (s[0] == 'f' ? 1 : (s[0] == 'h' ? 2 : (s[0] == 'e' ? 3 : 0)));
+    v = !s ? 0 : (s[0] == 'f' ? 1 : (s[0] == 'h' ? 2 : (s[0] == 'e' ? 3 : (s[0] == 'p' ? 4 : 0))));
   }
   return v;
 }
@@ -1623,6 +1566,8 @@ static void launch_n(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
   if (ov == 3 && N1 <= 3) v = 3;
   if (ov == 1 && N1 <= 8) v = 1;
   if (ov == 2 && N1 >= 3) v = 2;
+  if (ov == 4) v = 4;
+  if (v == 4 && launch_pl_stage(M, P, A, F, st)) return;
   if constexpr (N1 <= 3) {
     if (v == 3) {
       if (A.fh) launch_elem<N1, true>(M, P, A, F, st);
