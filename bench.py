@@ -192,7 +192,8 @@ def measure_gpu_distributed(N: int, steps: int, warmup: int, viscous: bool, rank
     import torch
     from paper_1804_02221_b200 import swdg
     from paper_1804_02221_b200.distributed import (GpuPartition, TorchExchanger,
-                                                   compute_dt_distributed, try_step_distributed)
+                                                   compute_dt_distributed, run_steps_distributed,
+                                                   try_step_distributed)
 
     spec = spec_for(N)
     cfg = run_config(N, viscous)
@@ -209,17 +210,14 @@ def measure_gpu_distributed(N: int, steps: int, warmup: int, viscous: bool, rank
     integ.upload(st)
     ex = TorchExchanger(b, "cuda")
     dt = 0.1 * compute_dt_distributed(b, ex, 0.5, N, cfg.phys)
-    for s in range(warmup):
-        try_step_distributed(b, ex, s * dt, dt)
+    run_steps_distributed(b, ex, warmup, 0.0, dt)
     torch.distributed.barrier()
     torch.cuda.synchronize()
     l0 = integ.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ok = True
     with ClockSampler(dev) as clk:
         ev0.record(stream)
-        for s in range(steps):
-            ok &= try_step_distributed(b, ex, (warmup + s) * dt, dt)
+        ok = run_steps_distributed(b, ex, steps, warmup * dt, dt)
         ev1.record(stream)
         torch.cuda.synchronize()
     if not ok:

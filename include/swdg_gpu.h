@@ -254,6 +254,15 @@ int swdg_gpu_stage_run(swdg_gpu* ctx, int stage, double t, double dt);
 int swdg_gpu_step_flags(swdg_gpu* ctx, int32_t* reject, int32_t* abort);
 int swdg_gpu_step_commit(swdg_gpu* ctx, int accept, swdg_step_info* info);
 
+/* Overlap of the halo exchange with interior work.  set_interior names an
+ * owned element range [lo, hi) none of whose faces touches a ghost element
+ * (lo is rounded up and hi down to even indices); stage_run_part then runs
+ * part 1 = that range, which needs no halo data and may run while the state
+ * exchange is in flight, and part 2 = the rest of the owned elements, after the
+ * unpack (part 0 = all, like stage_run).  Exact mode runs everything in part 2. */
+int swdg_gpu_set_interior(swdg_gpu* ctx, int32_t lo, int32_t hi);
+int swdg_gpu_stage_run_part(swdg_gpu* ctx, int stage, double t, double dt, int part);
+
 #ifdef __cplusplus
 }
 #endif

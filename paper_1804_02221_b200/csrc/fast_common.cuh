@@ -74,16 +74,13 @@ __device__ __forceinline__ double fsqrt0(double x) {
 }
 
 // velocity desingularisation (physics.hpp:23-36): hard cut below h_des
+// (branch-free: the reciprocal of the clamped height, then a select)
 __device__ __forceinline__ void vel(double h, double hu, double hv, double h_des, double& u,
                                     double& v) {
-  if (h >= h_des) {
-    const double r = frcp(h);
-    u = __dmul_rn(hu, r);
-    v = __dmul_rn(hv, r);
-  } else {
-    u = 0.0;
-    v = 0.0;
-  }
+  const bool wet = h >= h_des;
+  const double r = frcp(wet ? h : 1.0);
+  u = wet ? __dmul_rn(hu, r) : 0.0;
+  v = wet ? __dmul_rn(hv, r) : 0.0;
 }
 
 // gravity wave speed sqrt(g max(h, 0)) (fluxes.hpp:150)

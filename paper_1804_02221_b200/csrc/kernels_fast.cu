@@ -71,7 +71,7 @@ template <int N1>
 __device__ __forceinline__ void issue_line(double* sm, const Mesh& M, const CState& in, int g,
                                            uint64_t* bar) {
   using P = Plan<N1>;
-  const int e0 = g * P::E, ne = min(P::E, M.n_owned - e0);
+  const int e0 = M.e_lo + g * P::E, ne = min(P::E, M.n_owned - e0);
   const uint32_t fb = round16((size_t)ne * P::NP * sizeof(double));
   const uint32_t eb = (uint32_t)(ne * 4 * sizeof(int4));
   mbar_expect_tx(bar, P::kLineFields * fb + eb);
@@ -88,7 +88,7 @@ template <int N1>
 __device__ __forceinline__ void issue_node(double* sm, const Mesh& M, const StageArgs& A, int g,
                                            uint64_t* bar) {
   using P = Plan<N1>;
-  const int e0 = g * P::E, ne = min(P::E, M.n_owned - e0);
+  const int e0 = M.e_lo + g * P::E, ne = min(P::E, M.n_owned - e0);
   const uint32_t fb = round16((size_t)ne * P::NP * sizeof(double));
   const bool wn = A.update && A.stage > 0;
   mbar_expect_tx(bar, (wn ? 4 : 1) * fb);
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(Plan<N1>::THREADS, 1)
   const int tid = threadIdx.x, el = tid / T, lt = tid % T;
   const bool xi = lt < N1;
   const int li = xi ? lt : lt - N1;
-  const int ngroups = (M.n_owned + E - 1) / E;
+  const int ngroups = (M.n_owned - M.e_lo + E - 1) / E;
   const double g = Ph.g, h_des = Ph.h_des, inv2g = 1.0 / (2.0 * g), iw0 = 1.0 / M.w0;
 
   if (tid == 0) {
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(Plan<N1>::THREADS, 1)
   auto idx = [&](int k) { return xi ? k * N1 + li : li * N1 + k; };
 
   for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-    const int e0 = grp * E, ne = min(E, M.n_owned - e0);
+    const int e0 = M.e_lo + grp * E, ne = min(E, M.n_owned - e0);
     const bool active = el < ne;
     const int e = e0 + el;
     mbar_wait(bar_line, ph_line);
@@ -471,14 +471,24 @@ struct HL {
   enum { N_JAC, N_SX, N_SY, N_WH, N_WHU, N_WHV, kNodeFields };
   static constexpr int XS = 3 * (NB0 + H);  // exchange slots per line
   static constexpr int LP = 32 * WP;        // lane slots per part (>= L; tail lanes idle)
-  // shared-memory plan, in doubles
+  // shared-memory plan, in doubles.  The line data is double-buffered (group
+  // g+1 streams in while g is computed) when the second buffer still lets the
+  // register-limited number of CTAs share an SM.
+  static constexpr int LBUF = kLineFields * GPAD;
+  static constexpr int rest() {
+    return 3 * GPAD + LP * XS + kNodeFields * GNP + E * 4 * N1 * kTr + 2 * E * 4 * 2 +
+           2 * 32 * WR * 6 + 2;
+  }
+  static constexpr int kCtas = THREADS > 128 ? 1 : (N1 <= 8 ? 3 : 2);  // register-bound residency
+  static constexpr bool DB = false && (size_t)(2 * LBUF + rest()) * 8 * kCtas + kCtas * 1024 <= 227 * 1024;
+  static constexpr int NBUF = DB ? 2 : 1;
   static constexpr int LINE = 0;
-  static constexpr int ACC = LINE + kLineFields * GPAD;
+  static constexpr int ACC = LINE + NBUF * LBUF;
   static constexpr int XCH = ACC + 3 * GPAD;
   static constexpr int NODE = XCH + LP * XS;
   static constexpr int TR = NODE + kNodeFields * GNP;  // [kTr][E][4][N1]
-  static constexpr int EFO = TR + E * 4 * N1 * kTr;     // int4 [E][4]
-  static constexpr int RED = EFO + E * 4 * 2;          // [2][32 WR xi lines][6]
+  static constexpr int EFO = TR + E * 4 * N1 * kTr;     // int4 [NBUF][E][4]
+  static constexpr int RED = EFO + 2 * E * 4 * 2;      // [2][32 WR xi lines][6]
   static constexpr int BAR = RED + 2 * 32 * WR * 6;
   static constexpr int TOTAL = BAR + 2;
   static constexpr size_t bytes = TOTAL * sizeof(double);
@@ -532,16 +542,16 @@ __device__ __forceinline__ void hl_intra(const HArr<N1>& h, const HArr<N1>& u,
 
 template <int N1, bool V>
 __device__ __forceinline__ void hl_prefetch_line(double* sm, const Mesh& M, const CState& in,
-                                                 const StageArgs& A, int g, int tid) {
+                                                 const StageArgs& A, int g, int tid, int buf) {
   using P = HL<N1, V>;
-  const int e0 = g * P::E, ne = min(P::E, M.n_owned - e0);
+  const int e0 = M.e_lo + g * P::E, ne = min(P::E, M.n_owned - e0);
   const long long base = (long long)e0 * P::NP;
   const int cnt = ne * P::NP;
   // one node per iteration, all 7 fields; divisions by compile-time constants
   for (int r = tid; r < cnt; r += P::THREADS) {
     const int el = r / P::NP, q = r - el * P::NP;
     const int i = q / N1, j = q - i * N1;
-    double* d = sm + P::LINE + el * P::EPAD + i * P::PAD + j;
+    double* d = sm + P::LINE + buf * P::LBUF + el * P::EPAD + i * P::PAD + j;
     const long long s = base + r;
     cp_async8(d + P::F_H * P::GPAD, in.h + s);
     cp_async8(d + P::F_HU * P::GPAD, in.hu + s);
@@ -558,7 +568,7 @@ __device__ __forceinline__ void hl_prefetch_line(double* sm, const Mesh& M, cons
     }
   }
   const int4* ef = M.ef + (long long)e0 * 4;
-  int4* dst = reinterpret_cast<int4*>(sm + P::EFO);
+  int4* dst = reinterpret_cast<int4*>(sm + P::EFO) + buf * P::E * 4;
   for (int idx = tid; idx < ne * 4; idx += P::THREADS)
     asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst + idx)),
                  "l"(ef + idx)
@@ -569,7 +579,7 @@ template <int N1, bool V>
 __device__ __forceinline__ void hl_issue_node(double* sm, const Mesh& M, const StageArgs& A,
                                               int g, uint64_t* bar) {
   using P = HL<N1, V>;
-  const int e0 = g * P::E, ne = min(P::E, M.n_owned - e0);
+  const int e0 = M.e_lo + g * P::E, ne = min(P::E, M.n_owned - e0);
   const uint32_t fb = round16((size_t)ne * P::NP * sizeof(double));
   const bool wn = A.update && A.stage > 0;
   mbar_expect_tx(bar, (wn ? 6 : 3) * fb);
@@ -635,7 +645,7 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, (N1 <= 8 ? 3 : 1))
   const int line = (xi ? 0 : P::WR * 32) + lr;  // exchange/reduction slot of the line
   const int k0 = part ? H : 0;                  // first node of this thread's half
   const int nk = part ? N1 - H : H;             // nodes held
-  const int ngroups = (M.n_owned + P::E - 1) / P::E;
+  const int ngroups = (M.n_owned - M.e_lo + P::E - 1) / P::E;
   const double g = Ph.g, h_des = Ph.h_des, inv2g = 1.0 / (2.0 * g), iw0 = 1.0 / M.w0;
   const double g2 = 2.0 * g;
 
@@ -644,15 +654,16 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, (N1 <= 8 ? 3 : 1))
     fence_mbar_init();
   }
   if ((int)blockIdx.x >= ngroups) return;
-  hl_prefetch_line<N1, VISC>(sm, M, A.in, A, blockIdx.x, tid);
+  hl_prefetch_line<N1, VISC>(sm, M, A.in, A, blockIdx.x, tid, 0);
   cp_async_commit();
   uint32_t ph_node = 0;
+  int buf = 0;
 
   // padded in-element offset of node k of this line
   auto pidx = [&](int k) { return xi ? k * PAD + li : li * PAD + k; };
 
-  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-    const int e0 = grp * P::E, ne = min(P::E, M.n_owned - e0);
+  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x, buf = P::DB ? buf ^ 1 : 0) {
+    const int e0 = M.e_lo + grp * P::E, ne = min(P::E, M.n_owned - e0);
     const bool active = line_ok && el < ne;
     const int e = e0 + el;
     cp_async_wait_all();
@@ -664,7 +675,7 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, (N1 <= 8 ? 3 : 1))
 
     // ---- own half -> registers, gathers for the own endpoint
     double h[S], u[S], v[S], hu[S], hv[S], Am[S], Bm[S], r0[S], r1[S], r2[S];
-    const double* Lb = sm + P::LINE + el * P::EPAD;
+    const double* Lb = sm + P::LINE + buf * P::LBUF + el * P::EPAD;
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       r0[s] = r1[s] = r2[s] = 0.0;
@@ -686,7 +697,7 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, (N1 <= 8 ? 3 : 1))
     constexpr int TRS = P::E * 4 * N1;
     double* tr = sm + P::TR + (el * 4 + face) * N1 + li;
     if (active) {
-      const int4 ef = reinterpret_cast<const int4*>(sm + P::EFO)[el * 4 + face];
+      const int4 ef = reinterpret_cast<const int4*>(sm + P::EFO)[(buf * P::E + el) * 4 + face];
       efy = ef.y;
       const long long own = (long long)e * NP + face_node(N1, face, li);
       cp_async8(tr + 6 * TRS, M.b + own);
@@ -712,6 +723,11 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, (N1 <= 8 ? 3 : 1))
       }
     }
     cp_async_commit();
+    if constexpr (P::DB) {  // next group's line data into the other buffer, now
+      const int gn = grp + gridDim.x;
+      if (gn < ngroups) hl_prefetch_line<N1, VISC>(sm, M, A.in, A, gn, tid, buf ^ 1);
+      cp_async_commit();
+    }
 
     // ---- volume: pairs inside the own half (+ the corner diagonal); part is
     // warp-uniform, so each warp runs one fully unrolled, constant-operand body
@@ -809,9 +825,9 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, (N1 <= 8 ? 3 : 1))
         r2[s] += xch(3 * s + 2);
       }
     }
-    {  // prefetch the next group's line data behind the rest of this group
+    if constexpr (!P::DB) {  // single buffer: prefetch behind the rest of this group
       const int gn = grp + gridDim.x;
-      if (gn < ngroups) hl_prefetch_line<N1, VISC>(sm, M, A.in, A, gn, tid);
+      if (gn < ngroups) hl_prefetch_line<N1, VISC>(sm, M, A.in, A, gn, tid, 0);
       cp_async_commit();
     }
 
@@ -1248,7 +1264,7 @@ template <int N1, bool FORCE>
 __global__ void __launch_bounds__(128) k_stage_elem(Mesh M, Phys Ph, StageArgs A, Flags* F) {
   using O = Ops<N1>;
   constexpr int NP = N1 * N1;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int e = M.e_lo + blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = e < M.n_owned;
   const long long base = (long long)(active ? e : 0) * NP;
   const double g = Ph.g, h_des = Ph.h_des, inv2g = 1.0 / (2.0 * g), iw0 = 1.0 / M.w0;
@@ -1452,7 +1468,7 @@ __global__ void __launch_bounds__(128) k_stage_elem(Mesh M, Phys Ph, StageArgs A
 template <int N1, bool FORCE>
 static void launch_elem(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
                         cudaStream_t st) {
-  k_stage_elem<N1, FORCE><<<(M.n_owned + 127) / 128, 128, 0, st>>>(M, P, A, F);
+  k_stage_elem<N1, FORCE><<<(M.n_owned - M.e_lo + 127) / 128, 128, 0, st>>>(M, P, A, F);
 }
 
 // geometry-only split-source coefficients (dg_rhs.hpp:159-176), one thread per node
@@ -1522,7 +1538,7 @@ static void launch_full(const Mesh& M, const Phys& P, const StageArgs& A, Flags*
   using PL = Plan<N1>;
   static int cache = 0;
   auto kern = k_stage<N1, FORCE>;
-  const int grid = grid_for(kern, PL::THREADS, PL::bytes, (M.n_owned + PL::E - 1) / PL::E, cache);
+  const int grid = grid_for(kern, PL::THREADS, PL::bytes, (M.n_owned - M.e_lo + PL::E - 1) / PL::E, cache);
   kern<<<grid, PL::THREADS, PL::bytes, st>>>(M, P, A, F);
 }
 
@@ -1533,7 +1549,7 @@ static void launch_half(const Mesh& M, const Phys& P, const StageArgs& A, Flags*
   using PL = HL<N1, VISC>;
   static int cache = 0;
   auto kern = k_stage_hl<N1, FORCE, VISC>;
-  const int grid = grid_for(kern, PL::THREADS, PL::bytes, (M.n_owned + PL::E - 1) / PL::E, cache);
+  const int grid = grid_for(kern, PL::THREADS, PL::bytes, (M.n_owned - M.e_lo + PL::E - 1) / PL::E, cache);
   kern<<<grid, PL::THREADS, PL::bytes, st>>>(M, P, A, F);
 }
 

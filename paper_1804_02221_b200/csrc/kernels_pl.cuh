@@ -30,7 +30,7 @@ void launch_pl(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F, cudaS
   using PL = PLP<N1, C::P, C::E>;
   static int cache = 0;
   auto kern = k_stage_pl<N1, C::P, C::E, C::MINB, FORCE>;
-  const int grid = grid_for(kern, PL::THREADS, PL::bytes, (M.n_owned + PL::E - 1) / PL::E, cache);
+  const int grid = grid_for(kern, PL::THREADS, PL::bytes, (M.n_owned - M.e_lo + PL::E - 1) / PL::E, cache);
   kern<<<grid, PL::THREADS, PL::bytes, st>>>(M, P, A, F);
 }
 

@@ -304,7 +304,7 @@ template <class PL>
 __device__ __forceinline__ void pl_prefetch_line(double* sm, const Mesh& M, const CState& in,
                                                  int g, int tid) {
   constexpr int N1 = PL::N1, NP = PL::NP, GP = PL::GPAD;
-  const int e0 = g * PL::E, ne = min(PL::E, M.n_owned - e0);
+  const int e0 = M.e_lo + g * PL::E, ne = min(PL::E, M.n_owned - e0);
   const long long base = (long long)e0 * NP;
   const int cnt = ne * NP;
   for (int r = tid; r < cnt; r += PL::THREADS) {
@@ -343,7 +343,7 @@ __device__ __forceinline__ void l2_prefetch(const double* p, long long first, lo
 template <class PL>
 __device__ __forceinline__ int pl_issue_node(double* sm, const Mesh& M, const StageArgs& A, int g,
                                              uint64_t* bar) {
-  const int e0 = g * PL::E, ne = min(PL::E, M.n_owned - e0);
+  const int e0 = M.e_lo + g * PL::E, ne = min(PL::E, M.n_owned - e0);
   const long long off = (long long)e0 * PL::NP;
   const int shift = (int)(off & 1);
   const uint32_t fb = round16((size_t)(ne * PL::NP + shift) * sizeof(double));
@@ -365,7 +365,7 @@ __device__ __forceinline__ int pl_issue_node(double* sm, const Mesh& M, const St
 template <class PL>
 __device__ __forceinline__ void pl_prefetch_l2(const Mesh& M, const StageArgs& A, int g,
                                                bool line_fields) {
-  const int e0 = g * PL::E, ne = min(PL::E, M.n_owned - e0);
+  const int e0 = M.e_lo + g * PL::E, ne = min(PL::E, M.n_owned - e0);
   const long long off = (long long)e0 * PL::NP, cnt = (long long)ne * PL::NP;
   if (line_fields) {
     const double* f[7] = {A.in.h, A.in.hu, A.in.hv, M.ye, M.xe, M.yx, M.xx};
@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(PLP<N1, P, E>::THREADS, MINB)
   const bool xi = line < LPD;
   const int ld = xi ? line : line - LPD;
   const int el = line_ok ? ld / N1 : 0, li = line_ok ? ld - (ld / N1) * N1 : 0;
-  const int ngroups = (M.n_owned + E - 1) / E;
+  const int ngroups = (M.n_owned - M.e_lo + E - 1) / E;
   const double g = Ph.g, h_des = Ph.h_des, inv2g = 1.0 / (2.0 * g), iw0 = 1.0 / M.w0;
 
   if (tid == 0) {
@@ -512,7 +512,7 @@ __global__ void __launch_bounds__(PLP<N1, P, E>::THREADS, MINB)
   uint32_t ph_node = 0;
 
   for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-    const int e0 = grp * E, ne = min(E, M.n_owned - e0);
+    const int e0 = M.e_lo + grp * E, ne = min(E, M.n_owned - e0);
     const bool active = line_ok && el < ne;
     const int e = e0 + el;
     cp_async_wait_all();

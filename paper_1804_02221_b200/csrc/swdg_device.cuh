@@ -27,7 +27,10 @@ struct Phys {
 };
 
 struct Mesh {
-  int K, n_owned, n1, np, degree;
+  // the stage kernels advance elements [e_lo, n_owned): e_lo = 0 normally, a
+  // sub-range when a partition runs its interior and halo-adjacent elements as
+  // separate launches (overlap with the halo exchange)
+  int K, n_owned, n1, np, degree, e_lo;
   double w0;
   // Operators1D (operators.hpp:35-52), device copies
   const double *w, *D, *Dt, *Dh, *Vinv;

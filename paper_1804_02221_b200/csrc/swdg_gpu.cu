@@ -3,6 +3,8 @@
 // (kernels_exact.cu) or fast (kernels_fast.cu) kernels on one B200.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -66,6 +68,7 @@ struct swdg_gpu {
   double *fvu = nullptr, *fvv = nullptr, *gvu = nullptr, *gvv = nullptr;
   double *fh = nullptr, *fhu = nullptr, *fhv = nullptr;
   double *partial = nullptr, *sums = nullptr;
+  int int_lo = 0, int_hi = 0;   // interior element range (halo overlap), empty by default
   Flags* flags = nullptr;       // device, 3 (one per stage)
   Flags* flags_init = nullptr;  // device, reset image
   Flags* flags_h = nullptr;     // pinned host mirror, 3
@@ -202,7 +205,7 @@ double stage_visc(swdg_gpu* c, CState in, Flags* F) {
 // The stage proper: dW/dt of `in` (+ update into `out` and the limiter/reject
 // flags in F), consuming the flux pairs of a preceding stage_visc.
 void stage_main(swdg_gpu* c, CState in, double* const* out, int k, double t, double dt,
-                bool viscous, double* const* rhs, Flags* F) {
+                bool viscous, double* const* rhs, Flags* F, const Mesh* range = nullptr) {
   StageArgs a{};
   a.in = in;
   a.wn = cs(c->W);
@@ -227,7 +230,8 @@ void stage_main(swdg_gpu* c, CState in, double* const* out, int k, double t, dou
     a.fhv = c->fhv;
   }
   if (c->fast) {
-    c->launches += launch_fast_stage(c->M, c->phys, a, F, c->stream);
+    const Mesh& M = range ? *range : c->M;
+    if (M.n_owned > M.e_lo) c->launches += launch_fast_stage(M, c->phys, a, F, c->stream);
   } else {
     c->launches += launch_exact_rhs_stage(c->M, c->phys, a, c->stream);
     if (out) c->launches += launch_exact_limit(c->M, c->phys, st(out), F, c->stream);
@@ -297,9 +301,15 @@ void allocate(swdg_gpu* c, int K, int n_owned, int N, const std::vector<int4>& e
   const long long nn = (long long)K * np, nf = (long long)K * 4 * n1;
   c->nn = nn;
   c->nf = nf;
-  // nodal arrays sit at a padded stride: every array starts 16-byte aligned
-  // and a bulk copy of the last partial element group may round up by 8 bytes
-  const long long nnp = ((nn + 1) & ~1ll) + 2;
+  // nodal arrays sit at a padded stride: every array starts 16-byte aligned,
+  // a bulk copy of the last partial element group may round up by 8 bytes, and
+  // consecutive arrays are staggered by an odd multiple of 256 bytes so the
+  // same node of different fields does not land on the same DRAM channel
+  static const long long kStagger = [] {  // SWDG_NNP_PAD: experiments only
+    const char* s = getenv("SWDG_NNP_PAD");
+    return s ? (atoll(s) & ~1ll) : 544ll;
+  }();
+  const long long nnp = ((nn + 511) & ~511ll) + kStagger;
   c->geo = c->dalloc<double>(10 * nnp + 4 * nf);
   double* ops = c->dalloc<double>(n1 + 4 * np);
   upload(ops, ops_w, n1, "weights");
@@ -313,6 +323,7 @@ void allocate(swdg_gpu* c, int K, int n_owned, int N, const std::vector<int4>& e
   Mesh& M = c->M;
   M.K = K;
   M.n_owned = n_owned;
+  M.e_lo = 0;
   M.n1 = n1;
   M.np = np;
   M.degree = N;
@@ -926,6 +937,48 @@ int swdg_gpu_stage_run(swdg_gpu* c, int k, double t, double dt) {
     if (k < 0 || k > 2) throw InputError{"stage_run: bad stage"};
     stage_main(c, cs(stage_input(c, k)), stage_output(c, k), k, t, dt,
                c->params.visc_enabled != 0, nullptr, c->flags + k);
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_set_interior(swdg_gpu* c, int32_t lo, int32_t hi) {
+  return guarded(c, [&] {
+    if (lo < 0 || hi < lo || hi > c->M.n_owned) throw InputError{"set_interior: bad range"};
+    // even bounds keep the stage kernels' element groups 16-byte aligned
+    lo = (lo + 1) & ~1;
+    hi = hi & ~1;
+    c->int_lo = lo;
+    c->int_hi = hi > lo ? hi : lo;
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_stage_run_part(swdg_gpu* c, int k, double t, double dt, int part) {
+  return guarded(c, [&] {
+    if (k < 0 || k > 2) throw InputError{"stage_run_part: bad stage"};
+    if (part < 0 || part > 2) throw InputError{"stage_run_part: bad part"};
+    const CState in = cs(stage_input(c, k));
+    double* const* out = stage_output(c, k);
+    const bool visc = c->params.visc_enabled != 0;
+    if (part == 0 || !c->fast || c->int_hi <= c->int_lo) {
+      // everything at once (exact mode and partitions without an interior run
+      // all of it after the exchange)
+      if (part != 1) stage_main(c, in, out, k, t, dt, visc, nullptr, c->flags + k);
+      return SWDG_OK;
+    }
+    Mesh r = c->M;
+    if (part == 1) {
+      r.e_lo = c->int_lo;
+      r.n_owned = c->int_hi;
+      stage_main(c, in, out, k, t, dt, visc, nullptr, c->flags + k, &r);
+    } else {
+      r.e_lo = 0;
+      r.n_owned = c->int_lo;
+      stage_main(c, in, out, k, t, dt, visc, nullptr, c->flags + k, &r);
+      r.e_lo = c->int_hi;
+      r.n_owned = c->M.n_owned;
+      stage_main(c, in, out, k, t, dt, visc, nullptr, c->flags + k, &r);
+    }
     return SWDG_OK;
   });
 }

@@ -63,6 +63,11 @@ class TorchExchanger:
         self.recv = torch.zeros(max(nr, 1) * 4, dtype=torch.float64, device=device)
 
     def exchange(self, what: int, k: int):
+        self.finish(self.start(what, k))
+
+    def start(self, what: int, k: int):
+        """pack + post the sends/receives; NCCL runs them on its own stream, after
+        the pack on the current stream.  Returns the handle `finish` takes."""
         dist = self.torch.distributed
         nf = 4 if what else 3
         self.b.pack(what, k, self.send)
@@ -74,9 +79,13 @@ class TorchExchanger:
             o, n = self.roff[p]
             if n:
                 ops.append(dist.P2POp(dist.irecv, self.recv[o * nf:(o + n) * nf], p))
-        if ops:
-            for r in dist.batch_isend_irecv(ops):
-                r.wait()
+        return what, k, (dist.batch_isend_irecv(ops) if ops else [])
+
+    def finish(self, handle):
+        """the current stream waits for the transfers, then unpacks"""
+        what, k, works = handle
+        for r in works:
+            r.wait()
         self.b.unpack(what, k, self.recv)
 
     def all_max(self, vals):
@@ -113,10 +122,25 @@ class LoopbackExchanger:
             b.unpack(what, k, recv)
 
 
+INTERIOR, BOUNDARY = 1, 2
+
+
+def _overlap(b: Backend) -> bool:
+    """inviscid partitions with an interior run the stage in two parts, the
+    interior one while the state halo is in flight"""
+    return not b.visc and getattr(b, "has_interior", False)
+
+
 def try_step_distributed(b: Backend, ex, t: float, dt: float) -> bool:
     """One SSPRK3 step of this rank's partition, in lock step with the other ranks."""
     b.step_begin()
     for k in range(3):
+        if _overlap(b) and hasattr(ex, "start"):
+            h = ex.start(0, k)
+            b.stage_run_part(k, t, dt, INTERIOR)
+            ex.finish(h)
+            b.stage_run_part(k, t, dt, BOUNDARY)
+            continue
         ex.exchange(0, k)
         if b.visc:
             b.stage_visc(k, t, dt)
@@ -131,11 +155,47 @@ def try_step_distributed(b: Backend, ex, t: float, dt: float) -> bool:
     return accept
 
 
+def run_steps_distributed(b: Backend, ex, nsteps: int, t: float, dt: float) -> bool:
+    """Device-resident stepping for throughput runs (the partitioned counterpart of
+    swdg_gpu_run_steps): no per-step host synchronisation; the stage flags
+    accumulate over the run and are reduced over the ranks once at the end.
+    Returns False if any stage of any rank signalled a reject (the caller treats
+    the run as invalid)."""
+    b.step_begin()
+    for s in range(nsteps):
+        ts = t + s * dt
+        for k in range(3):
+            if _overlap(b) and hasattr(ex, "start"):
+                h = ex.start(0, k)
+                b.stage_run_part(k, ts, dt, INTERIOR)
+                ex.finish(h)
+                b.stage_run_part(k, ts, dt, BOUNDARY)
+                continue
+            ex.exchange(0, k)
+            if b.visc:
+                b.stage_visc(k, ts, dt)
+                ex.exchange(1, k)
+            b.stage_run(k, ts, dt)
+        b.step_commit(True)
+    rej, ab = b.step_flags()
+    rej, ab = ex.all_max([float(rej), float(ab)])
+    if ab:
+        raise swdg.NumericalAbort("negative water height without limiter")
+    return not rej
+
+
 def try_step_loopback(bs, ex: LoopbackExchanger, t: float, dt: float) -> bool:
     """All partitions of one process, one SSPRK3 step (the same schedule)."""
     for b in bs:
         b.step_begin()
     for k in range(3):
+        if all(_overlap(b) for b in bs):  # interior before the exchange, like NCCL ranks
+            for b in bs:
+                b.stage_run_part(k, t, dt, INTERIOR)
+            ex.exchange_all(0, k)
+            for b in bs:
+                b.stage_run_part(k, t, dt, BOUNDARY)
+            continue
         ex.exchange_all(0, k)
         if bs[0].visc:
             for b in bs:
@@ -184,6 +244,9 @@ class GpuPartition(Backend):
                            ("swdg_gpu_step_begin", [vp]),
                            ("swdg_gpu_stage_visc", [vp, C.c_int, C.c_double, C.c_double]),
                            ("swdg_gpu_stage_run", [vp, C.c_int, C.c_double, C.c_double]),
+                           ("swdg_gpu_set_interior", [vp, C.c_int32, C.c_int32]),
+                           ("swdg_gpu_stage_run_part", [vp, C.c_int, C.c_double, C.c_double,
+                                                        C.c_int]),
                            ("swdg_gpu_step_flags", [vp, i32p, i32p]),
                            ("swdg_gpu_step_commit", [vp, C.c_int, C.POINTER(swdg.StepInfoC)]),
                            ("swdg_gpu_dt_candidates", [vp, C.POINTER(C.c_double),
@@ -200,6 +263,10 @@ class GpuPartition(Backend):
         self._chk(L.swdg_gpu_halo_setup(self.integ._h, len(send), send.ctypes.data_as(i32p),
                                         len(recv), recv.ctypes.data_as(i32p)))
         self.info = swdg.StepInfoC()
+        from .partition import interior_range
+        lo, hi = interior_range(lm.faces, lm.n_owned)
+        self._chk(L.swdg_gpu_set_interior(self.integ._h, lo, hi))
+        self.has_interior = hi - lo >= 2
         # halo buffers are torch tensors moved by torch (NCCL / copies): order the
         # context's kernels on torch's current stream
         import torch
@@ -246,6 +313,9 @@ class GpuPartition(Backend):
 
     def stage_run(self, k, t, dt):
         self._chk(self.L.swdg_gpu_stage_run(self.integ._h, k, t, dt))
+
+    def stage_run_part(self, k, t, dt, part):
+        self._chk(self.L.swdg_gpu_stage_run_part(self.integ._h, k, t, dt, part))
 
     def step_flags(self):
         r, a = C.c_int32(), C.c_int32()

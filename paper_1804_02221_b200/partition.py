@@ -159,6 +159,30 @@ def local_mesh(mesh, P: int, rank: int) -> LocalMesh:
     return LocalMesh(mesh.degree, len(gids), n_owned, gids, lf, ords, arrays, plan)
 
 
+def interior_range(faces: np.ndarray, n_owned: int):
+    """The longest run [lo, hi) of owned elements none of whose faces touches a
+    ghost (local id >= n_owned): the part of a stage that needs no halo data and
+    can run while the exchange is in flight."""
+    f = np.asarray(faces, np.int64).reshape(-1, 6)
+    inter = f[:, 5] == 0
+    em, ep = f[:, 0], np.where(inter, f[:, 2], f[:, 0])
+    touch = np.zeros(n_owned + 1, bool)
+    cut = inter & ((em >= n_owned) | (ep >= n_owned))
+    for a, b in ((em, ep), (ep, em)):
+        sel = cut & (a < n_owned)
+        touch[a[sel]] = True
+    best, lo = (0, 0), None
+    for e in range(n_owned + 1):
+        if e < n_owned and not touch[e]:
+            if lo is None:
+                lo = e
+        elif lo is not None:
+            if e - lo > best[1] - best[0]:
+                best = (lo, e)
+            lo = None
+    return best
+
+
 def scatter_state(state, lm: LocalMesh):
     """Global state -> this rank's local arrays (owned + ghosts)."""
     np_ = lm.n1 * lm.n1

@@ -19,7 +19,7 @@ from typing import Callable, Optional
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "_lib", "libswdg_gpu.so")
+LIB_PATH = os.environ.get("SWDG_LIB") or os.path.join(_PKG, "_lib", "libswdg_gpu.so")
 _dp = C.POINTER(C.c_double)
 
 SWDG_OK, SWDG_ERR_CUDA, SWDG_ERR_INPUT, SWDG_ERR_ABORT = 0, 1, 2, 3

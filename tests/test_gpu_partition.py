@@ -67,6 +67,26 @@ def test_partitioned_equals_single(mode, sid, kx, deg, P):
         assert beq(got, s)
 
 
+@pytest.mark.parametrize("mode", [swdg.MODE_EXACT, swdg.MODE_FAST])
+@pytest.mark.parametrize("sid,kx,deg,P", [("wetdry_dambreak", 12, 3, 2),
+                                          ("oscillating_lake", 16, 4, 3),
+                                          ("parabolic_dam_dry", 12, 2, 2)])
+def test_partitioned_overlap_inviscid(mode, sid, kx, deg, P):
+    """Inviscid partitions with an interior run each stage as interior (before the
+    exchange) + the halo-adjacent rest (after it): still bitwise the single run."""
+    m, st = ref.scenario_mesh(sid, kx, kx, deg)
+    p, cfg = scenario_params(sid, deg, visc_enabled=0.0)
+    dt = ref.compute_dt(m, p, st, cfg["cfl"])
+    lo, hi = part.interior_range(part.local_mesh(m, P, 0).faces, part.local_mesh(m, P, 0).n_owned)
+    assert hi - lo >= 2  # the split path is the one exercised
+    single = swdg.TimeIntegrator(m, cfg_from(p, mode))
+    want = swdg.State(*[a.copy() for a in st])
+    acc_ref = [single.try_step(want, k * dt, dt) for k in range(4)]
+    got, acc = run_parts(m, cfg_from(p, mode), st, P, dt, 4)
+    assert acc == acc_ref
+    assert beq(got, want.arrays())
+
+
 def test_structured_partitions_match_global_mesh():
     """Device-generated partitions (owned + ghost elements by global id) carry exactly
     the global mesh's geometry, and partitioned fast stepping equals the global run."""
