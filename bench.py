@@ -41,6 +41,30 @@ def frozen_counts(N: int, viscous: bool):
     return bytes_node, flops_elem / (n1 * n1)
 
 
+def stage_kernel(N: int, viscous: bool) -> str:
+    """the fused stage kernel launch_fast_stage picks for this degree"""
+    n1 = N + 1
+    if viscous:
+        return "k_stage_hl<%d,..,visc> (half-line) + k_visc_pre<%d>" % (n1, n1)
+    if n1 <= 3:
+        return "k_stage_elem<%d> (element per thread)" % n1
+    if n1 <= 5:
+        return "k_stage<%d> (full-line)" % n1
+    return "k_stage_hl<%d> (half-line)" % n1
+
+
+def ncu_traffic(N: int, viscous: bool):
+    """DRAM bytes per launch of the stage kernel from the committed ncu --set full
+    capture of this configuration (profiles/r01_ncu_traffic.json), or None"""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+            d = json.load(f)
+        e = d.get("%s_N%d" % ("visc" if viscous else "inv", N))
+        return None if e is None else float(e["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 def peaks():
     p = {"hbm_gbs": 6541.8, "fp64_tflops": 36.8, "hbm_src": "fallback", "fp64_src": "fallback"}
     try:
@@ -365,8 +389,10 @@ def main():
             "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
             "frac": (achieved_gbs / pk["hbm_gbs"]) if bound == "hbm"
             else achieved_tf / pk["fp64_tflops"],
-            "traffic": None,
-            "kernel": "k_stage_lines (fused stage)",
+            "traffic": ncu_traffic(N, args.viscous),
+            "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, one launch, cold L2)",
+            "algorithmic_bytes_per_launch": bytes_node * r["nn"],
+            "kernel": stage_kernel(N, args.viscous),
             "algorithmic_bytes_per_node": bytes_node, "algorithmic_flops_per_node": flops_node,
             "achieved_fp64_tflops": achieved_tf, "achieved_gbs": achieved_gbs,
             "roof_dof_per_s": roof_dofs, "frac_of_roof": value / world / roof_dofs,

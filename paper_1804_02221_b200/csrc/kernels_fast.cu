@@ -44,6 +44,12 @@ namespace swdg_dev {
 
 namespace {
 
+// dynamic group scheduling: groups [0, gridDim.x) are taken statically by the
+// first wave, the rest in claim order (persistent CTAs stay in one wavefront)
+__device__ __forceinline__ int next_group(int* ctr, int grp) {
+  return ctr ? (int)gridDim.x + atomicAdd(ctr, 1) : grp + (int)gridDim.x;
+}
+
 // ---- shared-memory plan (in doubles) ---------------------------------------
 template <int N1>
 struct Plan {
@@ -130,7 +136,8 @@ __global__ void __launch_bounds__(Plan<N1>::THREADS, 1)
   // eta-line i=li -> (li,k)
   auto idx = [&](int k) { return xi ? k * N1 + li : li * N1 + k; };
 
-  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+  __shared__ int s_next;  // the next group, claimed by thread 0
+  for (int grp = blockIdx.x; grp < ngroups; grp = s_next) {
     const int e0 = M.e_lo + grp * E, ne = min(E, M.n_owned - e0);
     const bool active = el < ne;
     const int e = e0 + el;
@@ -180,7 +187,8 @@ __global__ void __launch_bounds__(Plan<N1>::THREADS, 1)
     cp_async_commit();
     __syncthreads();  // line buffer and connectivity consumed
     if (tid == 0) {
-      const int gn = grp + gridDim.x;
+      const int gn = next_group(A.gctr, grp);
+      s_next = gn;
       if (gn < ngroups) issue_line<N1>(sm, M, A.in, gn, bar_line);
       issue_node<N1>(sm, M, A, grp, bar_node);
     }
@@ -662,7 +670,8 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, (N1 <= 8 ? 3 : 1))
   // padded in-element offset of node k of this line
   auto pidx = [&](int k) { return xi ? k * PAD + li : li * PAD + k; };
 
-  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x, buf = P::DB ? buf ^ 1 : 0) {
+  __shared__ int s_next;  // the next group, claimed by thread 0
+  for (int grp = blockIdx.x; grp < ngroups; grp = s_next, buf = P::DB ? buf ^ 1 : 0) {
     const int e0 = M.e_lo + grp * P::E, ne = min(P::E, M.n_owned - e0);
     const bool active = line_ok && el < ne;
     const int e = e0 + el;
@@ -671,6 +680,7 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, (N1 <= 8 ? 3 : 1))
     if (tid == 0) {
       fence_proxy_async();
       hl_issue_node<N1, VISC>(sm, M, A, grp, bar_node);
+      s_next = next_group(A.gctr, grp);  // read by all threads after the next barrier
     }
 
     // ---- own half -> registers, gathers for the own endpoint
@@ -724,7 +734,8 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, (N1 <= 8 ? 3 : 1))
     }
     cp_async_commit();
     if constexpr (P::DB) {  // next group's line data into the other buffer, now
-      const int gn = grp + gridDim.x;
+      __syncthreads();
+      const int gn = s_next;
       if (gn < ngroups) hl_prefetch_line<N1, VISC>(sm, M, A.in, A, gn, tid, buf ^ 1);
       cp_async_commit();
     }
@@ -826,7 +837,7 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, (N1 <= 8 ? 3 : 1))
       }
     }
     if constexpr (!P::DB) {  // single buffer: prefetch behind the rest of this group
-      const int gn = grp + gridDim.x;
+      const int gn = s_next;
       if (gn < ngroups) hl_prefetch_line<N1, VISC>(sm, M, A.in, A, gn, tid, 0);
       cp_async_commit();
     }
@@ -1572,12 +1583,13 @@ static void launch_n(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
       return;
     }
   }
-  // inviscid kernel choice: element-per-thread (N+1 <= 3), full-line (N+1 = 4),
-  // half-line (N+1 >= 5); SWDG_FAST_VARIANT=elem/full/half overrides where the
-  // variant exists for this degree
-  // measured on B200 (1M elements): full-line wins where the half split is
-  // unbalanced (odd N+1: 5, 7), half-line at even N+1 >= 6
-  int v = N1 <= 3 ? 3 : ((N1 == 4 || N1 == 5 || N1 == 7) ? 1 : 2);
+  // inviscid kernel choice: element-per-thread (N+1 <= 3), full-line (N+1 = 4,
+  // 5), half-line (N+1 >= 6); SWDG_FAST_VARIANT=elem/full/half/pl overrides where
+  // the variant exists for this degree
+  // measured on B200 (1M elements, profiles/r01_sweep_variants.txt): full-line
+  // at N+1 = 4, 5; half-line from N+1 = 6 on (odd row stride: no bank conflicts
+  // at odd N+1 either)
+  int v = N1 <= 3 ? 3 : ((N1 == 4 || N1 == 5) ? 1 : 2);
   const int ov = variant_override();
   if (ov == 3 && N1 <= 3) v = 3;
   if (ov == 1 && N1 <= 8) v = 1;

@@ -69,6 +69,7 @@ struct swdg_gpu {
   double *fh = nullptr, *fhu = nullptr, *fhv = nullptr;
   double *partial = nullptr, *sums = nullptr;
   int int_lo = 0, int_hi = 0;   // interior element range (halo overlap), empty by default
+  int* gctr = nullptr;          // device group counter of the persistent stage kernels
   Flags* flags = nullptr;       // device, 3 (one per stage)
   Flags* flags_init = nullptr;  // device, reset image
   Flags* flags_h = nullptr;     // pinned host mirror, 3
@@ -231,6 +232,8 @@ void stage_main(swdg_gpu* c, CState in, double* const* out, int k, double t, dou
   }
   if (c->fast) {
     const Mesh& M = range ? *range : c->M;
+    ck(cudaMemsetAsync(c->gctr, 0, sizeof(int), c->stream), "group counter");
+    a.gctr = c->gctr;
     if (M.n_owned > M.e_lo) c->launches += launch_fast_stage(M, c->phys, a, F, c->stream);
   } else {
     c->launches += launch_exact_rhs_stage(c->M, c->phys, a, c->stream);
@@ -379,6 +382,7 @@ void allocate(swdg_gpu* c, int K, int n_owned, int N, const std::vector<int4>& e
   c->partial = c->dalloc<double>(2 * (size_t)K);
   c->sums = c->dalloc<double>(2);
   c->flags = c->dalloc<Flags>(3);
+  c->gctr = c->dalloc<int>(1);
   c->flags_init = c->dalloc<Flags>(3);
   ck(cudaMallocHost(&c->flags_h, 3 * sizeof(Flags)), "pinned flags");
   ck(cudaMallocHost(&c->sums_h, 2 * sizeof(double)), "pinned sums");
