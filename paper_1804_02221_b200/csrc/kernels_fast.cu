@@ -485,7 +485,7 @@ struct HL {
   static constexpr int LBUF = kLineFields * GPAD;
   static constexpr int rest() {
     return 3 * GPAD + LP * XS + kNodeFields * GNP + E * 4 * N1 * kTr + 2 * E * 4 * 2 +
-           2 * 32 * WR * 6 + 2;
+           2 * E * 2 * 5 + 2;
   }
   static constexpr int kCtas = THREADS > 128 ? 1 : (N1 <= 8 ? 3 : 2);  // register-bound residency
   static constexpr bool DB = false && (size_t)(2 * LBUF + rest()) * 8 * kCtas + kCtas * 1024 <= 227 * 1024;
@@ -496,8 +496,8 @@ struct HL {
   static constexpr int NODE = XCH + LP * XS;
   static constexpr int TR = NODE + kNodeFields * GNP;  // [kTr][E][4][N1]
   static constexpr int EFO = TR + E * 4 * N1 * kTr;     // int4 [NBUF][E][4]
-  static constexpr int RED = EFO + 2 * E * 4 * 2;      // [2][32 WR xi lines][6]
-  static constexpr int BAR = RED + 2 * 32 * WR * 6;
+  static constexpr int RED = EFO + 2 * E * 4 * 2;      // [2 parts][E][2 pieces][5]
+  static constexpr int BAR = RED + 2 * E * 2 * 5;
   static constexpr int TOTAL = BAR + 2;
   static constexpr size_t bytes = TOTAL * sizeof(double);
 };
@@ -930,7 +930,7 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, (N1 <= 8 ? 3 : 1))
     ph_node ^= 1;
 
     // ---- node phase on the xi-line threads: nodes (k, li), k in the own half
-    double* red = sm + P::RED + (part * 32 * P::WR + lr) * 6;  // xi threads only
+    double pv[5] = {0.0, 0.0, 0.0, 0.0, 1.0e300};  // element partials of this thread
     if (xi && active) {
       const double* acc = sm + P::ACC + el * P::EPAD;
       const double* Nd = sm + P::NODE + el * NP;
@@ -974,77 +974,100 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, (N1 <= 8 ? 3 : 1))
         s2 += wq * shv;
         mmin = smin(mmin, sh);
       }
-      red[0] = s_area;
-      red[1] = s0;
-      red[2] = s1;
-      red[3] = s2;
-      red[4] = mmin;
+      pv[0] = s_area;
+      pv[1] = s0;
+      pv[2] = s1;
+      pv[3] = s2;
+      pv[4] = mmin;
+    }
+    // element partial sums: segmented shuffle reduction over the xi lanes of each
+    // element inside the warp (fixed tree: reproducible), one piece per (warp,
+    // element) to shared memory; an element whose lines straddle two warps of
+    // its role has two pieces
+    if (xi) {
+      const int seg = line_ok ? lr / N1 : -1 - lane;  // element of this lane
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int seg2 = __shfl_down_sync(0xffffffffu, seg, o);
+        double t[5];
+#pragma unroll
+        for (int c = 0; c < 5; ++c) t[c] = __shfl_down_sync(0xffffffffu, pv[c], o);
+        if (lane + o < 32 && seg2 == seg) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) pv[c] += t[c];
+          pv[4] = smin(pv[4], t[4]);
+        }
+      }
+      const bool head = line_ok && (lane == 0 || li == 0);
+      if (head && active) {
+        double* rr = sm + P::RED + ((part * P::E + el) * 2 + (li == 0 ? 0 : 1)) * 5;
+#pragma unroll
+        for (int c = 0; c < 5; ++c) rr[c] = pv[c];
+      }
     }
     __syncthreads();
 
-    // ---- limiter (limit_element, limiter.hpp:43-84) and write-out
-    bool lim = active && A.update;
-    double area = 0.0, a0 = 0.0, a1 = 0.0, a2 = 0.0, mmin = 1.0e300;
+    // ---- limiter (limit_element, limiter.hpp:43-84) and write-out, xi threads
+    bool lim = xi && active && A.update;
     if (lim) {
+      // pieces in a fixed order: part X (first piece, continuation), part Y
+      const bool split = (el * N1) / 32 != (el * N1 + N1 - 1) / 32;
+      double area = 0.0, a0 = 0.0, a1 = 0.0, a2 = 0.0, mmin = 1.0e300;
 #pragma unroll
       for (int pp = 0; pp < 2; ++pp)
 #pragma unroll
-        for (int l = 0; l < N1; ++l) {
-          const double* rr = sm + P::RED + (pp * 32 * P::WR + el * N1 + l) * 6;
+        for (int pc = 0; pc < 2; ++pc) {
+          if (pc == 1 && !split) continue;
+          const double* rr = sm + P::RED + ((pp * P::E + el) * 2 + pc) * 5;
           area += rr[0];
           a0 += rr[1];
           a1 += rr[2];
           a2 += rr[3];
           mmin = smin(mmin, rr[4]);
         }
-    }
-    const double inv = 1.0 / area;
-    const double avg0 = inv * a0, avg1 = inv * a1, avg2 = inv * a2;
-    const bool lead = role == 0 && li == 0;  // one thread per element
-    if (lim && avg0 < 0.0) {
-      if (lead) {
-        atomicExch(&F->reject, 1);
-        if (!Ph.limiter) atomicExch(&F->abort, 1);
+      const double inv = 1.0 / area;
+      const double avg0 = inv * a0, avg1 = inv * a1, avg2 = inv * a2;
+      const bool lead = part == 0 && li == 0;  // one thread per element
+      if (avg0 < 0.0) {  // reject (timeloop.hpp:205-209): nothing written
+        if (lead) {
+          atomicExch(&F->reject, 1);
+          if (!Ph.limiter) atomicExch(&F->abort, 1);
+        }
+        lim = false;
       }
-      lim = false;
-    }
-    double theta = 1.0;
-    if (lim && Ph.limiter && mmin < 0.0) {
-      const double denom = avg0 - mmin;
-      theta = denom < 1e-14 ? 1.0 : smin(1.0, avg0 / denom);
-    }
-    if (lim && !Ph.limiter && mmin < 0.0 && lead) atomicExch(&F->abort, 1);
-    double mine = 1.0e300;
-    if (lim && xi) {
+      double theta = 1.0;
+      if (lim && Ph.limiter && mmin < 0.0) {
+        const double denom = avg0 - mmin;
+        theta = denom < 1e-14 ? 1.0 : smin(1.0, avg0 / denom);
+      }
+      if (lim && !Ph.limiter && mmin < 0.0 && lead) atomicExch(&F->abort, 1);
+      if (lim) {
 #pragma unroll
-      for (int s = 0; s < S; ++s) {
-        if (s >= nk) continue;
-        const long long n = (long long)e * NP + (k0 + s) * N1 + li;
-        double sh = h[s], shu = hu[s], shv = hv[s];
-        if (theta < 1.0) {
-          sh = smax(theta * (sh - avg0) + avg0, 0.0);
-          shu = theta * (shu - avg1) + avg1;
-          shv = theta * (shv - avg2) + avg2;
+        for (int s = 0; s < S; ++s) {
+          if (s >= nk) continue;
+          const long long n = (long long)e * NP + (k0 + s) * N1 + li;
+          double sh = h[s], shu = hu[s], shv = hv[s];
+          if (theta < 1.0) {
+            sh = smax(theta * (sh - avg0) + avg0, 0.0);
+            shu = theta * (shu - avg1) + avg1;
+            shv = theta * (shv - avg2) + avg2;
+          }
+          if (Ph.limiter && sh < Ph.h_tol) {
+            shu = 0.0;
+            shv = 0.0;
+          }
+          A.out.h[n] = sh;
+          A.out.hu[n] = shu;
+          A.out.hv[n] = shv;
         }
-        if (Ph.limiter && sh < Ph.h_tol) {
-          shu = 0.0;
-          shv = 0.0;
+        if (lead) {
+          // the limited heights are a monotone map of the unlimited ones: the
+          // element's minimum after limiting is the map of its minimum
+          const double m = theta < 1.0 ? smax(theta * (mmin - avg0) + avg0, 0.0) : mmin;
+          atomicMin(&F->min_h_key, order_key(m));
+          if (theta < 1.0) atomicAdd(&F->n_limited, 1);
         }
-        A.out.h[n] = sh;
-        A.out.hu[n] = shu;
-        A.out.hv[n] = shv;
-        mine = smin(mine, sh);
       }
-    }
-    if (xi) red[5] = mine;
-    __syncthreads();
-    if (lim && lead) {
-      double m = 1.0e300;
-      for (int pp = 0; pp < 2; ++pp)
-        for (int l = 0; l < N1; ++l)
-          m = smin(m, sm[P::RED + (pp * 32 * P::WR + el * N1 + l) * 6 + 5]);
-      atomicMin(&F->min_h_key, order_key(m));
-      if (theta < 1.0) atomicAdd(&F->n_limited, 1);
     }
   }
   cp_async_wait_all();
