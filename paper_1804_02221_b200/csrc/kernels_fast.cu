@@ -65,8 +65,8 @@ struct Plan {
   static constexpr int ACC = NODE + kNodeFields * GNP;
   static constexpr int TR = ACC + 3 * GNP;         // [E][4][N1][8] neighbour traces
   static constexpr int EFO = TR + E * 4 * N1 * 8;  // int4 [E][4] = 2 doubles each
-  static constexpr int RED = EFO + E * 4 * 2;      // [E][T][6]
-  static constexpr int BAR = RED + E * T * 6;      // 2 mbarriers
+  static constexpr int RED = EFO + E * 4 * 2;      // [E][N1 eta lines][5]
+  static constexpr int BAR = RED + E * N1 * 5;     // 2 mbarriers
   static constexpr int TOTAL = BAR + 2;
   static constexpr size_t bytes = TOTAL * sizeof(double);
 };
@@ -302,8 +302,8 @@ __global__ void __launch_bounds__(Plan<N1>::THREADS, 1)
     ph_node ^= 1;
 
     // ---- node phase on the eta-line threads: node (li, k), k = 0..N
-    double* red = sm + P::RED + (el * T + lt) * 6;
     const double* Nd = sm + P::NODE + el * NP;
+    double pv[5] = {0.0, 0.0, 0.0, 0.0, 1.0e300};  // element partials of this thread
     if (!xi && active) {
       double s_area = 0.0, s0 = 0.0, s1 = 0.0, s2 = 0.0, mmin = 1.0e300;
       const double wi = O::w(li);
@@ -344,71 +344,74 @@ __global__ void __launch_bounds__(Plan<N1>::THREADS, 1)
         s2 += wj * shv;
         mmin = smin(mmin, sh);
       }
-      red[0] = s_area;
-      red[1] = s0;
-      red[2] = s1;
-      red[3] = s2;
-      red[4] = mmin;
+      pv[0] = s_area;
+      pv[1] = s0;
+      pv[2] = s1;
+      pv[3] = s2;
+      pv[4] = mmin;
+    }
+    // element partials: one slot per eta line, summed below in line order by the
+    // eta threads (the order the trajectory tests were pinned with)
+    if (!xi && active) {
+      double* rr = sm + P::RED + (el * N1 + li) * 5;
+#pragma unroll
+      for (int c = 0; c < 5; ++c) rr[c] = pv[c];
     }
     __syncthreads();
 
-    // ---- limiter (limit_element, limiter.hpp:43-84) and write-out
-    bool lim = active && A.update;
-    double area = 0.0, a0 = 0.0, a1 = 0.0, a2 = 0.0, mmin = 1.0e300;
-    const double* red0 = sm + P::RED + el * T * 6;
+    // ---- limiter (limit_element, limiter.hpp:43-84) and write-out, eta threads
+    bool lim = !xi && active && A.update;
     if (lim) {
+      double area = 0.0, a0 = 0.0, a1 = 0.0, a2 = 0.0, mmin = 1.0e300;
 #pragma unroll
-      for (int q = N1; q < T; ++q) {
-        area += red0[q * 6 + 0];
-        a0 += red0[q * 6 + 1];
-        a1 += red0[q * 6 + 2];
-        a2 += red0[q * 6 + 3];
-        mmin = smin(mmin, red0[q * 6 + 4]);
+      for (int l = 0; l < N1; ++l) {
+        const double* rr = sm + P::RED + (el * N1 + l) * 5;
+        area += rr[0];
+        a0 += rr[1];
+        a1 += rr[2];
+        a2 += rr[3];
+        mmin = smin(mmin, rr[4]);
       }
-    }
-    const double inv = 1.0 / area;
-    const double avg0 = inv * a0, avg1 = inv * a1, avg2 = inv * a2;
-    if (lim && avg0 < 0.0) {
-      if (lt == 0) {
-        atomicExch(&F->reject, 1);
-        if (!Ph.limiter) atomicExch(&F->abort, 1);
+      const double inv = 1.0 / area;
+      const double avg0 = inv * a0, avg1 = inv * a1, avg2 = inv * a2;
+      const bool lead = lt == N1;
+      if (avg0 < 0.0) {
+        if (lead) {
+          atomicExch(&F->reject, 1);
+          if (!Ph.limiter) atomicExch(&F->abort, 1);
+        }
+        lim = false;
       }
-      lim = false;
-    }
-    double theta = 1.0;
-    if (lim && Ph.limiter && mmin < 0.0) {
-      const double denom = avg0 - mmin;
-      theta = denom < 1e-14 ? 1.0 : smin(1.0, avg0 / denom);
-    }
-    if (lim && !Ph.limiter && mmin < 0.0 && lt == 0) atomicExch(&F->abort, 1);
-    double mine = 1.0e300;
-    if (lim && !xi) {
-      const long long nb0 = (long long)e * NP + li * N1;
+      double theta = 1.0;
+      if (lim && Ph.limiter && mmin < 0.0) {
+        const double denom = avg0 - mmin;
+        theta = denom < 1e-14 ? 1.0 : smin(1.0, avg0 / denom);
+      }
+      if (lim && !Ph.limiter && mmin < 0.0 && lead) atomicExch(&F->abort, 1);
+      if (lim) {
+        const long long nb0 = (long long)e * NP + li * N1;
 #pragma unroll
-      for (int k = 0; k < N1; ++k) {
-        double sh = h[k], shu = hu[k], shv = hv[k];
-        if (theta < 1.0) {
-          sh = smax(theta * (sh - avg0) + avg0, 0.0);
-          shu = theta * (shu - avg1) + avg1;
-          shv = theta * (shv - avg2) + avg2;
+        for (int k = 0; k < N1; ++k) {
+          double sh = h[k], shu = hu[k], shv = hv[k];
+          if (theta < 1.0) {
+            sh = smax(theta * (sh - avg0) + avg0, 0.0);
+            shu = theta * (shu - avg1) + avg1;
+            shv = theta * (shv - avg2) + avg2;
+          }
+          if (Ph.limiter && sh < Ph.h_tol) {
+            shu = 0.0;
+            shv = 0.0;
+          }
+          A.out.h[nb0 + k] = sh;
+          A.out.hu[nb0 + k] = shu;
+          A.out.hv[nb0 + k] = shv;
         }
-        if (Ph.limiter && sh < Ph.h_tol) {
-          shu = 0.0;
-          shv = 0.0;
+        if (lead) {  // minimum after limiting: the monotone map of the minimum
+          const double m = theta < 1.0 ? smax(theta * (mmin - avg0) + avg0, 0.0) : mmin;
+          atomicMin(&F->min_h_key, order_key(m));
+          if (theta < 1.0) atomicAdd(&F->n_limited, 1);
         }
-        A.out.h[nb0 + k] = sh;
-        A.out.hu[nb0 + k] = shu;
-        A.out.hv[nb0 + k] = shv;
-        mine = smin(mine, sh);
       }
-    }
-    red[5] = mine;
-    __syncthreads();
-    if (lim && lt == 0) {
-      double m = red0[N1 * 6 + 5];
-      for (int q = N1 + 1; q < T; ++q) m = smin(m, red0[q * 6 + 5]);
-      atomicMin(&F->min_h_key, order_key(m));
-      if (theta < 1.0) atomicAdd(&F->n_limited, 1);
     }
   }
 }
@@ -635,7 +638,10 @@ __device__ __forceinline__ void hl_visc_div(const double* Lb, int li, bool xi,
 }
 
 template <int N1, bool FORCE, bool VISC>
-__global__ void __launch_bounds__(HL<N1, VISC>::THREADS, (N1 <= 8 ? 3 : 1))
+// resident CTAs the register allocation must allow: 3 (<= 168 registers) where
+// that costs no spills (N+1 <= 8 and N+1 = 10: measured 22% faster at N+1 = 10);
+// above, a 168-register cap spills (N+1 = 11, 13..16) and runs slower
+__global__ void __launch_bounds__(HL<N1, VISC>::THREADS, (N1 <= 8 || N1 == 10 ? 3 : 1))
     k_stage_hl(Mesh M, Phys Ph, StageArgs A, Flags* F) {
   using P = HL<N1, VISC>;
   using O = Ops<N1>;
