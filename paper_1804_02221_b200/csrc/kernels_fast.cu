@@ -454,10 +454,13 @@ struct HL {
   static constexpr int lanes_used(int e) { return e * N1; }
   static constexpr int warps_for(int e) { return (e * N1 + 31) / 32; }
   static constexpr int pick_e() {
+    // one warp per role while that fills >= 80% of the lanes (N+1 <= 10), else up
+    // to two; odd E works for odd N+1 (the node-field bulk copies shift by one)
     int best = 2, bu = 0;
+    const int wmax = 32 / N1 * N1 * 10 >= 32 * 8 ? 1 : 2;
     for (int e = 2; e <= 32; ++e) {
-      if ((N1 & 1) && (e & 1)) continue;
-      if (warps_for(e) > 2) break;
+      if (N1 > 10 && (N1 & 1) && (e & 1)) continue;  // measured configurations kept
+      if (warps_for(e) > wmax) break;
       const int u = 1000 * lanes_used(e) / (32 * warps_for(e));
       if (u > bu) {
         bu = u;
@@ -474,7 +477,7 @@ struct HL {
   static constexpr int PAD = N1 | 1;       // odd padded row stride: conflict-free rows and columns
   static constexpr int EPAD = N1 * PAD;    // one padded element field
   static constexpr int GPAD = E * EPAD;
-  static constexpr int GNP = (E * NP + 1) & ~1;
+  static constexpr int GNP = (E * NP + 3) & ~1;  // node field stride (+ shift slack)
   // line fields; the viscous variant adds the physical viscous flux pairs
   enum { F_H, F_HU, F_HV, F_YE, F_XE, F_YX, F_XX, F_FVU, F_GVU, F_FVV, F_GVV };
   static constexpr int kLineFields = V ? 11 : 7;
@@ -591,10 +594,13 @@ __device__ __forceinline__ void hl_issue_node(double* sm, const Mesh& M, const S
                                               int g, uint64_t* bar) {
   using P = HL<N1, V>;
   const int e0 = M.e_lo + g * P::E, ne = min(P::E, M.n_owned - e0);
-  const uint32_t fb = round16((size_t)ne * P::NP * sizeof(double));
+  // bulk copies need 16-byte aligned sources: an odd first node is copied from
+  // one double earlier and the group's data starts at offset (e0 * NP) & 1
+  const int shift = (int)(((long long)e0 * P::NP) & 1);
+  const uint32_t fb = round16((size_t)(ne * P::NP + shift) * sizeof(double));
   const bool wn = A.update && A.stage > 0;
   mbar_expect_tx(bar, (wn ? 6 : 3) * fb);
-  const long long off = (long long)e0 * P::NP;
+  const long long off = (long long)e0 * P::NP - shift;
   bulk_g2s(sm + P::NODE + P::N_JAC * P::GNP, M.jac + off, fb, bar);
   bulk_g2s(sm + P::NODE + P::N_SX * P::GNP, M.sx + off, fb, bar);
   bulk_g2s(sm + P::NODE + P::N_SY * P::GNP, M.sy + off, fb, bar);
@@ -639,9 +645,9 @@ __device__ __forceinline__ void hl_visc_div(const double* Lb, int li, bool xi,
 
 template <int N1, bool FORCE, bool VISC>
 // resident CTAs the register allocation must allow: 3 (<= 168 registers) where
-// that costs no spills (N+1 <= 8 and N+1 = 10: measured 22% faster at N+1 = 10);
+// that costs no spills (N+1 <= 10: measured 22% faster at N+1 = 10);
 // above, a 168-register cap spills (N+1 = 11, 13..16) and runs slower
-__global__ void __launch_bounds__(HL<N1, VISC>::THREADS, (N1 <= 8 || N1 == 10 ? 3 : 1))
+__global__ void __launch_bounds__(HL<N1, VISC>::THREADS, (N1 <= 10 ? 3 : 1))
     k_stage_hl(Mesh M, Phys Ph, StageArgs A, Flags* F) {
   using P = HL<N1, VISC>;
   using O = Ops<N1>;
@@ -939,7 +945,7 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, (N1 <= 8 || N1 == 10 ? 
     double pv[5] = {0.0, 0.0, 0.0, 0.0, 1.0e300};  // element partials of this thread
     if (xi && active) {
       const double* acc = sm + P::ACC + el * P::EPAD;
-      const double* Nd = sm + P::NODE + el * NP;
+      const double* Nd = sm + P::NODE + (int)(((long long)e0 * NP) & 1) + el * NP;
       double s_area = 0.0, s0 = 0.0, s1 = 0.0, s2 = 0.0, mmin = 1.0e300;
       const double wj = O::w(li);
 #pragma unroll
