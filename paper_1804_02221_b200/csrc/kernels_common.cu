@@ -33,8 +33,8 @@ __global__ void k_elem_sums(Mesh M, Phys P, CState S, double* partial, Flags* F)
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long key = ~0ull;
   if (e < M.n_owned) key = order_key(elem_sums(M, P, S, partial, e));
-  key = warp_min_key(key);
-  if ((threadIdx.x & 31) == 0) atomicMin(&F->min_h_key, key);
+  key = block_min_key(key);
+  if (threadIdx.x == 0) atomicMin(&F->min_h_key, key);
 }
 
 __device__ __forceinline__ double elem_sums(const Mesh& M, const Phys& P, const CState& S,
@@ -90,11 +90,15 @@ __device__ __forceinline__ double posdt_bound(const Mesh& M, const Phys& P, cons
                                                long long idx);
 
 __global__ void k_posdt(Mesh M, Phys P, CState S, Flags* F) {
-  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   unsigned long long key = ~0ull;
-  if (idx < (long long)M.n_owned * 4 * M.n1) key = order_key(posdt_bound(M, P, S, idx));
-  key = warp_min_key(key);  // one atomic per warp
-  if ((threadIdx.x & 31) == 0) atomicMin(&F->posdt_key, key);
+  const long long nf = (long long)M.n_owned * 4 * M.n1;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < nf;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long k = order_key(posdt_bound(M, P, S, idx));
+    key = k < key ? k : key;
+  }
+  key = block_min_key(key);  // one atomic per block
+  if (threadIdx.x == 0) atomicMin(&F->posdt_key, key);
 }
 
 __device__ __forceinline__ double posdt_bound(const Mesh& M, const Phys& P, const CState& S,
@@ -185,7 +189,8 @@ int launch_diagnostics(const Mesh& M, const Phys& P, CState S, double* partial, 
   k_elem_sums<<<(M.n_owned + 127) / 128, 128, 0, st>>>(M, P, S, partial, F);
   k_sum_partials<<<1, 1024, 0, st>>>(partial, M.n_owned, out2);
   const long long nf = (long long)M.n_owned * 4 * M.n1;
-  k_posdt<<<(unsigned)((nf + 255) / 256), 256, 0, st>>>(M, P, S, F);
+  const long long pb = (nf + 255) / 256;
+  k_posdt<<<(unsigned)(pb < 148 * 16 ? pb : 148 * 16), 256, 0, st>>>(M, P, S, F);
   return 3;
 }
 

@@ -513,10 +513,11 @@ __global__ void k_limit(Mesh M, Phys P, State S, Flags* F) {
 // compute_dt (timeloop.hpp:53-75): per-node candidates, min via ordered keys;
 // the lengths 2J/hypot(.) come precomputed by the host with std::hypot.
 __global__ void k_dt(Mesh M, Phys P, CState S, Flags* F) {
-  const long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   unsigned long long kdt = ~0ull, klen = ~0ull;
-  if (n < (long long)M.n_owned * M.np) {
-    const double order = 2.0 * M.degree + 1.0;
+  const long long nn = (long long)M.n_owned * M.np;
+  const double order = 2.0 * M.degree + 1.0;
+  for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < nn;
+       n += (long long)gridDim.x * blockDim.x) {
     double u, v;
     velocity(S.h[n], S.hu[n], S.hv[n], P.h_des, u, v);
     const double c = sqrt(P.g * smax(S.h[n], 0.0));
@@ -525,13 +526,14 @@ __global__ void k_dt(Mesh M, Phys P, CState S, Flags* F) {
     const double lx = fabs(u) + c, ly = fabs(v) + c;
     if (lx > 1e-14) dt = smin(dt, lxi / (order * lx));
     if (ly > 1e-14) dt = smin(dt, leta / (order * ly));
-    kdt = order_key(dt);
-    klen = order_key(smin(lxi, leta));
+    const unsigned long long a = order_key(dt), b = order_key(smin(lxi, leta));
+    kdt = a < kdt ? a : kdt;
+    klen = b < klen ? b : klen;
   }
-  // min is exact: reduce per warp, one atomic per warp
-  kdt = warp_min_key(kdt);
-  klen = warp_min_key(klen);
-  if ((threadIdx.x & 31) == 0) {
+  // min is exact (order-independent): one atomic per block
+  kdt = block_min_key(kdt);
+  klen = block_min_key(klen);
+  if (threadIdx.x == 0) {
     atomicMin(&F->dt_key, kdt);
     atomicMin(&F->minlen_key, klen);
   }
@@ -571,7 +573,8 @@ int launch_exact_limit(const Mesh& M, const Phys& P, State S, Flags* F, cudaStre
 
 int launch_exact_dt(const Mesh& M, const Phys& P, CState S, Flags* F, cudaStream_t st) {
   const long long nn = (long long)M.n_owned * M.np;
-  k_dt<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(M, P, S, F);
+  const long long blocks = (nn + 255) / 256;
+  k_dt<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, st>>>(M, P, S, F);
   return 1;
 }
 

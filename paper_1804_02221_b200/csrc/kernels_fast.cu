@@ -108,7 +108,10 @@ __device__ __forceinline__ void issue_node(double* sm, const Mesh& M, const Stag
 }
 
 template <int N1, bool FORCE>
-__global__ void __launch_bounds__(Plan<N1>::THREADS, 1)
+#ifndef FULL_MINB
+#define FULL_MINB 1
+#endif
+__global__ void __launch_bounds__(Plan<N1>::THREADS, FULL_MINB)
     k_stage(Mesh M, Phys Ph, StageArgs A, Flags* F) {
   using P = Plan<N1>;
   using O = Ops<N1>;
@@ -455,11 +458,11 @@ struct HL {
   static constexpr int warps_for(int e) { return (e * N1 + 31) / 32; }
   static constexpr int pick_e() {
     // one warp per role while that fills >= 80% of the lanes (N+1 <= 10), else up
-    // to two; odd E works for odd N+1 (the node-field bulk copies shift by one)
+    // to two; odd E works for odd N+1 (the node-field bulk copies shift by one):
+    // N+1 = 11 takes E = 5 (86% of 64 lanes), measured 8.6 -> 7.0 ms/stage
     int best = 2, bu = 0;
     const int wmax = 32 / N1 * N1 * 10 >= 32 * 8 ? 1 : 2;
     for (int e = 2; e <= 32; ++e) {
-      if (N1 > 10 && (N1 & 1) && (e & 1)) continue;  // measured configurations kept
       if (warps_for(e) > wmax) break;
       const int u = 1000 * lanes_used(e) / (32 * warps_for(e));
       if (u > bu) {
@@ -1307,7 +1310,10 @@ __device__ __forceinline__ void st_elem(double* __restrict__ p, long long base,
 }
 
 template <int N1, bool FORCE>
-__global__ void __launch_bounds__(128) k_stage_elem(Mesh M, Phys Ph, StageArgs A, Flags* F) {
+#ifndef ELEM_MINB
+#define ELEM_MINB 1
+#endif
+__global__ void __launch_bounds__(128, ELEM_MINB) k_stage_elem(Mesh M, Phys Ph, StageArgs A, Flags* F) {
   using O = Ops<N1>;
   constexpr int NP = N1 * N1;
   const int e = M.e_lo + blockIdx.x * blockDim.x + threadIdx.x;
