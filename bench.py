@@ -10,7 +10,10 @@ step = 3 RK stages; value = 3 * DOFs * steps / time, DOFs = 3 K (N+1)^2
 (bench.hpp:259).  Inputs (>= 5 GB of geometry+state) exceed the 126 MB L2, so no
 flush is needed between iterations.
 
-  python bench.py [--gpus N --steps K --warmup W] [--degree N] [--sweep]
+  python bench.py [--gpus N --steps K --warmup W] [--degree N] [--no-sweep] [--viscous]
+
+On one GPU the line also carries the N=1..15 sweep (the BASELINE metric is "vs
+N=1..15"): per degree the DOF-updates/s, the frozen roofline and its fraction.
   python bench.py --impl reference ...   # the reference CPU solver, same config
 """
 from __future__ import annotations
@@ -315,7 +318,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--degree", type=int, default=7)
     ap.add_argument("--viscous", action="store_true")
-    ap.add_argument("--sweep", action="store_true", help="also time N=1..15 (single GPU)")
+    ap.add_argument("--no-sweep", dest="sweep", action="store_false",
+                    help="skip the N=1..15 sweep (single GPU)")
     ap.add_argument("--distributed", action="store_true",
                     help="use the partitioned (NCCL halo) path even on one GPU")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
@@ -416,17 +420,22 @@ def main():
                       f"same mesh family, {cb['steps']} steps in {cb['seconds']:.1f} s, "
                       f"{cpu_model()}"}
         if args.sweep and not distributed:
-            sweep = {}
+            sweep, roof, frac = {}, {}, {}
             for n in range(1, 16):
-                if n == N:
-                    sweep[n] = value
-                    continue
                 if args.viscous and n < 2:
                     continue
-                ks = max(3, args.steps // 4)
-                rr = measure_gpu(n, ks, 3, args.viscous, rank, 1, e2e_steps=0)
-                sweep[n] = rr["dofs"] / (rr["ms"] * 1e-3 / (3 * ks))
+                if n == N:
+                    v = value
+                else:
+                    ks = max(3, args.steps // 4)
+                    rr = measure_gpu(n, ks, 3, args.viscous, rank, 1, e2e_steps=0)
+                    v = rr["dofs"] / (rr["ms"] * 1e-3 / (3 * ks))
+                bn, fn = frozen_counts(n, args.viscous)
+                rf = min(pk["hbm_gbs"] * 1e9 / (bn / 3.0), pk["fp64_tflops"] * 1e12 / (fn / 3.0))
+                sweep[n], roof[n], frac[n] = v, rf, v / rf
             out["sweep_dof_per_s_by_degree"] = sweep
+            out["sweep_roof_dof_per_s_by_degree"] = roof
+            out["sweep_frac_of_roof_by_degree"] = frac
         print(json.dumps(out), flush=True)
     if distributed:
         torch.distributed.destroy_process_group()

@@ -1089,44 +1089,70 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, (N1 <= 10 ? 3 : 1))
 }
 
 // ===========================================================================
-// Viscous pre-kernel (fast): per element the modal shock indicator and the
-// viscosity coefficient (viscosity.hpp:35-78, finished on the device with
-// CUDA log10/sin), the BR1 lifted velocity gradients (viscosity.hpp:95-168)
-// and the physical viscous flux pairs h eps grad (viscosity.hpp:187-194),
-// written per node for the stage kernel (its strong divergence and the
-// interface penalties).  One thread per node, E elements per CTA, element
-// data staged in shared memory.
 template <int N1>
 struct VP {
   static constexpr int NP = N1 * N1;
   static constexpr int E = (256 / NP) > 1 ? (256 / NP) : 1;
   static constexpr int THREADS = E * NP;
-  enum { H, U, V, YE, XE, YX, XX, TMP, C0, C1, C2, C3, kF };
-  static constexpr int RED = kF * E * NP;  // [E][4] shell sums
-  static constexpr int EPS = RED + E * 4;
+  static constexpr int OPAD = N1 + 1;  // operator row stride (conflict-free)
+  static constexpr int PMAX = (NP + 31) / 32 + 1;  // warp pieces of one element
+  enum { H, U, V, YE, XE, YX, XX, TMP, kF };
+  static constexpr int OPV = kF * E * NP;        // V^-1 [N1][OPAD]
+  static constexpr int OPD = OPV + N1 * OPAD;    // D-hat [N1][OPAD]
+  static constexpr int RED = OPD + N1 * OPAD;    // [E][PMAX][4] shell-sum pieces
+  static constexpr int EPS = RED + E * PMAX * 4;
   static constexpr int TOTAL = EPS + E;
   static constexpr size_t bytes = TOTAL * sizeof(double);
 };
 
+// Viscous pre-kernel (fast): per element the modal shock indicator and the
+// viscosity coefficient (viscosity.hpp:35-78, finished on the device with CUDA
+// log10/sin), the BR1 lifted velocity gradients (viscosity.hpp:95-168) and the
+// physical viscous flux pairs h eps grad (viscosity.hpp:187-194).  One thread
+// per node.  The operators sit in shared memory (per-thread indices: constant
+// memory would serialise), the neighbour traces for the BR1 face corrections
+// are requested first and consumed last, and the four shell energies are
+// summed by a segmented warp-shuffle reduction (fixed tree: reproducible).
 template <int N1>
 __global__ void __launch_bounds__(VP<N1>::THREADS)
     k_visc_pre(Mesh M, Phys Ph, CState S, double* eps_out, double* fvu, double* fvv,
                double* gvu, double* gvv, Flags* F) {
   using P = VP<N1>;
   using O = Ops<N1>;
-  constexpr int NP = P::NP, N = N1 - 1;
+  constexpr int NP = P::NP, N = N1 - 1, OP = P::OPAD;
   extern __shared__ __align__(16) double sm[];
-  const int el = threadIdx.x / NP, q = threadIdx.x % NP, i = q / N1, j = q % N1;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int el = tid / NP, q = tid % NP, i = q / N1, j = q % N1;
   const int e = blockIdx.x * P::E + el;
   const bool active = e < M.n_owned;
   const long long n = (long long)e * NP + q;
   double* f = sm + el * NP;
   auto fld = [&](int k) { return f + k * P::E * NP; };
-  double h = 0.0, hu = 0.0, hv = 0.0;
+  // neighbour traces of this node's faces (<= 2), requested before anything else
+  int fa[2] = {0, 0}, ta[2] = {0, 0}, fy[2] = {0, 0};
+  double nh[2] = {0.0, 0.0}, nhu[2] = {0.0, 0.0}, nhv[2] = {0.0, 0.0};
+  int nfc = 0;
+  if (active) {
+    nfc = node_faces(N1, i, j, fa, ta);
+    for (int c2 = 0; c2 < nfc; ++c2) {
+      const int4 ef = M.ef[e * 4 + fa[c2]];
+      fy[c2] = ef.y;
+      if ((ef.y & EF_PRESENT) && !(ef.y & EF_WALL)) {
+        const int nf = ef.y & EF_NBR_FACE_MASK;
+        const int tp = (ef.y & EF_REVERSED) ? N - ta[c2] : ta[c2];
+        const long long nb = (long long)ef.x * NP + face_node(N1, nf, tp);
+        nh[c2] = __ldg(S.h + nb);
+        nhu[c2] = __ldg(S.hu + nb);
+        nhv[c2] = __ldg(S.hv + nb);
+      }
+    }
+  }
+  double h = 0.0, hu = 0.0, hv = 0.0, jac = 1.0;
   if (active) {
     h = S.h[n];
     hu = S.hu[n];
     hv = S.hv[n];
+    jac = __ldg(M.jac + n);
     double u, v;
     vel(h, hu, hv, Ph.h_des, u, v);
     fld(P::H)[q] = h;
@@ -1137,39 +1163,54 @@ __global__ void __launch_bounds__(VP<N1>::THREADS)
     fld(P::YX)[q] = M.yx[n];
     fld(P::XX)[q] = M.xx[n];
   }
-  if (threadIdx.x < P::E * 4) sm[P::RED + threadIdx.x] = 0.0;
+  for (int k = tid; k < NP; k += P::THREADS) {
+    sm[P::OPV + (k / N1) * OP + k % N1] = O::Vinv(k / N1, k % N1);
+    sm[P::OPD + (k / N1) * OP + k % N1] = O::Dh(k / N1, k % N1);
+  }
   __syncthreads();
+  const double* VI = sm + P::OPV;
+  const double* DH = sm + P::OPD;
   // ---- modal transform of h: tmp = V^-1 h, modal = tmp V^-T
   double t = 0.0;
 #pragma unroll
-  for (int k = 0; k < N1; ++k) t += O::Vinv(i, k) * fld(P::H)[k * N1 + j];
+  for (int k = 0; k < N1; ++k) t += VI[i * OP + k] * fld(P::H)[k * N1 + j];
   fld(P::TMP)[q] = t;
   __syncthreads();
   double mo = 0.0;
 #pragma unroll
-  for (int k = 0; k < N1; ++k) mo += fld(P::TMP)[i * N1 + k] * O::Vinv(j, k);
-  const double m2 = mo * mo;
+  for (int k = 0; k < N1; ++k) mo += fld(P::TMP)[i * N1 + k] * VI[j * OP + k];
+  const double m2 = active ? mo * mo : 0.0;
   // shells: den1 all, den2 i,j<N, num1 top shell (i==N or j==N), num2 shell N-1
-  fld(P::C0)[q] = m2;
-  fld(P::C1)[q] = (i < N && j < N) ? m2 : 0.0;
-  fld(P::C2)[q] = (i == N || j == N) ? m2 : 0.0;
-  fld(P::C3)[q] = ((i == N - 1 && j <= N - 1) || (j == N - 1 && i <= N - 1)) ? m2 : 0.0;
-  __syncthreads();
-  // fixed-shape tree over the element's nodes: parallel and reproducible
-  constexpr int P2 = NP <= 4 ? 4 : NP <= 16 ? 16 : NP <= 64 ? 64 : NP <= 128 ? 128 : 256;
+  double c[4] = {m2, (i < N && j < N) ? m2 : 0.0, (i == N || j == N) ? m2 : 0.0,
+                 ((i == N - 1 && j <= N - 1) || (j == N - 1 && i <= N - 1)) ? m2 : 0.0};
 #pragma unroll
-  for (int s = P2 / 2; s > 0; s >>= 1) {
-    if (q < s && q + s < NP) {
-      fld(P::C0)[q] += fld(P::C0)[q + s];
-      fld(P::C1)[q] += fld(P::C1)[q + s];
-      fld(P::C2)[q] += fld(P::C2)[q + s];
-      fld(P::C3)[q] += fld(P::C3)[q + s];
+  for (int o = 1; o < 32; o <<= 1) {
+    const int el2 = __shfl_down_sync(0xffffffffu, el, o);
+    double tt[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) tt[k] = __shfl_down_sync(0xffffffffu, c[k], o);
+    if (lane + o < 32 && el2 == el) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) c[k] += tt[k];
     }
-    __syncthreads();
   }
+  const int w0 = (el * NP) >> 5;  // first warp of the element
+  if (lane == 0 || q == 0) {
+    double* rr = sm + P::RED + (el * P::PMAX + (tid >> 5) - w0) * 4;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) rr[k] = c[k];
+  }
+  __syncthreads();
   if (q == 0 && active) {
-    const double den1 = fld(P::C0)[0], den2 = fld(P::C1)[0];
-    const double num1 = fld(P::C2)[0], num2 = fld(P::C3)[0];
+    const int npc = ((el * NP + NP - 1) >> 5) - w0 + 1;
+    double den1 = 0.0, den2 = 0.0, num1 = 0.0, num2 = 0.0;
+    for (int pc = 0; pc < npc; ++pc) {
+      const double* rr = sm + P::RED + (el * P::PMAX + pc) * 4;
+      den1 += rr[0];
+      den2 += rr[1];
+      num1 += rr[2];
+      num2 += rr[3];
+    }
     const double floor_abs = 1e-28 * den1 + 1e-300;
     double eps = 0.0;
     if (!(den1 <= 1e-300)) {
@@ -1199,7 +1240,7 @@ __global__ void __launch_bounds__(VP<N1>::THREADS)
 #pragma unroll
   for (int m = 0; m < N1; ++m) {
     const int qx = m * N1 + j, qe = i * N1 + m;
-    const double di = O::Dh(i, m), dj = O::Dh(j, m);
+    const double di = DH[i * OP + m], dj = DH[j * OP + m];
     const double ux = fld(P::U)[qx], vx = fld(P::V)[qx], ue = fld(P::U)[qe], ve = fld(P::V)[qe];
     const double yex = fld(P::YE)[qx], xex = fld(P::XE)[qx];
     const double yxe = fld(P::YX)[qe], xxe = fld(P::XX)[qe];
@@ -1215,19 +1256,13 @@ __global__ void __launch_bounds__(VP<N1>::THREADS)
   double u1 = sye_u - syx_u, u2 = sxx_u - sxe_u, v1 = sye_v - syx_v, v2 = sxx_v - sxe_v;
   // interface corrections (viscosity.hpp:114-160): U* = <u> inside, u- on walls
   const double uo = fld(P::U)[q], vo = fld(P::V)[q], iw0 = 1.0 / M.w0;
-  int fa[2], ta[2];
-  const int nfc = node_faces(N1, i, j, fa, ta);
   for (int c2 = 0; c2 < nfc; ++c2) {
-    const int face = fa[c2], tt = ta[c2];
-    const int4 ef = M.ef[e * 4 + face];
-    if (!(ef.y & EF_PRESENT)) continue;
+    const int face = fa[c2];
+    if (!(fy[c2] & EF_PRESENT)) continue;
     double us = uo, vs = vo;
-    if (!(ef.y & EF_WALL)) {
-      const int nf = ef.y & EF_NBR_FACE_MASK;
-      const int tp = (ef.y & EF_REVERSED) ? N - tt : tt;
-      const long long nb = (long long)ef.x * NP + face_node(N1, nf, tp);
+    if (!(fy[c2] & EF_WALL)) {
       double ub, vb;
-      vel(S.h[nb], S.hu[nb], S.hv[nb], Ph.h_des, ub, vb);
+      vel(nh[c2], nhu[c2], nhv[c2], Ph.h_des, ub, vb);
       us = 0.5 * (uo + ub);
       vs = 0.5 * (vo + vb);
     }
@@ -1245,7 +1280,7 @@ __global__ void __launch_bounds__(VP<N1>::THREADS)
     v1 += cy * vs;
     v2 -= cx * vs;
   }
-  const double ij = 1.0 / M.jac[n];
+  const double ij = 1.0 / jac;
   const double he = h * sm[P::EPS + el] * ij;
   fvu[n] = he * u1;
   fvv[n] = he * v1;

@@ -11,7 +11,7 @@ O=gpurun_out/prof_r01
 mkdir -p $O
 timeout 900 python bench.py --steps 10 --warmup 3 > $O/bench_n7.json 2> $O/bench_n7.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-  --log-file $O/launches_n7.csv python bench.py --steps 2 --warmup 3 --cpu-budget 1 > /dev/null 2>&1
+  --log-file $O/launches_n7.csv python bench.py --steps 2 --warmup 3 --cpu-budget 1 --no-sweep > /dev/null 2>&1
 for n in ${DEGREES:-1 2 3 4 5 6 7 8 9 10 11 12 13 14 15}; do
   timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_stage -s 1 -c 1 \
     -o /tmp/stage_n$n -f python -m paper_1804_02221_b200.profile_stage --degree $n --kx 1000 --steps 1 \

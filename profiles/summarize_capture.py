@@ -105,7 +105,7 @@ def main():
             per.setdefault(name, []).append(v)
         tot = sum(sum(v) for v in per.values()) or 1.0
         with open(os.path.join(DST, "r01_launches_n7.txt"), "w") as f:
-            f.write("# ncu launch list of `python bench.py --steps 2 --warmup 3 --cpu-budget 1` (N=7, "
+            f.write("# ncu launch list of `python bench.py --steps 2 --warmup 3 --cpu-budget 1 --no-sweep` (N=7, "
                     "1M elements): gpu__time_duration per kernel, serialised, cold\n")
             f.write("kernel\tlaunches\tavg\tsum\tshare\n")
             for name, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
