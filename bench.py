@@ -31,7 +31,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "FP64 DOF-updates/sec per RK stage"
 UNIT = "DOF-updates/s"
-KX = 1000
+KX = int(os.environ.get("SWDG_BENCH_KX", "1000"))  # smaller meshes: debugging only
 
 
 def frozen_counts(N: int, viscous: bool):

@@ -108,10 +108,7 @@ __device__ __forceinline__ void issue_node(double* sm, const Mesh& M, const Stag
 }
 
 template <int N1, bool FORCE>
-#ifndef FULL_MINB
-#define FULL_MINB 1
-#endif
-__global__ void __launch_bounds__(Plan<N1>::THREADS, FULL_MINB)
+__global__ void __launch_bounds__(Plan<N1>::THREADS, 1)
     k_stage(Mesh M, Phys Ph, StageArgs A, Flags* F) {
   using P = Plan<N1>;
   using O = Ops<N1>;
@@ -1345,10 +1342,7 @@ __device__ __forceinline__ void st_elem(double* __restrict__ p, long long base,
 }
 
 template <int N1, bool FORCE>
-#ifndef ELEM_MINB
-#define ELEM_MINB 1
-#endif
-__global__ void __launch_bounds__(128, ELEM_MINB) k_stage_elem(Mesh M, Phys Ph, StageArgs A, Flags* F) {
+__global__ void __launch_bounds__(128) k_stage_elem(Mesh M, Phys Ph, StageArgs A, Flags* F) {
   using O = Ops<N1>;
   constexpr int NP = N1 * N1;
   const int e = M.e_lo + blockIdx.x * blockDim.x + threadIdx.x;
@@ -1558,6 +1552,8 @@ static void launch_elem(const Mesh& M, const Phys& P, const StageArgs& A, Flags*
   k_stage_elem<N1, FORCE><<<(M.n_owned - M.e_lo + 127) / 128, 128, 0, st>>>(M, P, A, F);
 }
 
+#include "visc_lines.cuh"
+
 // geometry-only split-source coefficients (dg_rhs.hpp:159-176), one thread per node
 __global__ void k_source_geometry(Mesh M, double* sx, double* sy) {
   const long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -1694,12 +1690,21 @@ static void launch_n(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
 
 int launch_fast_visc_pre(const Mesh& M, const Phys& P, CState S, double* eps, double* fvu,
                          double* fvv, double* gvu, double* gvv, Flags* F, cudaStream_t st) {
+  // line-based kernel up to N+1 = 10 (a line of 9 (N+1) doubles fits the
+  // registers), node-per-thread above; SWDG_VISC_NODE=1 forces the latter
+  static const bool node_only = getenv("SWDG_VISC_NODE") != nullptr;
   switch (M.n1) {
+#define SWDG_VL(n)                                                                 \
+  case n:                                                                          \
+    if (node_only) launch_visc_pre_n<n>(M, P, S, eps, fvu, fvv, gvu, gvv, F, st);  \
+    else launch_visc_lines_n<n>(M, P, S, eps, fvu, fvv, gvu, gvv, F, st);          \
+    break;
 #define SWDG_VP(n) \
   case n: launch_visc_pre_n<n>(M, P, S, eps, fvu, fvv, gvu, gvv, F, st); break;
-    SWDG_VP(3) SWDG_VP(4) SWDG_VP(5) SWDG_VP(6) SWDG_VP(7) SWDG_VP(8) SWDG_VP(9) SWDG_VP(10)
+    SWDG_VL(3) SWDG_VL(4) SWDG_VL(5) SWDG_VL(6) SWDG_VL(7) SWDG_VL(8) SWDG_VL(9) SWDG_VL(10)
     SWDG_VP(11) SWDG_VP(12) SWDG_VP(13) SWDG_VP(14) SWDG_VP(15) SWDG_VP(16)
 #undef SWDG_VP
+#undef SWDG_VL
     default: return 0;
   }
   return 1;

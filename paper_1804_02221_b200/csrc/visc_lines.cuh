@@ -1,0 +1,282 @@
+// visc_lines.cuh — line-based viscous pre-kernel (fast mode), included inside
+// kernels_fast.cu's anonymous namespace (uses Ops<>, vel, smin/smax).
+//
+// Per element: the modal shock indicator and viscosity coefficient
+// (shock_indicator / viscosity_coefficient, viscosity.hpp:35-78), the BR1
+// lifted velocity gradients (br1_gradients, viscosity.hpp:95-168) and the
+// physical viscous flux pairs h eps grad (viscous_lhs, viscosity.hpp:187-194),
+// written per node for the stage kernel.
+//
+// The node-per-thread version reads 2(N+1) neighbours x 4 fields from shared
+// memory for every node (shared-memory bandwidth bound: 2.9 ms at N=7, 1M
+// elements).  Here a thread owns a line: xi-line threads (column j) apply the
+// 1D operators along i with the line in registers and constant-bank
+// coefficients, eta-line threads (row i) along j, so each node's data is read
+// from shared memory once per direction:
+//   xi:  tmp = V^-1 h (first modal pass), the xi terms of the BR1 sums
+//        (D-hat of y_eta u, x_eta u, y_eta v, x_eta v) and the E/W face
+//        corrections at the line's endpoints;
+//   eta: the eta terms (D-hat of y_xi u, ...), the S/N face corrections, and —
+//        after the barrier — the second modal pass along j and the row's shell
+//        energies (segmented warp-shuffle reduction per element).
+// Both directions leave their four partials per node in shared memory; the
+// final phase is one thread per node (balanced, coalesced stores).
+#pragma once
+
+template <int N1>
+struct VLP {
+  static constexpr int NP = N1 * N1, N = N1 - 1;
+  static constexpr int E = (128 / (2 * N1)) > 1 ? 128 / (2 * N1) : 1;
+  static constexpr int LPD = E * N1;                 // lines per direction
+  static constexpr int LS = (LPD + 31) / 32 * 32;     // lane slots per direction
+  static constexpr int THREADS = 2 * LS;
+  static constexpr int PAD = N1 | 1, EPAD = N1 * PAD, GPAD = E * EPAD;
+  static constexpr int PMAX = (LPD + 31) / 32 + 1;
+  // shared fields [E][N1][PAD]: state and metrics, the first modal pass, and the
+  // four BR1 partials of each direction
+  enum { H, U, V, YE, XE, YX, XX, TMP, XU1, XU2, XV1, XV2, EU1, EU2, EV1, EV2, kF };
+  static constexpr int RED = kF * GPAD;             // [E][PMAX][4] shell-energy pieces
+  static constexpr int EPS = RED + E * PMAX * 4;
+  static constexpr int TOTAL = EPS + E;
+  static constexpr size_t bytes = TOTAL * sizeof(double);
+};
+
+template <int N1>
+__global__ void __launch_bounds__(VLP<N1>::THREADS)
+    k_visc_lines(Mesh M, Phys Ph, CState S, double* eps_out, double* fvu, double* fvv,
+                 double* gvu, double* gvv, Flags* F) {
+  using P = VLP<N1>;
+  using O = Ops<N1>;
+  constexpr int NP = P::NP, N = P::N, PAD = P::PAD, GP = P::GPAD, LPD = P::LPD;
+  extern __shared__ __align__(16) double sm[];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const bool xi = tid < P::LS;
+  const int ls = xi ? tid : tid - P::LS;  // line slot within the direction
+  const bool line_ok = ls < LPD;
+  const int el = line_ok ? ls / N1 : 0, li = line_ok ? ls - (ls / N1) * N1 : 0;
+  const int e0 = blockIdx.x * P::E, ne = min(P::E, M.n_owned - e0);
+  const bool active = line_ok && el < ne;
+  const int e = e0 + el;
+  const double h_des = Ph.h_des, iw0 = 1.0 / M.w0;
+
+  // neighbour traces at this line's two endpoints, requested first
+  int fy[2] = {0, 0};
+  double nh[2] = {0.0, 0.0}, nhu[2] = {0.0, 0.0}, nhv[2] = {0.0, 0.0};
+  if (active) {
+#pragma unroll
+    for (int end = 0; end < 2; ++end) {
+      const int face = xi ? (end ? 1 : 3) : (end ? 2 : 0);
+      const int4 ef = M.ef[e * 4 + face];
+      fy[end] = ef.y;
+      if ((ef.y & EF_PRESENT) && !(ef.y & EF_WALL)) {
+        const int nf = ef.y & EF_NBR_FACE_MASK;
+        const int tp = (ef.y & EF_REVERSED) ? N - li : li;
+        const long long nb = (long long)ef.x * NP + face_node(N1, nf, tp);
+        nh[end] = __ldg(S.h + nb);
+        nhu[end] = __ldg(S.hu + nb);
+        nhv[end] = __ldg(S.hv + nb);
+      }
+    }
+  }
+  // stage the group's state (+ velocities) and metrics, one thread per node
+  const long long base = (long long)e0 * NP;
+  for (int r = tid; r < ne * NP; r += P::THREADS) {
+    const int el2 = r / NP, q = r - el2 * NP, i = q / N1, j = q - i * N1;
+    double* d = sm + el2 * P::EPAD + i * PAD + j;
+    const long long n = base + r;
+    const double h = S.h[n], hu = S.hu[n], hv = S.hv[n];
+    double u, v;
+    vel(h, hu, hv, h_des, u, v);
+    d[P::H * GP] = h;
+    d[P::U * GP] = u;
+    d[P::V * GP] = v;
+    d[P::YE * GP] = M.ye[n];
+    d[P::XE * GP] = M.xe[n];
+    d[P::YX * GP] = M.yx[n];
+    d[P::XX * GP] = M.xx[n];
+  }
+  __syncthreads();
+
+  // ---- line phase: node k of this line at off0 + k*st
+  const int off0 = el * P::EPAD + (xi ? li : li * PAD), st = xi ? PAD : 1;
+  if (active) {
+    double u[N1], v[N1], A[N1], B[N1];
+    const int fa = (xi ? P::YE : P::YX) * GP, fb = (xi ? P::XE : P::XX) * GP;
+#pragma unroll
+    for (int k = 0; k < N1; ++k) {
+      const int q = off0 + k * st;
+      u[k] = sm[P::U * GP + q];
+      v[k] = sm[P::V * GP + q];
+      A[k] = sm[fa + q];
+      B[k] = sm[fb + q];
+    }
+    if (xi) {  // first modal pass along i: tmp(a, j) = sum_k Vinv(a, k) h(k, j)
+      double hh[N1];
+#pragma unroll
+      for (int k = 0; k < N1; ++k) hh[k] = sm[P::H * GP + off0 + k * st];
+#pragma unroll
+      for (int a = 0; a < N1; ++a) {
+        double t = 0.0;
+#pragma unroll
+        for (int k = 0; k < N1; ++k) t += O::Vinv(a, k) * hh[k];
+        sm[P::TMP * GP + off0 + a * st] = t;
+      }
+    }
+    // BR1 weak D-hat sums along the line (viscosity.hpp:114-126): xi lines give
+    // +Dh(y_eta u), -Dh(x_eta u), ... ; eta lines -Dh(y_xi u), +Dh(x_xi u), ...
+    const double sg = xi ? 1.0 : -1.0;
+    double pu1[N1], pu2[N1], pv1[N1], pv2[N1];
+#pragma unroll
+    for (int a = 0; a < N1; ++a) {
+      double s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
+#pragma unroll
+      for (int m = 0; m < N1; ++m) {
+        const double d = O::Dh(a, m);
+        s1 += d * (A[m] * u[m]);
+        s2 += d * (B[m] * u[m]);
+        s3 += d * (A[m] * v[m]);
+        s4 += d * (B[m] * v[m]);
+      }
+      pu1[a] = sg * s1;
+      pu2[a] = -sg * s2;
+      pv1[a] = sg * s3;
+      pv2[a] = -sg * s4;
+    }
+    // interface corrections at the endpoints (viscosity.hpp:127-160): U* = <u>
+    // inside, u- on walls; face metrics W: -(y_eta, x_eta), E: +(y_eta, x_eta),
+    // S: +(y_xi, x_xi), N: -(y_xi, x_xi)
+#pragma unroll
+    for (int end = 0; end < 2; ++end) {
+      if (!(fy[end] & EF_PRESENT)) continue;
+      const int k = end ? N : 0;
+      double us = u[k], vs = v[k];
+      if (!(fy[end] & EF_WALL)) {
+        double ub, vb;
+        vel(nh[end], nhu[end], nhv[end], h_des, ub, vb);
+        us = 0.5 * (u[k] + ub);
+        vs = 0.5 * (v[k] + vb);
+      }
+      const double s = (xi == (end == 1)) ? 1.0 : -1.0;
+      const double cy = s * A[k] * iw0, cx = s * B[k] * iw0;
+      pu1[k] += cy * us;
+      pu2[k] -= cx * us;
+      pv1[k] += cy * vs;
+      pv2[k] -= cx * vs;
+    }
+    const int f0 = xi ? P::XU1 : P::EU1;
+#pragma unroll
+    for (int k = 0; k < N1; ++k) {
+      const int q = off0 + k * st;
+      sm[(f0 + 0) * GP + q] = pu1[k];
+      sm[(f0 + 1) * GP + q] = pu2[k];
+      sm[(f0 + 2) * GP + q] = pv1[k];
+      sm[(f0 + 3) * GP + q] = pv2[k];
+    }
+  }
+  __syncthreads();  // first modal pass and both directions' partials published
+
+  // ---- eta lines: second modal pass along j and the row's shell energies
+  if (!xi) {
+    double c[4] = {0.0, 0.0, 0.0, 0.0};
+    if (active) {
+      double tr[N1];
+      const int i = li;
+#pragma unroll
+      for (int k = 0; k < N1; ++k) tr[k] = sm[P::TMP * GP + off0 + k];
+#pragma unroll
+      for (int b = 0; b < N1; ++b) {
+        double mo = 0.0;
+#pragma unroll
+        for (int k = 0; k < N1; ++k) mo += tr[k] * O::Vinv(b, k);
+        const double m2 = mo * mo;
+        // shells (viscosity.hpp:44-57): all; i,b < N; top (i or b = N); N-1
+        c[0] += m2;
+        if (i < N && b < N) c[1] += m2;
+        if (i == N || b == N) c[2] += m2;
+        if ((i == N - 1 && b <= N - 1) || (b == N - 1 && i <= N - 1)) c[3] += m2;
+      }
+    }
+    const int seg = active ? el : -1 - lane;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int seg2 = __shfl_down_sync(0xffffffffu, seg, o);
+      double t[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) t[k] = __shfl_down_sync(0xffffffffu, c[k], o);
+      if (lane + o < 32 && seg2 == seg) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) c[k] += t[k];
+      }
+    }
+    const int w0 = (el * N1) >> 5;  // first warp (of the eta half) of the element
+    if (active && (lane == 0 || li == 0)) {
+      double* rr = sm + P::RED + (el * P::PMAX + (ls >> 5) - w0) * 4;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) rr[k] = c[k];
+    }
+  }
+  __syncthreads();
+  // ---- eps per element (viscosity_coefficient, viscosity.hpp:60-78)
+  if (tid < ne) {
+    const int el2 = tid;
+    const int w0 = (el2 * N1) >> 5, npc = ((el2 * N1 + N1 - 1) >> 5) - w0 + 1;
+    double den1 = 0.0, den2 = 0.0, num1 = 0.0, num2 = 0.0;
+    for (int pc = 0; pc < npc; ++pc) {
+      const double* rr = sm + P::RED + (el2 * P::PMAX + pc) * 4;
+      den1 += rr[0];
+      den2 += rr[1];
+      num1 += rr[2];
+      num2 += rr[3];
+    }
+    const double floor_abs = 1e-28 * den1 + 1e-300;
+    double eps = 0.0;
+    if (!(den1 <= 1e-300)) {
+      const double r1 = num1 > floor_abs ? num1 / den1 : 0.0;
+      const double r2 = (num2 > floor_abs && den2 > floor_abs) ? num2 / den2 : 0.0;
+      const double r = smax(r1, r2);
+      if (r > 0.0) {
+        const double sigma = log10(r);
+        if (sigma >= Ph.sigma_max) {
+          eps = Ph.epsilon0;
+        } else if (!(sigma < Ph.sigma_min)) {
+          eps = 0.5 * Ph.epsilon0 *
+                (1.0 + sin(M_PI * (sigma - 0.5 * (Ph.sigma_max + Ph.sigma_min)) /
+                           (Ph.sigma_max - Ph.sigma_min)));
+        }
+      }
+    }
+    sm[P::EPS + el2] = eps;
+    eps_out[e0 + el2] = eps;
+    atomicMax(&F->max_eps_key, order_key(eps));
+  }
+  __syncthreads();
+  // ---- viscous flux pairs, one thread per node (coalesced)
+  for (int r = tid; r < ne * NP; r += P::THREADS) {
+    const int el2 = r / NP, q = r - el2 * NP, i = q / N1, j = q - i * N1;
+    const int pq = el2 * P::EPAD + i * PAD + j;
+    const long long n = base + r;
+    const double u1 = sm[P::XU1 * GP + pq] + sm[P::EU1 * GP + pq];
+    const double u2 = sm[P::XU2 * GP + pq] + sm[P::EU2 * GP + pq];
+    const double v1 = sm[P::XV1 * GP + pq] + sm[P::EV1 * GP + pq];
+    const double v2 = sm[P::XV2 * GP + pq] + sm[P::EV2 * GP + pq];
+    const double he = sm[P::H * GP + pq] * sm[P::EPS + el2] * (1.0 / __ldg(M.jac + n));
+    fvu[n] = he * u1;
+    fvv[n] = he * v1;
+    gvu[n] = he * u2;
+    gvv[n] = he * v2;
+  }
+}
+
+template <int N1>
+void launch_visc_lines_n(const Mesh& M, const Phys& P, CState S, double* eps, double* fvu,
+                         double* fvv, double* gvu, double* gvv, Flags* F, cudaStream_t st) {
+  using PL = VLP<N1>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_visc_lines<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)PL::bytes);
+    attr = true;
+  }
+  const int grid = (M.n_owned + PL::E - 1) / PL::E;
+  k_visc_lines<N1><<<grid, PL::THREADS, PL::bytes, st>>>(M, P, S, eps, fvu, fvv, gvu, gvv, F);
+}
