@@ -79,3 +79,59 @@ def run_simulation(integ: TimeIntegrator, state: State, final_time: float, cfl: 
             next_snap += 1
     out.t = t
     return out
+
+
+def run_simulation_device(integ: TimeIntegrator, state: State, final_time: float, cfl: float,
+                          snapshot_times=(), keep_series: bool = True, diagnostics: bool = True,
+                          max_steps: int | None = None, on_snapshot=None) -> RunResult:
+    """run_simulation (driver.hpp:62-142) with the state resident on the device
+    (SURVEY §8f row 1): the state is uploaded once and downloaded at snapshot
+    events and at the end; each step moves only dt, the accept flag and the step
+    diagnostics across PCIe.  Reject-and-halve rolls back on the device (the
+    integrator keeps W^n until a step is accepted).  Same decisions, same kernels,
+    hence bitwise the same trajectory as run_simulation.  `on_snapshot(t, state)`
+    receives the downloaded state at each snapshot time."""
+    out = RunResult(state=state)
+    integ.upload(state)
+    if diagnostics:
+        d0 = integ.diagnostics_device()
+        out.mass_initial, out.entropy_initial = d0.mass, d0.entropy
+    snaps = sorted(set(float(s) for s in snapshot_times if s <= final_time + 1e-12))
+    next_snap = 0
+    t = 0.0
+    t_eps = 1e-12 * max(1.0, final_time)
+    while t < final_time - t_eps:
+        if max_steps is not None and out.steps >= max_steps:
+            break
+        dt = integ.compute_dt_device(cfl)
+        t_event = final_time
+        if next_snap < len(snaps):
+            t_event = min(t_event, snaps[next_snap])
+        hit_event = False
+        if t + dt >= t_event - t_eps:
+            dt = t_event - t
+            hit_event = True
+        rejections = 0
+        while not integ.try_step_device(t, dt):
+            dt *= 0.5
+            hit_event = False
+            rejections += 1
+            if rejections >= 10:
+                raise NumericalAbort(f"step rejected 10 times at t={t}")
+        t = t_event if hit_event else t + dt
+        out.steps += 1
+        if diagnostics:
+            d = integ.diagnostics_device()
+            sd = StepDiagnostics(out.steps, t, dt, d.mass, d.entropy, d.min_h,
+                                 integ.last_limited_count(), integ.last_max_eps(),
+                                 integ.last_min_stage_h(), d.positivity_dt)
+            if keep_series:
+                out.series.append(sd)
+        while next_snap < len(snaps) and t >= snaps[next_snap] - t_eps:
+            if on_snapshot is not None:
+                integ.download(state)
+                on_snapshot(snaps[next_snap], state)
+            next_snap += 1
+    integ.download(state)
+    out.t = t
+    return out

@@ -479,6 +479,19 @@ class TimeIntegrator:
         self._check(lib().swdg_gpu_last_info(self._h, C.byref(info)))
         return info
 
+    def try_step_device(self, t: float, dt: float) -> bool:
+        """try_step of the device-resident state (no host copies): on a reject the
+        state stays W^n on the device (the stage buffers are discarded)."""
+        self._sync_forcing()
+        self._check(lib().swdg_gpu_try_step(self._h, t, dt, C.byref(self._info)))
+        return bool(self._info.accepted)
+
+    def diagnostics_device(self) -> DiagnosticsC:
+        """mass, entropy, min h and the positivity bound of the device-resident state"""
+        d = DiagnosticsC()
+        self._check(lib().swdg_gpu_diagnostics(self._h, C.byref(d)))
+        return d
+
     def compute_dt_device(self, cfl: float) -> float:
         """compute_dt of the device-resident state (no upload)."""
         dt = C.c_double()

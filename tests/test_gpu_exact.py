@@ -12,7 +12,7 @@ import pytest
 
 from oracle import port, ref
 from paper_1804_02221_b200 import swdg
-from paper_1804_02221_b200.driver import run_simulation
+from paper_1804_02221_b200.driver import run_simulation, run_simulation_device
 from tests.conftest import gpu_available
 from tests.helpers import (MESHES, beq, build, random_state, reversed_mesh, scenario_params,
                            smooth_state)
@@ -139,6 +139,35 @@ def test_full_run_fingerprints(sid, kx, T, steps, fp):
     res = run_simulation(gi, S(st), T, cfg["cfl"], diagnostics=False)
     assert res.steps == steps
     assert ref.fnv1a_state(res.state.arrays()) == fp
+
+
+@pytest.mark.parametrize("mode", [swdg.MODE_EXACT, swdg.MODE_FAST])
+@pytest.mark.parametrize("sid,kx,T,steps,fp", [
+    ("wetdry_dambreak", 12, 0.2, 12, "b7a50b5a3ff22ec4"),
+    ("parabolic_dam_dry", 8, 0.1, 13, "a57e2e67759014a6"),
+])
+def test_device_driver_matches_host_driver(mode, sid, kx, T, steps, fp):
+    """The device-resident driver (state uploaded once, reject-and-halve rolled back
+    on the device, snapshots downloaded on the way) takes the same decisions as the
+    host-state driver: bitwise the same trajectory, step count and diagnostics; in
+    exact mode that is the reference's fingerprint."""
+    m, st = ref.scenario_mesh(sid, kx, kx, 0)
+    p, cfg = scenario_params(sid)
+    host = run_simulation(swdg.TimeIntegrator(m, cfg_from(p, mode)), S(st), T, cfg["cfl"],
+                          snapshot_times=(0.5 * T,))
+    snaps = []
+    dev = run_simulation_device(swdg.TimeIntegrator(m, cfg_from(p, mode)), S(st), T, cfg["cfl"],
+                                snapshot_times=(0.5 * T,),
+                                on_snapshot=lambda t, s: snaps.append((t, s.copy())))
+    assert dev.steps == host.steps and dev.t == host.t
+    assert beq(dev.state.arrays(), host.state.arrays())
+    assert [(a.step, a.dt, a.mass, a.entropy, a.min_h, a.n_limited) for a in dev.series] == \
+        [(a.step, a.dt, a.mass, a.entropy, a.min_h, a.n_limited) for a in host.series]
+    assert len(snaps) == 1 and snaps[0][0] == 0.5 * T
+    if mode == swdg.MODE_EXACT:  # without the snapshot event: the reference's fingerprint
+        plain = run_simulation_device(swdg.TimeIntegrator(m, cfg_from(p, mode)), S(st), T,
+                                      cfg["cfl"], diagnostics=False)
+        assert plain.steps == steps and ref.fnv1a_state(plain.state.arrays()) == fp
 
 
 def test_forcing_callback_bitwise():
