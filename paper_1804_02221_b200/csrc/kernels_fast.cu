@@ -570,8 +570,13 @@ __device__ __forceinline__ void hl_prefetch_line(double* sm, const Mesh& M, cons
   const int e0 = M.e_lo + g * P::E, ne = min(P::E, M.n_owned - e0);
   const long long base = (long long)e0 * P::NP;
   const int cnt = ne * P::NP;
-  // one node per iteration, all 7 fields; divisions by compile-time constants
-  for (int r = tid; r < cnt; r += P::THREADS) {
+  // one node per pass, all fields; the padded shared offset of a thread's node
+  // is the same for every group (divisions by constants, folded per pass)
+  constexpr int PF = (P::E * P::NP + P::THREADS - 1) / P::THREADS;
+#pragma unroll(PF <= 2 ? PF : 1)
+  for (int m = 0; m < PF; ++m) {
+    const int r = tid + m * P::THREADS;
+    if (r >= cnt) break;
     const int el = r / P::NP, q = r - el * P::NP;
     const int i = q / N1, j = q - i * N1;
     double* d = sm + P::LINE + buf * P::LBUF + el * P::EPAD + i * P::PAD + j;
@@ -1020,39 +1025,40 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, (N1 <= 10 ? 3 : 1))
       const double As = part ? Am[SY] : Am[0], Bs = part ? Bm[SY] : Bm[0];
       const double om0 = xi ? As : -As, om1 = xi ? Bs : -Bs;
       const double bo = tr[6 * TRS];
-      double wm0, wm1, wm2, wp0, wp1, wp2, bm, bp, nx, ny, js, sgn = 1.0;
+      // own velocities from the volume phase (the same vel() the neighbour
+      // applies to the gathered trace: both sides see identical bits)
+      const double us = part ? u[SY] : u[0], vs = part ? v[SY] : v[0];
+      const double cs = wave_c(g, hs);
+      double hn, hun, hvn, bn, un, vn, nx, ny, js, sgn = 1.0;
       if (efy & EF_MINUS) {
         face_normal(face, om0, om1, nx, ny, js);
-        wm0 = hs;
-        wm1 = hus;
-        wm2 = hvs;
-        bm = bo;
-        if (efy & EF_WALL) {
-          const double mn = wm1 * nx + wm2 * ny;
-          wp0 = wm0;
-          wp1 = wm1 - 2.0 * mn * nx;
-          wp2 = wm2 - 2.0 * mn * ny;
-          bp = bm;
+        if (efy & EF_WALL) {  // exterior_state (mesh.hpp:382-386)
+          const double mn = hus * nx + hvs * ny;
+          hn = hs;
+          hun = hus - 2.0 * mn * nx;
+          hvn = hvs - 2.0 * mn * ny;
+          bn = bo;
         } else {
-          wp0 = tr[0 * TRS];
-          wp1 = tr[1 * TRS];
-          wp2 = tr[2 * TRS];
-          bp = tr[3 * TRS];
+          hn = tr[0 * TRS];
+          hun = tr[1 * TRS];
+          hvn = tr[2 * TRS];
+          bn = tr[3 * TRS];
         }
       } else {
         face_normal(efy & EF_NBR_FACE_MASK, tr[4 * TRS], tr[5 * TRS], nx, ny, js);
-        wm0 = tr[0 * TRS];
-        wm1 = tr[1 * TRS];
-        wm2 = tr[2 * TRS];
-        bm = tr[3 * TRS];
-        wp0 = hs;
-        wp1 = hus;
-        wp2 = hvs;
-        bp = bo;
+        hn = tr[0 * TRS];
+        hun = tr[1 * TRS];
+        hvn = tr[2 * TRS];
+        bn = tr[3 * TRS];
         sgn = -1.0;
       }
+      vel(hn, hun, hvn, h_des, un, vn);
+      const double cn = wave_c(g, hn);
       double f0, f1, f2;
-      es_flux_fast(wm0, wm1, wm2, wp0, wp1, wp2, bm, bp, nx, ny, g, inv2g, h_des, f0, f1, f2);
+      if (sgn > 0.0)
+        es_flux_pre(hs, us, vs, cs, hn, un, vn, cn, bo, bn, nx, ny, g, inv2g, f0, f1, f2);
+      else
+        es_flux_pre(hn, un, vn, cn, hs, us, vs, cs, bn, bo, nx, ny, g, inv2g, f0, f1, f2);
       const double c = sgn * js * iw0;
       if constexpr (VISC) {
         // viscous interface penalty (viscosity.hpp:224-246): with the minus-side
@@ -1164,7 +1170,21 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, (N1 <= 10 ? 3 : 1))
     // element inside the warp (fixed tree: reproducible), one piece per (warp,
     // element) to shared memory; an element whose lines straddle two warps of
     // its role has two pieces
-    if (xi) {
+    if (xi && (32 % N1 == 0)) {
+      // N+1 divides 32: each element's lines are an aligned lane segment of
+      // N+1 lanes; an xor butterfly leaves the segment sum on all of them
+#pragma unroll
+      for (int o = N1 / 2; o > 0; o >>= 1) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) pv[c] += __shfl_xor_sync(0xffffffffu, pv[c], o);
+        pv[4] = smin(pv[4], __shfl_xor_sync(0xffffffffu, pv[4], o));
+      }
+      if (line_ok && li == 0 && active) {
+        double* rr = sm + P::RED + ((part * P::E + el) * 2) * 5;
+#pragma unroll
+        for (int c = 0; c < 5; ++c) rr[c] = pv[c];
+      }
+    } else if (xi) {
       const int seg = line_ok ? lr / N1 : -1 - lane;  // element of this lane
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
