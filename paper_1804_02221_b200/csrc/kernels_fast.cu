@@ -482,7 +482,11 @@ struct HL {
   enum { F_H, F_HU, F_HV, F_YE, F_XE, F_YX, F_XX, F_FVU, F_GVU, F_FVV, F_GVV };
   static constexpr int kLineFields = V ? 11 : 7;
   static constexpr int kTr = V ? 11 : 7;  // trace slots per face node
-  enum { N_JAC, N_SX, N_SY, N_WH, N_WHU, N_WHV, kNodeFields };
+  // node fields staged per group; the viscous N+1 = 16 variant reads S_x, S_y
+  // straight from global memory (its shared memory then fits two CTAs per SM)
+  static constexpr bool kSxGlobal = V && N1 >= 16;
+  enum { N_JAC, N_WH, N_WHU, N_WHV, N_SX, N_SY };
+  static constexpr int kNodeFields = kSxGlobal ? 4 : 6;
   static constexpr int XS = 3 * (NB0 + H);  // exchange slots per line
   static constexpr int LP = 32 * WP;        // lane slots per part (>= L; tail lanes idle)
   // shared-memory plan, in doubles.  The line data is double-buffered (group
@@ -613,11 +617,13 @@ __device__ __forceinline__ void hl_issue_node(double* sm, const Mesh& M, const S
   const int shift = (int)(((long long)e0 * P::NP) & 1);
   const uint32_t fb = round16((size_t)(ne * P::NP + shift) * sizeof(double));
   const bool wn = A.update && A.stage > 0;
-  mbar_expect_tx(bar, (wn ? 6 : 3) * fb);
+  mbar_expect_tx(bar, ((wn ? 4 : 1) + (P::kSxGlobal ? 0 : 2)) * fb);
   const long long off = (long long)e0 * P::NP - shift;
   bulk_g2s(sm + P::NODE + P::N_JAC * P::GNP, M.jac + off, fb, bar);
-  bulk_g2s(sm + P::NODE + P::N_SX * P::GNP, M.sx + off, fb, bar);
-  bulk_g2s(sm + P::NODE + P::N_SY * P::GNP, M.sy + off, fb, bar);
+  if constexpr (!P::kSxGlobal) {
+    bulk_g2s(sm + P::NODE + P::N_SX * P::GNP, M.sx + off, fb, bar);
+    bulk_g2s(sm + P::NODE + P::N_SY * P::GNP, M.sy + off, fb, bar);
+  }
   if (wn) {
     bulk_g2s(sm + P::NODE + P::N_WH * P::GNP, A.wn.h + off, fb, bar);
     bulk_g2s(sm + P::NODE + P::N_WHU * P::GNP, A.wn.hu + off, fb, bar);
@@ -1130,8 +1136,10 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, (N1 <= 10 ? 3 : 1))
         const double jac = Nd[P::N_JAC * P::GNP + q];
         const double ij = -1.0 / jac, hg2 = 0.5 * g * h[s];
         double rh = (acc[0 * P::GPAD + qp] + r0[s]) * ij;
-        double rhu = (acc[1 * P::GPAD + qp] + r1[s] + hg2 * Nd[P::N_SX * P::GNP + q]) * ij;
-        double rhv = (acc[2 * P::GPAD + qp] + r2[s] + hg2 * Nd[P::N_SY * P::GNP + q]) * ij;
+        const double sxv = P::kSxGlobal ? __ldg(M.sx + n) : Nd[P::N_SX * P::GNP + q];
+        const double syv = P::kSxGlobal ? __ldg(M.sy + n) : Nd[P::N_SY * P::GNP + q];
+        double rhu = (acc[1 * P::GPAD + qp] + r1[s] + hg2 * sxv) * ij;
+        double rhv = (acc[2 * P::GPAD + qp] + r2[s] + hg2 * syv) * ij;
         if (FORCE) {
           rh += A.fh[n];
           rhu += A.fhu[n];

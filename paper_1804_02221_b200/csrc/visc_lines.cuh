@@ -125,17 +125,24 @@ __global__ void __launch_bounds__(VLP<N1>::THREADS)
     // BR1 weak D-hat sums along the line (viscosity.hpp:114-126): xi lines give
     // +Dh(y_eta u), -Dh(x_eta u), ... ; eta lines -Dh(y_xi u), +Dh(x_xi u), ...
     const double sg = xi ? 1.0 : -1.0;
-    double pu1[N1], pu2[N1], pv1[N1], pv2[N1];
+    double pu1[N1], pu2[N1], pv1[N1], pv2[N1], Au[N1], Bu[N1], Av[N1], Bv[N1];
+#pragma unroll
+    for (int m = 0; m < N1; ++m) {
+      Au[m] = A[m] * u[m];
+      Bu[m] = B[m] * u[m];
+      Av[m] = A[m] * v[m];
+      Bv[m] = B[m] * v[m];
+    }
 #pragma unroll
     for (int a = 0; a < N1; ++a) {
       double s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
 #pragma unroll
       for (int m = 0; m < N1; ++m) {
         const double d = O::Dh(a, m);
-        s1 += d * (A[m] * u[m]);
-        s2 += d * (B[m] * u[m]);
-        s3 += d * (A[m] * v[m]);
-        s4 += d * (B[m] * v[m]);
+        s1 += d * Au[m];
+        s2 += d * Bu[m];
+        s3 += d * Av[m];
+        s4 += d * Bv[m];
       }
       pu1[a] = sg * s1;
       pu2[a] = -sg * s2;
