@@ -10,6 +10,9 @@ set -x
 O=gpurun_out/prof_r01
 mkdir -p $O
 timeout 900 python bench.py --steps 10 --warmup 3 > $O/bench_n7.json 2> $O/bench_n7.err
+timeout 600 python bench.py --steps 10 --warmup 3 --viscous --no-sweep > $O/bench_n7_visc.json 2> $O/bench_n7_visc.err
+timeout 600 python bench.py --steps 5 --warmup 3 --distributed --no-sweep --cpu-budget 1 > $O/bench_n7_dist1.json 2> $O/bench_n7_dist1.err
+timeout 600 python bench.py --impl reference --steps 10 --warmup 3 > $O/bench_ref.json 2> $O/bench_ref.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file $O/launches_n7.csv python bench.py --steps 2 --warmup 3 --cpu-budget 1 --no-sweep > /dev/null 2>&1
 for n in ${DEGREES:-1 2 3 4 5 6 7 8 9 10 11 12 13 14 15}; do

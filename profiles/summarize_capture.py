@@ -110,7 +110,10 @@ def main():
             f.write("kernel\tlaunches\tavg\tsum\tshare\n")
             for name, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
                 f.write(f"{name}\t{len(v)}\t{sum(v) / len(v):.1f}\t{sum(v):.1f}\t{sum(v) / tot:.3f}\n")
-    for a, b in (("bench_n7.json", "r01_bench_n7.json"), ("sweep.txt", "r01_sweep.txt")):
+    for a, b in (("bench_n7.json", "r01_bench_n7.json"), ("sweep.txt", "r01_sweep.txt"),
+                 ("bench_n7_visc.json", "r01_bench_n7_visc.json"),
+                 ("bench_n7_dist1.json", "r01_bench_n7_dist1.json"),
+                 ("bench_ref.json", "r01_bench_ref.json")):
         p = os.path.join(SRC, a)
         if os.path.exists(p):
             with open(p) as fi, open(os.path.join(DST, b), "w") as fo:
