@@ -164,3 +164,37 @@ def test_gloo_two_ranks_bitwise(tmp_path):
         for j in range(3):
             got[j][sel] = mine[j]
     assert beq(got, want)
+
+
+@pytest.mark.parametrize("kx,ky,P", [(8, 12, 3), (10, 10, 2), (6, 20, 4)])
+def test_interior_range_is_halo_free(kx, ky, P):
+    """interior_range (the part of a stage that runs while the halo is in flight):
+    no element in [lo, hi) has a face to a ghost, and for a band partition it is the
+    band minus its first and last element row."""
+    from paper_1804_02221_b200 import swdg
+    faces = swdg.structured_faces(kx, ky, True, True)
+    for r in range(P):
+        _, n_owned, lf, _, _ = part.build_plan(faces, kx * ky, 3, P, r)
+        lo, hi = part.interior_range(lf, n_owned)
+        f = np.asarray(lf).reshape(-1, 6)
+        inter = f[:, 5] == 0
+        for a, b in ((f[:, 0], f[:, 2]), (f[:, 2], f[:, 0])):
+            sel = inter & (a >= lo) & (a < hi)
+            assert not np.any(b[sel] >= n_owned)
+        if n_owned // kx >= 3:
+            assert (lo, hi) == (kx, n_owned - kx)
+
+
+def test_bench_frozen_roofline():
+    """bench.py's frozen counts: 112 B/node, the flop model, and the
+    roof per degree (HBM-bound up to N=8, FP64 above, 1.10e11 DOF/s at N=15)."""
+    import bench
+    b, f = bench.frozen_counts(7, False)
+    assert b == 112.0 and abs(f / 3 - 174.2) < 0.1
+    b, f = bench.frozen_counts(15, False)
+    assert abs(f / 3 - 336.4) < 0.1
+    roof = lambda n: min(6541.8e9 / (bench.frozen_counts(n, False)[0] / 3),
+                         36.8e12 / (bench.frozen_counts(n, False)[1] / 3))
+    assert abs(roof(7) - 1.752e11) < 1e9 and abs(roof(15) - 1.094e11) < 1e9
+    assert "half-line" in bench.stage_kernel(7, False)
+    assert "element" in bench.stage_kernel(1, False)
