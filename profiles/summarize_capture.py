@@ -116,8 +116,12 @@ def main():
                  ("bench_ref.json", "r01_bench_ref.json")):
         p = os.path.join(SRC, a)
         if os.path.exists(p):
-            with open(p) as fi, open(os.path.join(DST, b), "w") as fo:
-                fo.write(fi.read())
+            with open(p) as fi:
+                lines = fi.read().splitlines()
+            if a.endswith(".json"):  # the bench line (drop any banner before it)
+                lines = [l for l in lines if l.startswith("{")][-1:]
+            with open(os.path.join(DST, b), "w") as fo:
+                fo.write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
 
