@@ -318,6 +318,33 @@ def cpu_reference(N: int, viscous: bool, budget_s: float = 15.0, kx: int = 64, s
     return dict(value=3 * dofs * n / el, seconds=el, steps=n, kx=kx, dofs=dofs)
 
 
+def _ref_worker(args):
+    N, viscous, steps, budget, barrier = args
+    barrier.wait()
+    if steps is None:
+        return cpu_reference(N, viscous, budget_s=budget)
+    return cpu_reference(N, viscous, steps=steps)
+
+
+def cpu_reference_parallel(N: int, viscous: bool, steps, procs: int, budget_s: float = 15.0):
+    """P concurrent processes of cpu_reference (each its own patch, released
+    together by a barrier): the aggregate DOF-updates/s of the host."""
+    if procs <= 1:
+        r = (cpu_reference(N, viscous, budget_s=budget_s) if steps is None
+             else cpu_reference(N, viscous, steps=steps))
+        r["procs"] = 1
+        return r
+    import multiprocessing as mp
+    ctx = mp.get_context("fork")
+    with ctx.Manager() as man:
+        barrier = man.Barrier(procs)
+        with ctx.Pool(procs) as pool:
+            rs = pool.map(_ref_worker, [(N, viscous, steps, budget_s, barrier)] * procs)
+    secs = max(r["seconds"] for r in rs)
+    return dict(value=sum(r["value"] for r in rs), seconds=secs, steps=rs[0]["steps"],
+                kx=rs[0]["kx"], dofs=rs[0]["dofs"], procs=procs)
+
+
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
@@ -359,17 +386,21 @@ def main():
     if args.impl == "reference":
         if world > 1 and rank != 0:
             return
-        steps = max(1, args.steps // 10)
-        r = cpu_reference(N, args.viscous, steps=steps + args.warmup)
+        # the reference is single-threaded: on all host cores it is P independent
+        # processes, each stepping its own patch of the workload at the same time
+        steps = max(1, args.steps // 10) + args.warmup
+        P = int(os.environ.get("SWDG_REF_PROCS", "0")) or max(1, len(os.sched_getaffinity(0)))
+        r = cpu_reference_parallel(N, args.viscous, steps, P)
         line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
                 "n_gpus": args.gpus, "steps": r["steps"], "warmup": 0,
                 "ms_per_step": 1e3 * r["seconds"] / r["steps"], "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": config,
-                "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": 1,
+                "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["procs"],
                                  "kind": "reference",
-                                 "sample": f"reference TimeIntegrator::try_step on a "
-                                           f"{r['kx']}x{r['kx']} patch of the same mesh family, "
+                                 "sample": f"{r['procs']} concurrent single-threaded processes of the "
+                                           f"reference TimeIntegrator::try_step (oracle/_ref), each on "
+                                           f"a {r['kx']}x{r['kx']} patch of the same mesh family, "
                                            f"{r['steps']} steps, {r['seconds']:.1f} s, {cpu_model()}"},
                 "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
@@ -447,10 +478,12 @@ def main():
     if distributed:
         out["halo_peers_rank0"] = r.get("halo_peers")
     if rank == 0:
-        cb = cpu_reference(N, args.viscous, budget_s=args.cpu_budget)
+        procs = int(os.environ.get("SWDG_REF_PROCS", "0")) or max(1, len(os.sched_getaffinity(0)))
+        cb = cpu_reference_parallel(N, args.viscous, None, procs, budget_s=args.cpu_budget)
         out["cpu_baseline"] = {
-            "value": cb["value"], "unit": UNIT, "cores": 1, "kind": "reference",
-            "sample": f"oracle/_ref TimeIntegrator::try_step, {cb['kx']}x{cb['kx']} patch of the "
+            "value": cb["value"], "unit": UNIT, "cores": cb["procs"], "kind": "reference",
+            "sample": f"{cb['procs']} concurrent single-threaded processes of oracle/_ref "
+                      f"TimeIntegrator::try_step, each on a {cb['kx']}x{cb['kx']} patch of the "
                       f"same mesh family, {cb['steps']} steps in {cb['seconds']:.1f} s, "
                       f"{cpu_model()}"}
         if args.sweep and not distributed:

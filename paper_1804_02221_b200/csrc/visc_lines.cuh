@@ -26,7 +26,10 @@
 template <int N1>
 struct VLP {
   static constexpr int NP = N1 * N1, N = N1 - 1;
-  static constexpr int E = (128 / (2 * N1)) > 1 ? 128 / (2 * N1) : 1;
+#ifndef VL_THREADS
+#define VL_THREADS 128
+#endif
+  static constexpr int E = (VL_THREADS / (2 * N1)) > 1 ? VL_THREADS / (2 * N1) : 1;
   static constexpr int LPD = E * N1;                 // lines per direction
   static constexpr int LS = (LPD + 31) / 32 * 32;     // lane slots per direction
   static constexpr int THREADS = 2 * LS;
