@@ -152,6 +152,26 @@ def smooth_state(x, y):
     return h, 0.3 * h, -0.2 * h
 
 
+def memcpy_d2d_gbs(nbytes: int = 4 << 30, reps: int = 10) -> float:
+    """cudaMemcpy device-to-device bandwidth (read + write bytes / time), the
+    paper's memory reference (bench.hpp:216-229 memcopy_baseline)"""
+    import torch
+    a = torch.empty(nbytes // 8, dtype=torch.float64, device="cuda")
+    b = torch.empty_like(a)
+    b.copy_(a)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        b.copy_(a)
+    e1.record()
+    torch.cuda.synchronize()
+    gbs = 2 * nbytes * reps / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    del a, b
+    torch.cuda.empty_cache()
+    return gbs
+
+
 def measure_gpu(N: int, steps: int, warmup: int, viscous: bool, rank: int, world: int,
                 e2e_steps: int = 20):
     import numpy as np
@@ -477,6 +497,8 @@ def main():
     }
     if distributed:
         out["halo_peers_rank0"] = r.get("halo_peers")
+    if rank == 0 and not distributed:
+        out["roofline"]["memcpy_d2d_gbs"] = memcpy_d2d_gbs()
     if rank == 0:
         procs = int(os.environ.get("SWDG_REF_PROCS", "0")) or max(1, len(os.sched_getaffinity(0)))
         cb = cpu_reference_parallel(N, args.viscous, None, procs, budget_s=args.cpu_budget)
