@@ -51,7 +51,7 @@ def stage_kernel(N: int, viscous: bool) -> str:
         return "k_stage_hl<%d,..,visc> (half-line) + k_visc_pre<%d>" % (n1, n1)
     if n1 <= 3:
         return "k_stage_elem<%d> (element per thread)" % n1
-    if n1 <= 5:
+    if n1 <= 4:
         return "k_stage<%d> (full-line)" % n1
     return "k_stage_hl<%d> (half-line)" % n1
 

@@ -1851,13 +1851,12 @@ static void launch_n(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
       return;
     }
   }
-  // inviscid kernel choice: element-per-thread (N+1 <= 3), full-line (N+1 = 4,
-  // 5), half-line (N+1 >= 6); SWDG_FAST_VARIANT=elem/full/half/pl overrides where
-  // the variant exists for this degree
-  // measured on B200 (1M elements, profiles/r01_sweep_variants.txt): full-line
-  // at N+1 = 4, 5; half-line from N+1 = 6 on (odd row stride: no bank conflicts
-  // at odd N+1 either)
-  int v = N1 <= 3 ? 3 : ((N1 == 4 || N1 == 5) ? 1 : 2);
+  // inviscid kernel choice: element-per-thread (N+1 <= 3), full-line (N+1 = 4),
+  // half-line (N+1 >= 5); SWDG_FAST_VARIANT=elem/full/half/pl overrides where the
+  // variant exists for this degree.  Measured on B200 (1M elements,
+  // profiles/r01_sweep_variants.txt): full-line 0.93 vs half-line 1.65 ms/stage at
+  // N+1 = 4, half-line 1.355 vs full-line 1.378 at N+1 = 5
+  int v = N1 <= 3 ? 3 : (N1 == 4 ? 1 : 2);
   const int ov = variant_override();
   if (ov == 3 && N1 <= 3) v = 3;
   if (ov == 1 && N1 <= 8) v = 1;

@@ -61,6 +61,23 @@ class TorchExchanger:
         self.roff, nr = _offsets(plan, "recv_idx")
         self.send = torch.zeros(max(ns, 1) * 4, dtype=torch.float64, device=device)
         self.recv = torch.zeros(max(nr, 1) * 4, dtype=torch.float64, device=device)
+        self._ops = {}  # what -> the P2P op list (same buffers every stage: built once)
+
+    def _p2p_ops(self, what: int):
+        ops = self._ops.get(what)
+        if ops is None:
+            dist = self.torch.distributed
+            nf = 4 if what else 3
+            ops = []
+            for p in self.b.plan.peers:
+                o, n = self.soff[p]
+                if n:
+                    ops.append(dist.P2POp(dist.isend, self.send[o * nf:(o + n) * nf], p))
+                o, n = self.roff[p]
+                if n:
+                    ops.append(dist.P2POp(dist.irecv, self.recv[o * nf:(o + n) * nf], p))
+            self._ops[what] = ops
+        return ops
 
     def exchange(self, what: int, k: int):
         self.finish(self.start(what, k))
@@ -68,18 +85,9 @@ class TorchExchanger:
     def start(self, what: int, k: int):
         """pack + post the sends/receives; NCCL runs them on its own stream, after
         the pack on the current stream.  Returns the handle `finish` takes."""
-        dist = self.torch.distributed
-        nf = 4 if what else 3
         self.b.pack(what, k, self.send)
-        ops = []
-        for p in self.b.plan.peers:
-            o, n = self.soff[p]
-            if n:
-                ops.append(dist.P2POp(dist.isend, self.send[o * nf:(o + n) * nf], p))
-            o, n = self.roff[p]
-            if n:
-                ops.append(dist.P2POp(dist.irecv, self.recv[o * nf:(o + n) * nf], p))
-        return what, k, (dist.batch_isend_irecv(ops) if ops else [])
+        ops = self._p2p_ops(what)
+        return what, k, (self.torch.distributed.batch_isend_irecv(ops) if ops else [])
 
     def finish(self, handle):
         """the current stream waits for the transfers, then unpacks"""
