@@ -1885,8 +1885,10 @@ static void launch_n(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
 
 int launch_fast_visc_pre(const Mesh& M, const Phys& P, CState S, double* eps, double* fvu,
                          double* fvv, double* gvu, double* gvv, Flags* F, cudaStream_t st) {
-  // line-based kernel up to N+1 = 10 (a line of 9 (N+1) doubles fits the
-  // registers), node-per-thread above; SWDG_VISC_NODE=1 forces the latter
+  // line-based kernel (one velocity component at a time: ~5 (N+1) doubles per
+  // thread) up to N+1 = 13 (measured 22.5 vs 24.5 ms/stage at N=12), the
+  // node-per-thread kernel above (at N+1 = 16 the line kernel's 212 registers
+  // and 70 KB leave 6 warps/SM: 50.3 vs 47.6 ms); SWDG_VISC_NODE=1 forces it
   static const bool node_only = getenv("SWDG_VISC_NODE") != nullptr;
   switch (M.n1) {
 #define SWDG_VL(n)                                                                 \
@@ -1897,7 +1899,7 @@ int launch_fast_visc_pre(const Mesh& M, const Phys& P, CState S, double* eps, do
 #define SWDG_VP(n) \
   case n: launch_visc_pre_n<n>(M, P, S, eps, fvu, fvv, gvu, gvv, F, st); break;
     SWDG_VL(3) SWDG_VL(4) SWDG_VL(5) SWDG_VL(6) SWDG_VL(7) SWDG_VL(8) SWDG_VL(9) SWDG_VL(10)
-    SWDG_VP(11) SWDG_VP(12) SWDG_VP(13) SWDG_VP(14) SWDG_VP(15) SWDG_VP(16)
+    SWDG_VL(11) SWDG_VL(12) SWDG_VL(13) SWDG_VP(14) SWDG_VP(15) SWDG_VP(16)
 #undef SWDG_VP
 #undef SWDG_VL
     default: return 0;

@@ -105,13 +105,11 @@ __global__ void __launch_bounds__(VLP<N1>::THREADS)
   // ---- line phase: node k of this line at off0 + k*st
   const int off0 = el * P::EPAD + (xi ? li : li * PAD), st = xi ? PAD : 1;
   if (active) {
-    double u[N1], v[N1], A[N1], B[N1];
+    double A[N1], B[N1];
     const int fa = (xi ? P::YE : P::YX) * GP, fb = (xi ? P::XE : P::XX) * GP;
 #pragma unroll
     for (int k = 0; k < N1; ++k) {
       const int q = off0 + k * st;
-      u[k] = sm[P::U * GP + q];
-      v[k] = sm[P::V * GP + q];
       A[k] = sm[fa + q];
       B[k] = sm[fb + q];
     }
@@ -127,62 +125,53 @@ __global__ void __launch_bounds__(VLP<N1>::THREADS)
         sm[P::TMP * GP + off0 + a * st] = t;
       }
     }
-    // BR1 weak D-hat sums along the line (viscosity.hpp:114-126): xi lines give
-    // +Dh(y_eta u), -Dh(x_eta u), ... ; eta lines -Dh(y_xi u), +Dh(x_xi u), ...
+    // neighbour velocities at the endpoints (interface U* = <u>, walls u-)
+    double nu[2] = {0.0, 0.0}, nv[2] = {0.0, 0.0};
+#pragma unroll
+    for (int end = 0; end < 2; ++end)
+      if ((fy[end] & EF_PRESENT) && !(fy[end] & EF_WALL))
+        vel(nh[end], nhu[end], nhv[end], h_des, nu[end], nv[end]);
+    // BR1 weak D-hat sums along the line (viscosity.hpp:114-126), one velocity
+    // component at a time (register footprint ~5 (N+1) doubles): xi lines give
+    // +Dh(y_eta w), -Dh(x_eta w); eta lines -Dh(y_xi w), +Dh(x_xi w); then the
+    // interface corrections at the endpoints (viscosity.hpp:127-160), face
+    // metrics W: -(y_eta, x_eta), E: +(y_eta, x_eta), S: +(y_xi, x_xi), N: -(y_xi, x_xi)
     const double sg = xi ? 1.0 : -1.0;
-    double pu1[N1], pu2[N1], pv1[N1], pv2[N1], Au[N1], Bu[N1], Av[N1], Bv[N1];
-#pragma unroll
-    for (int m = 0; m < N1; ++m) {
-      Au[m] = A[m] * u[m];
-      Bu[m] = B[m] * u[m];
-      Av[m] = A[m] * v[m];
-      Bv[m] = B[m] * v[m];
-    }
-#pragma unroll
-    for (int a = 0; a < N1; ++a) {
-      double s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
-#pragma unroll
-      for (int m = 0; m < N1; ++m) {
-        const double d = O::Dh(a, m);
-        s1 += d * Au[m];
-        s2 += d * Bu[m];
-        s3 += d * Av[m];
-        s4 += d * Bv[m];
-      }
-      pu1[a] = sg * s1;
-      pu2[a] = -sg * s2;
-      pv1[a] = sg * s3;
-      pv2[a] = -sg * s4;
-    }
-    // interface corrections at the endpoints (viscosity.hpp:127-160): U* = <u>
-    // inside, u- on walls; face metrics W: -(y_eta, x_eta), E: +(y_eta, x_eta),
-    // S: +(y_xi, x_xi), N: -(y_xi, x_xi)
-#pragma unroll
-    for (int end = 0; end < 2; ++end) {
-      if (!(fy[end] & EF_PRESENT)) continue;
-      const int k = end ? N : 0;
-      double us = u[k], vs = v[k];
-      if (!(fy[end] & EF_WALL)) {
-        double ub, vb;
-        vel(nh[end], nhu[end], nhv[end], h_des, ub, vb);
-        us = 0.5 * (u[k] + ub);
-        vs = 0.5 * (v[k] + vb);
-      }
-      const double s = (xi == (end == 1)) ? 1.0 : -1.0;
-      const double cy = s * A[k] * iw0, cx = s * B[k] * iw0;
-      pu1[k] += cy * us;
-      pu2[k] -= cx * us;
-      pv1[k] += cy * vs;
-      pv2[k] -= cx * vs;
-    }
     const int f0 = xi ? P::XU1 : P::EU1;
 #pragma unroll
-    for (int k = 0; k < N1; ++k) {
-      const int q = off0 + k * st;
-      sm[(f0 + 0) * GP + q] = pu1[k];
-      sm[(f0 + 1) * GP + q] = pu2[k];
-      sm[(f0 + 2) * GP + q] = pv1[k];
-      sm[(f0 + 3) * GP + q] = pv2[k];
+    for (int c = 0; c < 2; ++c) {
+      double w[N1], Aw[N1], Bw[N1];
+#pragma unroll
+      for (int m = 0; m < N1; ++m) {
+        w[m] = sm[(c ? P::V : P::U) * GP + off0 + m * st];
+        Aw[m] = A[m] * w[m];
+        Bw[m] = B[m] * w[m];
+      }
+      double* o1 = sm + (f0 + 2 * c) * GP + off0;      // u1 / v1 partial
+      double* o2 = sm + (f0 + 2 * c + 1) * GP + off0;  // u2 / v2 partial
+#pragma unroll
+      for (int a = 0; a < N1; ++a) {
+        double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) {
+          const double d = O::Dh(a, m);
+          s1 += d * Aw[m];
+          s2 += d * Bw[m];
+        }
+        double p1 = sg * s1, p2 = -sg * s2;
+        if (a == 0 || a == N) {
+          const int end = a == N ? 1 : 0;
+          if (fy[end] & EF_PRESENT) {
+            const double nb = c ? nv[end] : nu[end];
+            const double ws = (fy[end] & EF_WALL) ? w[a] : 0.5 * (w[a] + nb);
+            const double s = (xi == (end == 1)) ? 1.0 : -1.0;
+            p1 += (s * A[a] * iw0) * ws;
+            p2 -= (s * B[a] * iw0) * ws;
+          }
+        }
+        o1[a * st] = p1;
+        o2[a * st] = p2;
+      }
     }
   }
   __syncthreads();  // first modal pass and both directions' partials published

@@ -229,6 +229,27 @@ def test_fast_viscous_rhs(name):
             assert np.abs(e_gpu - e_ref).max() <= 1e-13 * max(1e-300, e_ref.max(), 1.0)
 
 
+@pytest.mark.parametrize("degree", [2, 5, 9, 10, 12, 15])
+def test_fast_viscous_all_degrees(degree):
+    """The line-based viscous pre-kernel and the viscous stage kernel across the
+    degree range (the element configurations differ per degree): one stage within
+    1e-12 normwise, eps within 1e-13, with elements inside the sine ramp."""
+    m = ref.build_mesh("wavy", degree, 3, 2, periodic_x=True, periodic_y=True).bathymetry("smooth")
+    smin = -(4.0 + 4.25 * math.log10(degree)) - 1.0
+    p = ref.params(g=9.81, visc=True, epsilon0=0.1, sigma_min=smin, sigma_max=smin + 2.0)
+    s = random_state(m.n_nodes, np.random.default_rng(degree), dry_prob=0.05)
+    ri = ref.Integrator(m, p)
+    r_ref = ri.evaluate_rhs(s)
+    gi = swdg.TimeIntegrator(m, cfg_from(p))
+    r_gpu = gi.evaluate_rhs(S(s))
+    err = max(np.abs(a - b).max() for a, b in zip(r_gpu.arrays(), r_ref))
+    flux_scale = 9.81 * float(np.max(s[0])) ** 2
+    assert err <= TOL_STAGE * max(max(np.abs(b).max() for b in r_ref), flux_scale)
+    e_ref, e_gpu = ri.last_eps(), gi.last_eps()
+    assert e_ref.max() > 0.0
+    assert np.abs(e_gpu - e_ref).max() <= 1e-13 * max(e_ref.max(), 1.0)
+
+
 @pytest.mark.parametrize("sid,kx,deg", [("wetdry_dambreak", 10, 3), ("parabolic_dam_dry", 8, 3),
                                         ("oscillating_lake", 12, 4), ("parabolic_dam_wet", 8, 7)])
 def test_fast_viscous_step(sid, kx, deg):
