@@ -55,6 +55,17 @@ extern "C" {
 #define SWDG_MODE_EXACT 0
 #define SWDG_MODE_FAST 1
 
+/* Discretisation, SchemeMode (dg_rhs.hpp:14, RunConfig::mode timeloop.hpp:27).
+ * ES: split-form entropy-conservative volume + entropy-stable interface flux
+ * (the throughput path).  STANDARD: pointwise fluxes differentiated with D
+ * (standard_volume_element dg_rhs.hpp:75-117) + the local Lax-Friedrichs
+ * interface flux in strong form (llf_surface_flux fluxes.hpp:192-202,
+ * surface_terms dg_rhs.hpp:228-246), no artificial viscosity (evaluate_rhs
+ * timeloop.hpp:178).  STANDARD always runs the exact-mode kernels: it is the
+ * paper's comparison scheme, bitwise with the reference, not a throughput path. */
+#define SWDG_SCHEME_ES 0
+#define SWDG_SCHEME_STANDARD 1
+
 /* Face tags, BoundaryTag (mesh.hpp:30). */
 #define SWDG_TAG_INTERIOR 0
 #define SWDG_TAG_WALL 1
@@ -101,8 +112,8 @@ typedef struct swdg_params {
   double epsilon0, sigma_min, sigma_max;
   int32_t visc_enabled;
   int32_t limiter_enabled;
-  int32_t mode; /* SWDG_MODE_* */
-  int32_t reserved;
+  int32_t mode;   /* SWDG_MODE_* */
+  int32_t scheme; /* SWDG_SCHEME_* (0 = ES) */
 } swdg_params;
 
 /* Per-try_step report: TimeIntegrator::last_limited_count / last_max_eps /

@@ -29,8 +29,6 @@ class TimeIntegrator {
   // otherwise the fused fast kernels (1e-12 per stage).
   TimeIntegrator(const Mesh& mesh, const RunConfig& cfg, bool exact = true, int device = 0)
       : mesh_(mesh), cfg_(cfg) {
-    if (cfg.mode != SchemeMode::es)
-      throw SwdgError("gpu::TimeIntegrator: only the entropy-stable scheme runs on the GPU");
     faces_.reserve(mesh.topo.faces.size());
     for (const FaceInfo& f : mesh.topo.faces)
       faces_.push_back(swdg_face{f.elem_minus, f.face_minus, f.elem_plus, f.face_plus,
@@ -71,6 +69,7 @@ class TimeIntegrator {
     p.visc_enabled = cfg.visc.enabled ? 1 : 0;
     p.limiter_enabled = cfg.limiter_enabled ? 1 : 0;
     p.mode = exact ? SWDG_MODE_EXACT : SWDG_MODE_FAST;
+    p.scheme = cfg.mode == SchemeMode::standard ? SWDG_SCHEME_STANDARD : SWDG_SCHEME_ES;
     const int rc = swdg_gpu_create(&v, &p, device, &ctx_);
     if (rc != SWDG_OK) raise(rc, swdg_gpu_create_error());
   }

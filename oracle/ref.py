@@ -29,7 +29,7 @@ class Params(C.Structure):
     _fields_ = [("g", C.c_double), ("h_tol", C.c_double), ("h_des", C.c_double),
                 ("h_ref", C.c_double), ("epsilon0", C.c_double), ("sigma_min", C.c_double),
                 ("sigma_max", C.c_double), ("visc_enabled", C.c_int32),
-                ("limiter_enabled", C.c_int32), ("mode", C.c_int32), ("reserved", C.c_int32)]
+                ("limiter_enabled", C.c_int32), ("mode", C.c_int32), ("scheme", C.c_int32)]
 
 
 class StepInfo(C.Structure):
@@ -110,9 +110,10 @@ def check(rc: int):
 
 
 def params(g=9.81, h_tol=1e-4, h_des=1e-8, h_ref=1.0, epsilon0=0.0, sigma_min=0.0,
-           sigma_max=0.0, visc=False, limiter=True, mode=0) -> Params:
+           sigma_max=0.0, visc=False, limiter=True, mode=0, scheme=0) -> Params:
+    """scheme: 0 = SchemeMode::es, 1 = SchemeMode::standard (dg_rhs.hpp:14)."""
     return Params(g, h_tol, h_des, h_ref, epsilon0, sigma_min, sigma_max, int(visc),
-                  int(limiter), mode, 0)
+                  int(limiter), mode, scheme)
 
 
 NODE_ARRAYS = ("x", "y", "x_xi", "x_eta", "y_xi", "y_eta", "jac", "b",

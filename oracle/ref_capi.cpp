@@ -44,7 +44,7 @@ RunConfig make_cfg(const Mesh& m, const swdg_params* p) {
   c.visc.sigma_min = p->sigma_min;
   c.visc.sigma_max = p->sigma_max;
   c.limiter_enabled = p->limiter_enabled != 0;
-  c.mode = SchemeMode::es;
+  c.mode = p->scheme == 1 ? SchemeMode::standard : SchemeMode::es;
   return c;
 }
 

@@ -73,6 +73,45 @@ __device__ void es_flux(double hm, double hum, double hvm, double hp, double hup
   f2 = ny * a1 + nx * a2;
 }
 
+// phys::physical_flux (physics.hpp:39-45)
+__device__ __forceinline__ void phys_flux(double h, double hu, double hv, double g,
+                                          double h_des, double* fx, double* fy) {
+  double u, v;
+  velocity(h, hu, hv, h_des, u, v);
+  const double pr = 0.5 * g * h * h;
+  fx[0] = h * u;
+  fx[1] = h * u * u + pr;
+  fx[2] = h * u * v;
+  fy[0] = h * v;
+  fy[1] = h * u * v;
+  fy[2] = h * v * v + pr;
+}
+
+// fluxes::llf_surface_flux (fluxes.hpp:192-202) with phys::max_wave_speed
+// (physics.hpp:101-112): central flux minus (lambda_max / 2) [[w]]
+__device__ void llf_flux(double hm, double hum, double hvm, double hp, double hup, double hvp,
+                         double nx, double ny, double g, double h_des, double& f0, double& f1,
+                         double& f2) {
+  double fxm[3], fym[3], fxp[3], fyp[3];
+  phys_flux(hm, hum, hvm, g, h_des, fxm, fym);
+  phys_flux(hp, hup, hvp, g, h_des, fxp, fyp);
+  double um, vm, up, vp;
+  velocity(hm, hum, hvm, h_des, um, vm);
+  velocity(hp, hup, hvp, h_des, up, vp);
+  const double unm = nx * um + ny * vm, unp = nx * up + ny * vp;
+  const double cm = sqrt(g * smax(hm, 0.0)), cp = sqrt(g * smax(hp, 0.0));
+  const double lmax = smax(fabs(unm) + cm, fabs(unp) + cp);
+  const double wm[3] = {hm, hum, hvm}, wp[3] = {hp, hup, hvp};
+  double f[3];
+  for (int c = 0; c < 3; ++c) {
+    f[c] = 0.5 * (nx * fxm[c] + ny * fym[c] + nx * fxp[c] + ny * fyp[c]);
+    f[c] -= 0.5 * lmax * (wp[c] - wm[c]);
+  }
+  f0 = f[0];
+  f1 = f[1];
+  f2 = f[2];
+}
+
 // Face visiting order at a node: up to two faces sorted by global ordinal.
 // `minus_first` picks the side order inside one FaceInfo (surface_terms and
 // viscous_lhs scatter minus then plus; br1_gradients plus then minus).
@@ -267,9 +306,28 @@ __global__ void k_rhs_stage(Mesh M, Phys P, StageArgs A) {
   double un, vn;
   velocity(hn, hun, hvn, h_des, un, vn);
 
-  // split_volume_element (dg_rhs.hpp:23-71) with volume_flux_pair (fluxes.hpp:21-39)
+  // split_volume_element (dg_rhs.hpp:23-71) with volume_flux_pair (fluxes.hpp:21-39),
+  // or standard_volume_element (dg_rhs.hpp:75-117): pointwise contravariant
+  // fluxes (recomputed per partner node: bitwise the reference's ft/gt) and D
   double ah = 0.0, ahu = 0.0, ahv = 0.0;
-  for (int dir = 0; dir < 2; ++dir)
+  if (P.standard) {
+    for (int m = 0; m < n1; ++m) {
+      const double di = M.D[i * n1 + m], dj = M.D[j * n1 + m];
+      const long long qx = base + m * n1 + j, qe = base + i * n1 + m;
+      double fx[3], fy[3], ex[3], ey[3];
+      phys_flux(h[qx], hu[qx], hv[qx], g, h_des, fx, fy);
+      phys_flux(h[qe], hu[qe], hv[qe], g, h_des, ex, ey);
+      double ft[3], gt[3];
+      for (int c = 0; c < 3; ++c) {
+        ft[c] = M.ye[qx] * fx[c] - M.xe[qx] * fy[c];
+        gt[c] = M.xx[qe] * ey[c] - M.yx[qe] * ex[c];
+      }
+      ah += di * ft[0] + dj * gt[0];
+      ahu += di * ft[1] + dj * gt[1];
+      ahv += di * ft[2] + dj * gt[2];
+    }
+  }
+  for (int dir = 0; dir < (P.standard ? 0 : 2); ++dir)
     for (int m = 0; m < n1; ++m) {
       const long long q = dir == 0 ? base + m * n1 + j : base + i * n1 + m;
       const double hq = h[q], huq = hu[q], hvq = hv[q];
@@ -335,7 +393,7 @@ __global__ void k_rhs_stage(Mesh M, Phys P, StageArgs A) {
     for (int q = 0; q < nf.n; ++q) {
       const int face = nf.face[q], t = nf.t[q];
       const int4 ef = M.ef[e * 4 + face];
-      double f0, f1, f2, js;
+      double f0, f1, f2, js, snx, sny;
       if (ef.y & EF_WALL) {
         const long long fi = ((long long)e * 4 + face) * n1 + t;
         const double nx = M.fnx[fi], ny = M.fny[fi];
@@ -344,20 +402,42 @@ __global__ void k_rhs_stage(Mesh M, Phys P, StageArgs A) {
         const double mn = hun * nx + hvn * ny;
         const double hup = hun - 2.0 * mn * nx, hvp = hvn - 2.0 * mn * ny;
         const double bn = M.b[n];
-        es_flux(hn, hun, hvn, hn, hup, hvp, bn, bn, nx, ny, g, h_des, f0, f1, f2);
+        if (P.standard)
+          llf_flux(hn, hun, hvn, hn, hup, hvp, nx, ny, g, h_des, f0, f1, f2);
+        else
+          es_flux(hn, hun, hvn, hn, hup, hvp, bn, bn, nx, ny, g, h_des, f0, f1, f2);
+        snx = nx;
+        sny = ny;
       } else {
         long long nb, fi;
         partner_of(M, e, face, t, ef, nb, fi);
         const double nx = M.fnx[fi], ny = M.fny[fi];
         js = M.fjs[fi];
-        if (ef.y & EF_MINUS)
+        snx = nx;
+        sny = ny;
+        if (P.standard) {
+          if (ef.y & EF_MINUS)
+            llf_flux(hn, hun, hvn, h[nb], hu[nb], hv[nb], nx, ny, g, h_des, f0, f1, f2);
+          else
+            llf_flux(h[nb], hu[nb], hv[nb], hn, hun, hvn, nx, ny, g, h_des, f0, f1, f2);
+        } else if (ef.y & EF_MINUS) {
           es_flux(hn, hun, hvn, h[nb], hu[nb], hv[nb], M.b[n], M.b[nb], nx, ny, g, h_des, f0,
                   f1, f2);
-        else
+        } else {
           es_flux(h[nb], hu[nb], hv[nb], hn, hun, hvn, M.b[nb], M.b[n], nx, ny, g, h_des, f0,
                   f1, f2);
+        }
       }
-      const double c0 = js * f0, c1 = js * f1, c2 = js * f2;
+      double c0 = js * f0, c1 = js * f1, c2 = js * f2;
+      if (P.standard) {
+        // strong form: minus the node's own normal physical flux (dg_rhs.hpp:228-246;
+        // the plus side's exterior trace is its own state)
+        double fx[3], fy[3];
+        phys_flux(hn, hun, hvn, g, h_des, fx, fy);
+        c0 -= js * (snx * fx[0] + sny * fy[0]);
+        c1 -= js * (snx * fx[1] + sny * fy[1]);
+        c2 -= js * (snx * fx[2] + sny * fy[2]);
+      }
       if (ef.y & EF_MINUS) {
         rh += c0 / M.w0;
         rhu += c1 / M.w0;

@@ -40,6 +40,21 @@
 
 #include "fast_common.cuh"
 
+// resident half-line CTAs per SM the register allocation is compiled for
+// (__launch_bounds__ min blocks), per N+1; the -D overrides are for A/B builds
+#ifndef SWDG_HL_BLOCKMIN
+#define SWDG_HL_BLOCKMIN 0  // half-line: min-height key reduced per CTA (1) or per element (0)
+#endif
+#ifndef SWDG_HL_MB5
+#define SWDG_HL_MB5 4
+#endif
+#ifndef SWDG_HL_MB6
+#define SWDG_HL_MB6 4
+#endif
+#ifndef SWDG_HL_MB7
+#define SWDG_HL_MB7 4
+#endif
+
 namespace swdg_dev {
 
 namespace {
@@ -137,6 +152,7 @@ __global__ void __launch_bounds__(Plan<N1>::THREADS, 1)
   auto idx = [&](int k) { return xi ? k * N1 + li : li * N1 + k; };
 
   __shared__ int s_next;  // the next group, claimed by thread 0
+  unsigned long long kmin = ~0ull;  // min height key of this thread's elements
   for (int grp = blockIdx.x; grp < ngroups; grp = s_next) {
     const int e0 = M.e_lo + grp * E, ne = min(E, M.n_owned - e0);
     const bool active = el < ne;
@@ -811,11 +827,20 @@ __device__ __forceinline__ void hl_node_phase_t(double* sm, const Mesh& M, const
   }
 }
 
+// resident CTAs the register allocation must allow: 4 (<= 128 registers) for
+// N+1 = 5..7 (measured on B200, 1M elements: N=4 1.352 -> 1.132, N=5 1.635 ->
+// 1.609, N=6 2.438 -> 2.374 ms/stage; at N+1 = 8 the 128-register cap spills 88
+// bytes and runs 11% slower), 3 (<= 168 registers) up to N+1 = 10 (measured 22%
+// faster at N+1 = 10); above, a 168-register cap spills (N+1 = 11, 13..16)
+// The viscous variant keeps 3 at N+1 = 6, 7 (measured: N=5 3.566 vs 3.721, N=6
+// 5.180 vs 5.547 ms/stage with 4) and takes 4 at N+1 = 5 (2.777 -> 2.559).
+__host__ __device__ constexpr int hl_min_blocks(int n1, bool visc) {
+  return n1 == 5 ? SWDG_HL_MB5 : (n1 == 6 && !visc) ? SWDG_HL_MB6
+         : (n1 == 7 && !visc) ? SWDG_HL_MB7 : n1 <= 10 ? 3 : 1;
+}
+
 template <int N1, bool FORCE, bool VISC>
-// resident CTAs the register allocation must allow: 3 (<= 168 registers) where
-// that costs no spills (N+1 <= 10: measured 22% faster at N+1 = 10);
-// above, a 168-register cap spills (N+1 = 11, 13..16) and runs slower
-__global__ void __launch_bounds__(HL<N1, VISC>::THREADS, (N1 <= 10 ? 3 : 1))
+__global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC))
     k_stage_hl(Mesh M, Phys Ph, StageArgs A, Flags* F) {
   using P = HL<N1, VISC>;
   using O = Ops<N1>;
@@ -851,6 +876,7 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, (N1 <= 10 ? 3 : 1))
   auto pidx = [&](int k) { return xi ? k * PAD + li : li * PAD + k; };
 
   __shared__ int s_next;  // the next group, claimed by thread 0
+  unsigned long long kmin = ~0ull;  // min height key of this thread's elements
   for (int grp = blockIdx.x; grp < ngroups; grp = s_next, buf = P::DB ? buf ^ 1 : 0) {
     const int e0 = M.e_lo + grp * P::E, ne = min(P::E, M.n_owned - e0);
     const bool active = line_ok && el < ne;
@@ -1272,13 +1298,22 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, (N1 <= 10 ? 3 : 1))
           // the limited heights are a monotone map of the unlimited ones: the
           // element's minimum after limiting is the map of its minimum
           const double m = theta < 1.0 ? smax(theta * (mmin - avg0) + avg0, 0.0) : mmin;
-          atomicMin(&F->min_h_key, order_key(m));
+          if (SWDG_HL_BLOCKMIN) {
+            const unsigned long long k = order_key(m);
+            kmin = k < kmin ? k : kmin;
+          } else {
+            atomicMin(&F->min_h_key, order_key(m));
+          }
           if (theta < 1.0) atomicAdd(&F->n_limited, 1);
         }
       }
     }
   }
   cp_async_wait_all();
+  if (SWDG_HL_BLOCKMIN) {  // one atomic per CTA for the whole launch
+    const unsigned long long bmin = block_min_key(kmin);
+    if (tid == 0 && bmin != ~0ull) atomicMin(&F->min_h_key, bmin);
+  }
 }
 
 // ===========================================================================
@@ -1748,6 +1783,343 @@ static void launch_elem(const Mesh& M, const Phys& P, const StageArgs& A, Flags*
   k_stage_elem<N1, FORCE><<<(M.n_owned - M.e_lo + 127) / 128, 128, 0, st>>>(M, P, A, F);
 }
 
+// Node-per-thread kernel for the smallest degrees (N+1 <= 4, inviscid).  A warp
+// holds EPW = 32 / (N+1)^2 whole elements, lane = one node: every load and store
+// is one coalesced 8-byte-per-lane stream (the element-per-thread kernel strides
+// its lanes by a whole element and runs out of registers for loads in flight).
+// The line partners of a node are the lanes of its xi- and eta-line: their
+// state, velocity and metrics arrive by warp shuffles, partner k of node i being
+// node (i + k) mod (N+1), so no lane idles and no shared memory or barrier is
+// needed.  Each lane evaluates its own row of the ordered pairs (the flux is
+// symmetric, so the value equals the element kernel's), then the interface
+// fluxes of its (at most two) faces — slot s = the node's s-th face, so every
+// lane runs the same code — the node update, and the element mean / limiter by
+// a segmented shuffle reduction (fixed tree, broadcast from the element's first
+// lane: every lane of an element sees the same bits).  Persistent grid-stride
+// warps; one flag atomic per block.
+template <int N1>
+__device__ __forceinline__ double seg_sum(double x, int q, int base_lane) {
+  constexpr int NP = N1 * N1;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    if (off >= NP) continue;
+    const double o = __shfl_down_sync(0xffffffffu, x, off);
+    if (q + off < NP) x += o;
+  }
+  return __shfl_sync(0xffffffffu, x, base_lane);
+}
+template <int N1>
+__device__ __forceinline__ double seg_min(double x, int q, int base_lane) {
+  constexpr int NP = N1 * N1;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    if (off >= NP) continue;
+    const double o = __shfl_down_sync(0xffffffffu, x, off);
+    if (q + off < NP) x = smin(x, o);
+  }
+  return __shfl_sync(0xffffffffu, x, base_lane);
+}
+
+// shared-memory plan of the node-per-thread kernel (doubles): STAGES groups of
+// G = 8 warps x EPW elements in flight, each as 14 node fields of G (N+1)^2
+// doubles (+ slack for a one-double shift when the group's first node is at an
+// odd index: bulk copies need 16-byte aligned sources) and the group's
+// element-face records
+template <int N1>
+struct NodePlan {
+  static constexpr int NP = N1 * N1, EPW = 32 / NP, WARPS = 8, THREADS = 32 * WARPS;
+  static constexpr int G = WARPS * EPW, GN = G * NP, GNS = (GN + 3) & ~1;
+  enum { F_H, F_HU, F_HV, F_YE, F_XE, F_YX, F_XX, F_B, F_JAC, F_SX, F_SY, F_WH, F_WHU, F_WHV,
+         kFields };
+  static constexpr int EF = kFields * GNS;     // int4 [G][4] = 2 doubles each
+  static constexpr int STAGE = EF + G * 4 * 2;  // doubles per stage
+  static constexpr int STAGES = 3;
+  static constexpr int BAR = STAGES * STAGE;    // STAGES mbarriers
+  static constexpr int GIDX = BAR + STAGES;     // STAGES group ids (ints)
+  static constexpr int CNT = GIDX + STAGES;      // STAGES warp-done counters (ints)
+  static constexpr int TOTAL = CNT + STAGES;
+  static constexpr size_t bytes = TOTAL * sizeof(double);
+};
+
+// thread 0: stream group g's node fields and face records into stage buffer sb
+template <int N1>
+__device__ __forceinline__ void node_issue(double* sb, uint64_t* bar, const Mesh& M,
+                                           const StageArgs& A, int g, bool comb) {
+  using P = NodePlan<N1>;
+  const int e0 = M.e_lo + g * P::G, ne = min(P::G, M.n_owned - e0);
+  const long long n0 = (long long)e0 * P::NP;
+  const int shift = (int)(n0 & 1);
+  const uint32_t fb = round16((size_t)(ne * P::NP + shift) * sizeof(double));
+  const uint32_t eb = (uint32_t)(ne * 4 * sizeof(int4));
+  const int nf = comb ? P::kFields : P::F_WH;
+  mbar_expect_tx(bar, nf * fb + eb);
+  const double* src[P::kFields] = {A.in.h, A.in.hu, A.in.hv, M.ye, M.xe, M.yx, M.xx,
+                                   M.b, M.jac, M.sx, M.sy, A.wn.h, A.wn.hu, A.wn.hv};
+#pragma unroll
+  for (int f = 0; f < P::kFields; ++f)
+    if (f < nf) bulk_g2s(sb + f * P::GNS, src[f] + n0 - shift, fb, bar);
+  bulk_g2s(sb + P::EF, M.ef + (long long)e0 * 4, eb, bar);
+}
+
+template <int N1, bool FORCE>
+__global__ void __launch_bounds__(256, 2) k_stage_node(Mesh M, Phys Ph, StageArgs A, Flags* F) {
+  using P = NodePlan<N1>;
+  constexpr int NP = N1 * N1, EPW = P::EPW;
+  extern __shared__ __align__(16) double sm[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + P::BAR);
+  int* gidx = reinterpret_cast<int*>(sm + P::GIDX);
+  int* cnt = reinterpret_cast<int*>(sm + P::CNT);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int le = lane / NP, q = lane - le * NP, i = q / N1, j = q - i * N1;
+  const int base_lane = le * NP;
+  const bool lane_ok = le < EPW;
+  // this lane's D~ rows, rotated: slot k holds column (i + k) mod (N+1) (xi
+  // line) and (j + k) mod (N+1) (eta line).  The pair sums accumulate D~ F and
+  // are scaled by 1/4, 1/8 afterwards: power-of-two scaling commutes with
+  // rounding, so this is bitwise (D~/4) F summed.
+  double dx[N1], de[N1];
+#pragma unroll
+  for (int k = 0; k < N1; ++k) {
+    dx[k] = __ldg(M.Dt + i * N1 + (i + k) % N1);
+    de[k] = __ldg(M.Dt + j * N1 + (j + k) % N1);
+  }
+  const double wij = __ldg(M.w + i) * __ldg(M.w + j);
+  const double g = Ph.g, h_des = Ph.h_des, inv2g = 1.0 / (2.0 * g), iw0 = 1.0 / M.w0;
+  const double g2 = 2.0 * g;
+  const bool comb = A.stage > 0 && A.update;
+  int fid0 = -1, fid1 = -1;  // smallest and second-smallest face id touching the node
+#pragma unroll
+  for (int f = 3; f >= 0; --f) {
+    const bool on = f == 0 ? j == 0 : f == 1 ? i == N1 - 1 : f == 2 ? j == N1 - 1 : i == 0;
+    if (on && lane_ok) {
+      fid1 = fid0;
+      fid0 = f;
+    }
+  }
+  const int ngroups = (M.n_owned - M.e_lo + P::G - 1) / P::G;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < P::STAGES; ++s) {
+      mbar_init(&bars[s], 1);
+      cnt[s] = 0;
+    }
+    fence_mbar_init();
+    int grp = blockIdx.x;
+    for (int s = 0; s < P::STAGES; ++s) {
+      gidx[s] = grp < ngroups ? grp : -1;
+      if (grp < ngroups) node_issue<N1>(sm + s * P::STAGE, &bars[s], M, A, grp, comb);
+      else mbar_arrive(&bars[s]);
+      if (s + 1 < P::STAGES) grp = grp < ngroups ? next_group(A.gctr, grp) : ngroups;
+    }
+  }
+  __syncthreads();
+  unsigned long long kmin = ~0ull;
+  int nlim = 0;
+  for (int it = 0;; ++it) {
+    // no CTA barrier in the loop: the last warp to finish a stage refills it
+    // (or, past the last group, completes its phase with gidx = -1); a warp reads
+    // the group id only after the phase completed (mbarrier release/acquire)
+    const int s = it % P::STAGES;
+    mbar_wait(&bars[s], (it / P::STAGES) & 1);
+    const int grp = *(volatile int*)&gidx[s];
+    if (grp < 0) break;  // CTA-uniform
+    const double* sb = sm + s * P::STAGE;
+    const int e0 = M.e_lo + grp * P::G;
+    const int shift = (int)(((long long)e0 * NP) & 1);
+    const int el = warp * EPW + le;  // element within the group
+    const int e = e0 + el;
+    const bool active = lane_ok && e < M.n_owned;
+    const int ln = (lane_ok ? el * NP + q : 0) + shift;
+    const long long n = (long long)e * NP + q;
+    double h = sb[P::F_H * P::GNS + ln], hu = sb[P::F_HU * P::GNS + ln],
+           hv = sb[P::F_HV * P::GNS + ln];
+    const double ye = sb[P::F_YE * P::GNS + ln], xe = sb[P::F_XE * P::GNS + ln],
+                 yx = sb[P::F_YX * P::GNS + ln], xx = sb[P::F_XX * P::GNS + ln];
+    const double bo = sb[P::F_B * P::GNS + ln];
+    double u, v;
+    vel(h, hu, hv, h_des, u, v);
+    double r0 = 0.0, r1 = 0.0, r2 = 0.0;
+    // volume: xi line (b, j), metrics (y_eta, x_eta); eta line (i, b), -(y_xi, x_xi)
+#pragma unroll
+    for (int dir = 0; dir < 2; ++dir) {
+      const double Aa = dir == 0 ? ye : -yx, Ba = dir == 0 ? xe : -xx;
+#pragma unroll
+      for (int k = 0; k < N1; ++k) {
+        double hb = h, ub = u, vb = v, hub = hu, hvb = hv, Ab = Aa, Bb = Ba;
+        if (k > 0) {
+          const int src = dir == 0 ? base_lane + ((i + k) % N1) * N1 + j
+                                   : base_lane + i * N1 + (j + k) % N1;
+          hb = __shfl_sync(0xffffffffu, h, src);
+          ub = __shfl_sync(0xffffffffu, u, src);
+          vb = __shfl_sync(0xffffffffu, v, src);
+          hub = __shfl_sync(0xffffffffu, hu, src);
+          hvb = __shfl_sync(0xffffffffu, hv, src);
+          Ab = __shfl_sync(0xffffffffu, Aa, src);
+          Bb = __shfl_sync(0xffffffffu, Ba, src);
+        }
+        double F0, T1, T2;
+        pair_flux(h, u, v, hu, hv, Aa, Ba, hb, ub, vb, hub, hvb, Ab, Bb, g2, F0, T1, T2);
+        const double c = dir == 0 ? dx[k] : de[k];
+        r0 += c * F0;
+        r1 += c * T1;
+        r2 += c * T2;
+      }
+    }
+    r0 *= 0.25;
+    r1 *= 0.125;
+    r2 *= 0.125;
+    // interface fluxes: slot s is the node's s-th face
+    const double co = wave_c(g, h);
+    const int4* efs = reinterpret_cast<const int4*>(sb + P::EF);
+#pragma unroll
+    for (int sl = 0; sl < 2; ++sl) {
+      const int face = sl == 0 ? fid0 : fid1;
+      if (!active || face < 0) continue;
+      const int t = (face == 0 || face == 2) ? i : j;
+      const int4 ef = efs[el * 4 + face];
+      if (!(ef.y & EF_PRESENT)) continue;
+      const int nf = ef.y & EF_NBR_FACE_MASK;
+      const bool minus = ef.y & EF_MINUS, wall = minus && (ef.y & EF_WALL);
+      const bool ew = face == 1 || face == 3;
+      double hn = h, hun = hu, hvn = hv, bn = bo, m0, m1;
+      long long nb = 0;
+      if (!wall) {
+        const int tp = (ef.y & EF_REVERSED) ? N1 - 1 - t : t;
+        nb = (long long)ef.x * NP + face_node(N1, nf, tp);
+        hn = __ldg(A.in.h + nb);
+        hun = __ldg(A.in.hu + nb);
+        hvn = __ldg(A.in.hv + nb);
+        bn = __ldg(M.b + nb);
+      }
+      if (minus) {
+        m0 = ew ? ye : yx;
+        m1 = ew ? xe : xx;
+      } else {
+        const bool new_ = nf == 1 || nf == 3;
+        m0 = __ldg((new_ ? M.ye : M.yx) + nb);
+        m1 = __ldg((new_ ? M.xe : M.xx) + nb);
+      }
+      double nx, ny, js;
+      face_normal(minus ? face : nf, m0, m1, nx, ny, js);
+      if (wall) {  // exterior_state (mesh.hpp:382-386)
+        const double mn = hu * nx + hv * ny;
+        hun = hu - 2.0 * mn * nx;
+        hvn = hv - 2.0 * mn * ny;
+      }
+      double un, vn;
+      vel(hn, hun, hvn, h_des, un, vn);
+      const double cn = wave_c(g, hn);
+      double f0, f1, f2;
+      if (minus)
+        es_flux_pre(h, u, v, co, hn, un, vn, cn, bo, bn, nx, ny, g, inv2g, f0, f1, f2);
+      else
+        es_flux_pre(hn, un, vn, cn, h, u, v, co, bn, bo, nx, ny, g, inv2g, f0, f1, f2);
+      const double c = (minus ? 1.0 : -1.0) * js * iw0;
+      r0 += c * f0;
+      r1 += c * f1;
+      r2 += c * f2;
+    }
+    // node update (assemble_rhs tail, axpy, SSPRK3 combination)
+    const double jac = sb[P::F_JAC * P::GNS + ln];
+    {
+      const double ij = -frcp(jac), hg2 = 0.5 * g * h;
+      double rh = r0 * ij;
+      double rhu = (r1 + hg2 * sb[P::F_SX * P::GNS + ln]) * ij;
+      double rhv = (r2 + hg2 * sb[P::F_SY * P::GNS + ln]) * ij;
+      if (FORCE && active) {
+        rh += A.fh[n];
+        rhu += A.fhu[n];
+        rhv += A.fhv[n];
+      }
+      if (A.rhs.h && active) {
+        A.rhs.h[n] = rh;
+        A.rhs.hu[n] = rhu;
+        A.rhs.hv[n] = rhv;
+      }
+      h = h + A.dt * rh;
+      hu = hu + A.dt * rhu;
+      hv = hv + A.dt * rhv;
+      if (comb) {
+        h = A.ca * sb[P::F_WH * P::GNS + ln] + A.cb * h;
+        hu = A.ca * sb[P::F_WHU * P::GNS + ln] + A.cb * hu;
+        hv = A.ca * sb[P::F_WHV * P::GNS + ln] + A.cb * hv;
+      }
+    }
+    if (A.update) {  // kernel-uniform
+      // element mean and minimum (limiter.hpp:24-37, 43-84)
+      const double wq = wij * jac;
+      const double area = seg_sum<N1>(wq, q, base_lane);
+      const double a0 = seg_sum<N1>(wq * h, q, base_lane);
+      const double a1 = seg_sum<N1>(wq * hu, q, base_lane);
+      const double a2 = seg_sum<N1>(wq * hv, q, base_lane);
+      const double mmin = seg_min<N1>(h, q, base_lane);
+      bool lim = active;
+      const double inv = frcp(area);
+      const double avg0 = inv * a0, avg1 = inv * a1, avg2 = inv * a2;
+      if (lim && avg0 < 0.0) {
+        if (q == 0) {
+          atomicExch(&F->reject, 1);
+          if (!Ph.limiter) atomicExch(&F->abort, 1);
+        }
+        lim = false;
+      }
+      double theta = 1.0;
+      if (lim && Ph.limiter && mmin < 0.0) {
+        const double denom = avg0 - mmin;
+        theta = denom < 1e-14 ? 1.0 : smin(1.0, avg0 / denom);
+      }
+      if (lim && !Ph.limiter && mmin < 0.0 && q == 0) atomicExch(&F->abort, 1);
+      if (lim) {
+        if (theta < 1.0) {
+          h = smax(theta * (h - avg0) + avg0, 0.0);
+          hu = theta * (hu - avg1) + avg1;
+          hv = theta * (hv - avg2) + avg2;
+          nlim += q == 0;
+        }
+        if (Ph.limiter && h < Ph.h_tol) {
+          hu = 0.0;
+          hv = 0.0;
+        }
+        A.out.h[n] = h;
+        A.out.hu[n] = hu;
+        A.out.hv[n] = hv;
+        const unsigned long long key = order_key(h);
+        kmin = key < kmin ? key : kmin;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd(&cnt[s], 1) == P::WARPS - 1) {  // stage s consumed by every warp
+        cnt[s] = 0;
+        const int nx_ = next_group(A.gctr, grp);
+        gidx[s] = nx_ < ngroups ? nx_ : -1;
+        if (nx_ < ngroups) {
+          fence_proxy_async();
+          node_issue<N1>(sm + s * P::STAGE, &bars[s], M, A, nx_, comb);
+        } else {
+          mbar_arrive(&bars[s]);
+        }
+      }
+    }
+  }
+  // one atomic per block for the min height, per warp (rare) for the count
+  const unsigned long long bmin = block_min_key(kmin);
+  if (threadIdx.x == 0 && bmin != ~0ull) atomicMin(&F->min_h_key, bmin);
+  const int wl = __reduce_add_sync(0xffffffffu, nlim);
+  if (lane == 0 && wl) atomicAdd(&F->n_limited, wl);
+}
+
+template <int N1, bool FORCE>
+static void launch_node(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
+                        cudaStream_t st) {
+  using PL = NodePlan<N1>;
+  static int cache = 0;
+  auto kern = k_stage_node<N1, FORCE>;
+  const int groups = (M.n_owned - M.e_lo + PL::G - 1) / PL::G;
+  const int grid = grid_for(kern, PL::THREADS, PL::bytes, groups, cache);
+  if (grid > 0) kern<<<grid, PL::THREADS, PL::bytes, st>>>(M, P, A, F);
+}
+
 #include "visc_lines.cuh"
 
 // geometry-only split-source coefficients (dg_rhs.hpp:159-176), one thread per node
@@ -1836,7 +2208,7 @@ static int variant_override() {
   static int v = -1;
   if (v < 0) {
     const char* s = getenv("SWDG_FAST_VARIANT");  // "elem" / "full" / "half" (experiments)
-    v = !s ? 0 : (s[0] == 'f' ? 1 : (s[0] == 'h' ? 2 : (s[0] == 'e' ? 3 : (s[0] == 'p' ? 4 : 0))));
+    v = !s ? 0 : (s[0] == 'f' ? 1 : (s[0] == 'h' ? 2 : (s[0] == 'e' ? 3 : (s[0] == 'p' ? 4 : (s[0] == 'n' ? 5 : 0)))));
   }
   return v;
 }
@@ -1851,18 +2223,28 @@ static void launch_n(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
       return;
     }
   }
-  // inviscid kernel choice: element-per-thread (N+1 <= 3), full-line (N+1 = 4),
-  // half-line (N+1 >= 5); SWDG_FAST_VARIANT=elem/full/half/pl overrides where the
-  // variant exists for this degree.  Measured on B200 (1M elements,
-  // profiles/r01_sweep_variants.txt): full-line 0.93 vs half-line 1.65 ms/stage at
-  // N+1 = 4, half-line 1.355 vs full-line 1.378 at N+1 = 5
-  int v = N1 <= 3 ? 3 : (N1 == 4 ? 1 : 2);
+  // inviscid kernel choice: element-per-thread (N+1 <= 3), node-per-thread (N+1 =
+  // 4), half-line (N+1 >= 5); SWDG_FAST_VARIANT=elem/full/half/pl/node overrides
+  // where the variant exists for this degree.  Measured on B200 (1M elements,
+  // profiles/r01_sweep_variants.txt, r01_node_variants.txt): node 0.853-0.863 vs
+  // full-line 0.926 vs half-line 1.65 ms/stage at N+1 = 4; element 0.185 / 0.483
+  // vs node 0.197 / 0.552 at N+1 = 2 / 3; half-line 1.355 vs full-line 1.378 at
+  // N+1 = 5
+  int v = N1 <= 3 ? 3 : (N1 == 4 ? 5 : 2);
   const int ov = variant_override();
+  if (ov == 5 && N1 <= 4) v = 5;
   if (ov == 3 && N1 <= 3) v = 3;
   if (ov == 1 && N1 <= 8) v = 1;
   if (ov == 2 && N1 >= 3) v = 2;
   if (ov == 4) v = 4;
   if (v == 4 && launch_pl_stage(M, P, A, F, st)) return;
+  if constexpr (N1 <= 4) {
+    if (v == 5) {
+      if (A.fh) launch_node<N1, true>(M, P, A, F, st);
+      else launch_node<N1, false>(M, P, A, F, st);
+      return;
+    }
+  }
   if constexpr (N1 <= 3) {
     if (v == 3) {
       if (A.fh) launch_elem<N1, true>(M, P, A, F, st);

@@ -24,6 +24,7 @@ struct Phys {
   double g, h_tol, h_des, h_ref;
   double epsilon0, sigma_min, sigma_max;
   int visc, limiter;
+  int standard;  // SchemeMode::standard (exact kernels only)
 };
 
 struct Mesh {

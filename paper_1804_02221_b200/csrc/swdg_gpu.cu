@@ -262,6 +262,8 @@ void validate_params(const swdg_params* p, int N) {
   if (p->visc_enabled && p->epsilon0 < 0.0) throw InputError{"viscosity: epsilon0 must be >= 0"};
   if (p->mode != SWDG_MODE_EXACT && p->mode != SWDG_MODE_FAST)
     throw InputError{"unknown arithmetic mode"};
+  if (p->scheme != SWDG_SCHEME_ES && p->scheme != SWDG_SCHEME_STANDARD)
+    throw InputError{"unknown scheme"};
 }
 
 // element-face connectivity from MeshTopology::faces (mesh.hpp:46-54)
@@ -402,8 +404,15 @@ swdg_gpu* new_context(const swdg_params* p, int device) {
   auto* c = new swdg_gpu;
   c->device = device;
   c->params = *p;
+  // the standard scheme has no artificial viscosity (evaluate_rhs
+  // timeloop.hpp:178 adds it for SchemeMode::es only) and runs the exact kernels
+  if (p->scheme == SWDG_SCHEME_STANDARD) {
+    c->params.visc_enabled = 0;
+    c->params.mode = SWDG_MODE_EXACT;
+  }
   c->phys = Phys{p->g, p->h_tol, p->h_des, p->h_ref, p->epsilon0, p->sigma_min,
-                 p->sigma_max, p->visc_enabled, p->limiter_enabled};
+                 p->sigma_max, c->params.visc_enabled, p->limiter_enabled,
+                 p->scheme == SWDG_SCHEME_STANDARD ? 1 : 0};
   return c;
 }
 

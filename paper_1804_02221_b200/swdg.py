@@ -24,6 +24,7 @@ _dp = C.POINTER(C.c_double)
 
 SWDG_OK, SWDG_ERR_CUDA, SWDG_ERR_INPUT, SWDG_ERR_ABORT = 0, 1, 2, 3
 MODE_EXACT, MODE_FAST = 0, 1
+SCHEME_ES, SCHEME_STANDARD = 0, 1  # SchemeMode (dg_rhs.hpp:14)
 TAG_INTERIOR, TAG_WALL = 0, 1
 
 
@@ -59,7 +60,7 @@ class ParamsC(C.Structure):
     _fields_ = [("g", C.c_double), ("h_tol", C.c_double), ("h_des", C.c_double),
                 ("h_ref", C.c_double), ("epsilon0", C.c_double), ("sigma_min", C.c_double),
                 ("sigma_max", C.c_double), ("visc_enabled", C.c_int32),
-                ("limiter_enabled", C.c_int32), ("mode", C.c_int32), ("reserved", C.c_int32)]
+                ("limiter_enabled", C.c_int32), ("mode", C.c_int32), ("scheme", C.c_int32)]
 
 
 class StepInfoC(C.Structure):
@@ -214,11 +215,15 @@ class RunConfig:
     visc: ViscosityConfig = field(default_factory=ViscosityConfig)
     limiter_enabled: bool = True
     mode: int = MODE_EXACT
+    # SchemeMode (dg_rhs.hpp:14): SCHEME_ES, or SCHEME_STANDARD (standard DGSEM + LLF,
+    # no artificial viscosity, always on the exact kernels)
+    scheme: int = 0
 
     def c_params(self) -> ParamsC:
         return ParamsC(self.phys.g, self.phys.h_tol, self.phys.h_des, self.phys.h_ref,
                        self.visc.epsilon0, self.visc.sigma_min, self.visc.sigma_max,
-                       int(self.visc.enabled), int(self.limiter_enabled), int(self.mode), 0)
+                       int(self.visc.enabled), int(self.limiter_enabled), int(self.mode),
+                       int(self.scheme))
 
 
 # ---------------------------------------------------------------- mesh / state
