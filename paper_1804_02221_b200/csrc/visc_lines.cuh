@@ -40,6 +40,13 @@ struct VLP {
   // shared fields [E][N1][PAD]: state and metrics, the first modal pass, and the
   // four BR1 partials of each direction
   enum { H, U, V, YE, XE, YX, XX, TMP, XU1, XU2, XV1, XV2, EU1, EU2, EV1, EV2, kF };
+  // asynchronous (LDGSTS) staging, measured (viscous ms/stage, pre-kernel +
+  // stage): N=10 14.94 -> 13.67, N=12 22.44 -> 20.80; slower at N+1 = 8 (6.24
+  // synchronous vs 6.32-6.37) and N+1 = 5 (2.57 -> 2.80)
+#ifndef VL_ASYNC_MIN
+#define VL_ASYNC_MIN 9
+#endif
+  static constexpr bool kAsync = N1 >= VL_ASYNC_MIN;
   static constexpr int RED = kF * GPAD;             // [E][PMAX][4] shell-energy pieces
   static constexpr int EPS = RED + E * PMAX * 4;
   static constexpr int TOTAL = EPS + E;
@@ -64,7 +71,35 @@ __global__ void __launch_bounds__(VLP<N1>::THREADS)
   const int e = e0 + el;
   const double h_des = Ph.h_des, iw0 = 1.0 / M.w0;
 
-  // neighbour traces at this line's two endpoints, requested first
+  const long long base = (long long)e0 * NP;
+  // this thread's nodes of the final (flux-pair) phase: J prefetched now
+  constexpr int R = (P::E * NP + P::THREADS - 1) / P::THREADS;
+  double jr[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int r = tid + k * P::THREADS;
+    jr[k] = r < ne * NP ? __ldg(M.jac + base + r) : 1.0;
+  }
+  if constexpr (P::kAsync) {
+    // the group's state and metrics go to shared memory by asynchronous 8-byte
+    // copies (LDGSTS), in flight together with the connectivity and neighbour
+    // gathers below (hu, hv land in the x-partial slots, free until the line
+    // phase)
+    for (int r = tid; r < ne * NP; r += P::THREADS) {
+      const int el2 = r / NP, q = r - el2 * NP, i = q / N1, j = q - i * N1;
+      double* d = sm + el2 * P::EPAD + i * PAD + j;
+      const long long n = base + r;
+      cp_async8(d + P::H * GP, S.h + n);
+      cp_async8(d + P::XU1 * GP, S.hu + n);
+      cp_async8(d + P::XU2 * GP, S.hv + n);
+      cp_async8(d + P::YE * GP, M.ye + n);
+      cp_async8(d + P::XE * GP, M.xe + n);
+      cp_async8(d + P::YX * GP, M.yx + n);
+      cp_async8(d + P::XX * GP, M.xx + n);
+    }
+    cp_async_commit();
+  }
+  // neighbour traces at this line's two endpoints
   int fy[2] = {0, 0};
   double nh[2] = {0.0, 0.0}, nhu[2] = {0.0, 0.0}, nhv[2] = {0.0, 0.0};
   if (active) {
@@ -83,22 +118,35 @@ __global__ void __launch_bounds__(VLP<N1>::THREADS)
       }
     }
   }
-  // stage the group's state (+ velocities) and metrics, one thread per node
-  const long long base = (long long)e0 * NP;
-  for (int r = tid; r < ne * NP; r += P::THREADS) {
-    const int el2 = r / NP, q = r - el2 * NP, i = q / N1, j = q - i * N1;
-    double* d = sm + el2 * P::EPAD + i * PAD + j;
-    const long long n = base + r;
-    const double h = S.h[n], hu = S.hu[n], hv = S.hv[n];
-    double u, v;
-    vel(h, hu, hv, h_des, u, v);
-    d[P::H * GP] = h;
-    d[P::U * GP] = u;
-    d[P::V * GP] = v;
-    d[P::YE * GP] = M.ye[n];
-    d[P::XE * GP] = M.xe[n];
-    d[P::YX * GP] = M.yx[n];
-    d[P::XX * GP] = M.xx[n];
+  if constexpr (P::kAsync) {
+    // velocities of the staged state (each thread reads the words its own copies
+    // wrote: no barrier needed before this pass)
+    cp_async_wait_all();
+    for (int r = tid; r < ne * NP; r += P::THREADS) {
+      const int el2 = r / NP, q = r - el2 * NP, i = q / N1, j = q - i * N1;
+      double* d = sm + el2 * P::EPAD + i * PAD + j;
+      double u, v;
+      vel(d[P::H * GP], d[P::XU1 * GP], d[P::XU2 * GP], h_des, u, v);
+      d[P::U * GP] = u;
+      d[P::V * GP] = v;
+    }
+  } else {
+    // stage the group's state (+ velocities) and metrics, one thread per node
+    for (int r = tid; r < ne * NP; r += P::THREADS) {
+      const int el2 = r / NP, q = r - el2 * NP, i = q / N1, j = q - i * N1;
+      double* d = sm + el2 * P::EPAD + i * PAD + j;
+      const long long n = base + r;
+      const double h = S.h[n], hu = S.hu[n], hv = S.hv[n];
+      double u, v;
+      vel(h, hu, hv, h_des, u, v);
+      d[P::H * GP] = h;
+      d[P::U * GP] = u;
+      d[P::V * GP] = v;
+      d[P::YE * GP] = M.ye[n];
+      d[P::XE * GP] = M.xe[n];
+      d[P::YX * GP] = M.yx[n];
+      d[P::XX * GP] = M.xx[n];
+    }
   }
   __syncthreads();
 
@@ -248,11 +296,24 @@ __global__ void __launch_bounds__(VLP<N1>::THREADS)
     }
     sm[P::EPS + el2] = eps;
     eps_out[e0 + el2] = eps;
-    atomicMax(&F->max_eps_key, order_key(eps));
+  }
+  // max eps: one atomic per CTA (E <= 32 elements, all in warp 0); one per
+  // element put 1M same-address atomics into every launch
+  if (tid < 32) {
+    unsigned long long k = tid < ne ? order_key(sm[P::EPS + tid]) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long t = __shfl_xor_sync(0xffffffffu, k, o);
+      k = t > k ? t : k;
+    }
+    if (tid == 0) atomicMax(&F->max_eps_key, k);
   }
   __syncthreads();
   // ---- viscous flux pairs, one thread per node (coalesced)
-  for (int r = tid; r < ne * NP; r += P::THREADS) {
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int r = tid + k * P::THREADS;
+    if (r >= ne * NP) break;
     const int el2 = r / NP, q = r - el2 * NP, i = q / N1, j = q - i * N1;
     const int pq = el2 * P::EPAD + i * PAD + j;
     const long long n = base + r;
@@ -260,7 +321,7 @@ __global__ void __launch_bounds__(VLP<N1>::THREADS)
     const double u2 = sm[P::XU2 * GP + pq] + sm[P::EU2 * GP + pq];
     const double v1 = sm[P::XV1 * GP + pq] + sm[P::EV1 * GP + pq];
     const double v2 = sm[P::XV2 * GP + pq] + sm[P::EV2 * GP + pq];
-    const double he = sm[P::H * GP + pq] * sm[P::EPS + el2] * (1.0 / __ldg(M.jac + n));
+    const double he = sm[P::H * GP + pq] * sm[P::EPS + el2] * (1.0 / jr[k]);
     fvu[n] = he * u1;
     fvv[n] = he * v1;
     gvu[n] = he * u2;
