@@ -42,8 +42,14 @@
 
 // resident half-line CTAs per SM the register allocation is compiled for
 // (__launch_bounds__ min blocks), per N+1; the -D overrides are for A/B builds
+// viscous stages up to this N+1 take the node-per-thread kernel
+#ifndef SWDG_VISC_NODE_MAX
+#define SWDG_VISC_NODE_MAX 3  // measured: N=2 1.224 -> 1.013 ms/stage; N+1 = 4 slower (1.585 -> 1.798)
+#endif
+// half-line: min-height key reduced per CTA (1) or one atomic per element (0);
+// -1 = per degree (hl_blockmin)
 #ifndef SWDG_HL_BLOCKMIN
-#define SWDG_HL_BLOCKMIN 0  // half-line: min-height key reduced per CTA (1) or per element (0)
+#define SWDG_HL_BLOCKMIN -1
 #endif
 #ifndef SWDG_HL_MB5
 #define SWDG_HL_MB5 4
@@ -839,6 +845,15 @@ __host__ __device__ constexpr int hl_min_blocks(int n1, bool visc) {
          : (n1 == 7 && !visc) ? SWDG_HL_MB7 : n1 <= 10 ? 3 : 1;
 }
 
+// One min-height atomic per CTA instead of one per element (1M same-address
+// atomics per launch): viscous N=3 2.08 -> 1.58, N=2 1.29 -> 1.22 ms/stage.
+// Inviscid stays per element: within +-1.5% at N = 4, 5, 7, 10, and the extra
+// register pushed N+1 = 7 (128-register cap) from 48 to 60 B of spills (N=6
+// 2.375 -> 2.520 ms)
+__host__ __device__ constexpr bool hl_blockmin(int n1, bool visc) {
+  return SWDG_HL_BLOCKMIN >= 0 ? SWDG_HL_BLOCKMIN != 0 : visc;
+}
+
 template <int N1, bool FORCE, bool VISC>
 __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC))
     k_stage_hl(Mesh M, Phys Ph, StageArgs A, Flags* F) {
@@ -1298,7 +1313,7 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
           // the limited heights are a monotone map of the unlimited ones: the
           // element's minimum after limiting is the map of its minimum
           const double m = theta < 1.0 ? smax(theta * (mmin - avg0) + avg0, 0.0) : mmin;
-          if (SWDG_HL_BLOCKMIN) {
+          if (hl_blockmin(N1, VISC)) {
             const unsigned long long k = order_key(m);
             kmin = k < kmin ? k : kmin;
           } else {
@@ -1310,7 +1325,7 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
     }
   }
   cp_async_wait_all();
-  if (SWDG_HL_BLOCKMIN) {  // one atomic per CTA for the whole launch
+  if (hl_blockmin(N1, VISC)) {  // one atomic per CTA for the whole launch
     const unsigned long long bmin = block_min_key(kmin);
     if (tid == 0 && bmin != ~0ull) atomicMin(&F->min_h_key, bmin);
   }
@@ -1825,12 +1840,14 @@ __device__ __forceinline__ double seg_min(double x, int q, int base_lane) {
 // doubles (+ slack for a one-double shift when the group's first node is at an
 // odd index: bulk copies need 16-byte aligned sources) and the group's
 // element-face records
-template <int N1>
+template <int N1, bool V = false>
 struct NodePlan {
   static constexpr int NP = N1 * N1, EPW = 32 / NP, WARPS = 8, THREADS = 32 * WARPS;
   static constexpr int G = WARPS * EPW, GN = G * NP, GNS = (GN + 3) & ~1;
+  // the viscous variant streams the four physical viscous flux pairs too
   enum { F_H, F_HU, F_HV, F_YE, F_XE, F_YX, F_XX, F_B, F_JAC, F_SX, F_SY, F_WH, F_WHU, F_WHV,
-         kFields };
+         F_FVU, F_GVU, F_FVV, F_GVV };
+  static constexpr int kFields = V ? 18 : 14;
   static constexpr int EF = kFields * GNS;     // int4 [G][4] = 2 doubles each
   static constexpr int STAGE = EF + G * 4 * 2;  // doubles per stage
   static constexpr int STAGES = 3;
@@ -1842,28 +1859,29 @@ struct NodePlan {
 };
 
 // thread 0: stream group g's node fields and face records into stage buffer sb
-template <int N1>
+template <int N1, bool V>
 __device__ __forceinline__ void node_issue(double* sb, uint64_t* bar, const Mesh& M,
                                            const StageArgs& A, int g, bool comb) {
-  using P = NodePlan<N1>;
+  using P = NodePlan<N1, V>;
   const int e0 = M.e_lo + g * P::G, ne = min(P::G, M.n_owned - e0);
   const long long n0 = (long long)e0 * P::NP;
   const int shift = (int)(n0 & 1);
   const uint32_t fb = round16((size_t)(ne * P::NP + shift) * sizeof(double));
   const uint32_t eb = (uint32_t)(ne * 4 * sizeof(int4));
-  const int nf = comb ? P::kFields : P::F_WH;
+  const int nf = (comb ? 14 : P::F_WH) + (V ? 4 : 0);
   mbar_expect_tx(bar, nf * fb + eb);
-  const double* src[P::kFields] = {A.in.h, A.in.hu, A.in.hv, M.ye, M.xe, M.yx, M.xx,
-                                   M.b, M.jac, M.sx, M.sy, A.wn.h, A.wn.hu, A.wn.hv};
+  const double* src[18] = {A.in.h, A.in.hu, A.in.hv, M.ye, M.xe, M.yx, M.xx,
+                           M.b, M.jac, M.sx, M.sy, A.wn.h, A.wn.hu, A.wn.hv,
+                           A.fvu, A.gvu, A.fvv, A.gvv};
 #pragma unroll
   for (int f = 0; f < P::kFields; ++f)
-    if (f < nf) bulk_g2s(sb + f * P::GNS, src[f] + n0 - shift, fb, bar);
+    if (f >= P::F_FVU || comb || f < P::F_WH) bulk_g2s(sb + f * P::GNS, src[f] + n0 - shift, fb, bar);
   bulk_g2s(sb + P::EF, M.ef + (long long)e0 * 4, eb, bar);
 }
 
-template <int N1, bool FORCE>
+template <int N1, bool FORCE, bool VISC>
 __global__ void __launch_bounds__(256, 2) k_stage_node(Mesh M, Phys Ph, StageArgs A, Flags* F) {
-  using P = NodePlan<N1>;
+  using P = NodePlan<N1, VISC>;
   constexpr int NP = N1 * N1, EPW = P::EPW;
   extern __shared__ __align__(16) double sm[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + P::BAR);
@@ -1882,6 +1900,15 @@ __global__ void __launch_bounds__(256, 2) k_stage_node(Mesh M, Phys Ph, StageArg
   for (int k = 0; k < N1; ++k) {
     dx[k] = __ldg(M.Dt + i * N1 + (i + k) % N1);
     de[k] = __ldg(M.Dt + j * N1 + (j + k) % N1);
+  }
+  // viscous: the plain D rows, same rotation (strong divergence, viscosity.hpp:195-223)
+  double vx[VISC ? N1 : 1], ve[VISC ? N1 : 1];
+  if constexpr (VISC) {
+#pragma unroll
+    for (int k = 0; k < N1; ++k) {
+      vx[k] = __ldg(M.D + i * N1 + (i + k) % N1);
+      ve[k] = __ldg(M.D + j * N1 + (j + k) % N1);
+    }
   }
   const double wij = __ldg(M.w + i) * __ldg(M.w + j);
   const double g = Ph.g, h_des = Ph.h_des, inv2g = 1.0 / (2.0 * g), iw0 = 1.0 / M.w0;
@@ -1906,7 +1933,7 @@ __global__ void __launch_bounds__(256, 2) k_stage_node(Mesh M, Phys Ph, StageArg
     int grp = blockIdx.x;
     for (int s = 0; s < P::STAGES; ++s) {
       gidx[s] = grp < ngroups ? grp : -1;
-      if (grp < ngroups) node_issue<N1>(sm + s * P::STAGE, &bars[s], M, A, grp, comb);
+      if (grp < ngroups) node_issue<N1, VISC>(sm + s * P::STAGE, &bars[s], M, A, grp, comb);
       else mbar_arrive(&bars[s]);
       if (s + 1 < P::STAGES) grp = grp < ngroups ? next_group(A.gctr, grp) : ngroups;
     }
@@ -1967,6 +1994,34 @@ __global__ void __launch_bounds__(256, 2) k_stage_node(Mesh M, Phys Ph, StageArg
     r0 *= 0.25;
     r1 *= 0.125;
     r2 *= 0.125;
+    double fvo[4] = {0.0, 0.0, 0.0, 0.0};  // own physical viscous flux pairs
+    if constexpr (VISC) {
+      // strong divergence of the contravariant viscous fluxes along both lines
+      // (viscous_lhs viscosity.hpp:195-223): xi lines (y_eta, x_eta), eta lines
+      // -(y_xi, x_xi), the same metrics as the volume pairs
+      fvo[0] = sb[P::F_FVU * P::GNS + ln];
+      fvo[1] = sb[P::F_GVU * P::GNS + ln];
+      fvo[2] = sb[P::F_FVV * P::GNS + ln];
+      fvo[3] = sb[P::F_GVV * P::GNS + ln];
+#pragma unroll
+      for (int dir = 0; dir < 2; ++dir) {
+        const double Aa = dir == 0 ? ye : -yx, Ba = dir == 0 ? xe : -xx;
+        const double tu = Aa * fvo[0] - Ba * fvo[1], tv = Aa * fvo[2] - Ba * fvo[3];
+#pragma unroll
+        for (int k = 0; k < N1; ++k) {
+          double tub = tu, tvb = tv;
+          if (k > 0) {
+            const int src = dir == 0 ? base_lane + ((i + k) % N1) * N1 + j
+                                     : base_lane + i * N1 + (j + k) % N1;
+            tub = __shfl_sync(0xffffffffu, tu, src);
+            tvb = __shfl_sync(0xffffffffu, tv, src);
+          }
+          const double d = dir == 0 ? vx[k] : ve[k];
+          r1 -= d * tub;
+          r2 -= d * tvb;
+        }
+      }
+    }
     // interface fluxes: slot s is the node's s-th face
     const double co = wave_c(g, h);
     const int4* efs = reinterpret_cast<const int4*>(sb + P::EF);
@@ -1981,6 +2036,7 @@ __global__ void __launch_bounds__(256, 2) k_stage_node(Mesh M, Phys Ph, StageArg
       const bool minus = ef.y & EF_MINUS, wall = minus && (ef.y & EF_WALL);
       const bool ew = face == 1 || face == 3;
       double hn = h, hun = hu, hvn = hv, bn = bo, m0, m1;
+      double fvn[4] = {0.0, 0.0, 0.0, 0.0};  // neighbour's viscous flux pairs
       long long nb = 0;
       if (!wall) {
         const int tp = (ef.y & EF_REVERSED) ? N1 - 1 - t : t;
@@ -1989,6 +2045,12 @@ __global__ void __launch_bounds__(256, 2) k_stage_node(Mesh M, Phys Ph, StageArg
         hun = __ldg(A.in.hu + nb);
         hvn = __ldg(A.in.hv + nb);
         bn = __ldg(M.b + nb);
+        if constexpr (VISC) {
+          fvn[0] = __ldg(A.fvu + nb);
+          fvn[1] = __ldg(A.gvu + nb);
+          fvn[2] = __ldg(A.fvv + nb);
+          fvn[3] = __ldg(A.gvv + nb);
+        }
       }
       if (minus) {
         m0 = ew ? ye : yx;
@@ -2013,6 +2075,24 @@ __global__ void __launch_bounds__(256, 2) k_stage_node(Mesh M, Phys Ph, StageArg
         es_flux_pre(h, u, v, co, hn, un, vn, cn, bo, bn, nx, ny, g, inv2g, f0, f1, f2);
       else
         es_flux_pre(hn, un, vn, cn, h, u, v, co, bn, bo, nx, ny, g, inv2g, f0, f1, f2);
+      if constexpr (VISC) {
+        // viscous interface penalty (viscosity.hpp:224-246): with the minus-side
+        // normal, (phi+ - phi-)/2 lands on both sides; walls take 0 - phi-
+        const double pu_o = nx * fvo[0] + ny * fvo[1], pv_o = nx * fvo[2] + ny * fvo[3];
+        double du, dv;
+        if (wall) {
+          du = -pu_o;
+          dv = -pv_o;
+        } else {
+          const double pu_n = nx * fvn[0] + ny * fvn[1], pv_n = nx * fvn[2] + ny * fvn[3];
+          const double sg = minus ? 1.0 : -1.0;  // (plus - minus)
+          du = 0.5 * sg * (pu_n - pu_o);
+          dv = 0.5 * sg * (pv_n - pv_o);
+        }
+        // folded into the flux: c = sgn js / w0
+        f1 -= minus ? du : -du;
+        f2 -= minus ? dv : -dv;
+      }
       const double c = (minus ? 1.0 : -1.0) * js * iw0;
       r0 += c * f0;
       r1 += c * f1;
@@ -2095,7 +2175,7 @@ __global__ void __launch_bounds__(256, 2) k_stage_node(Mesh M, Phys Ph, StageArg
         gidx[s] = nx_ < ngroups ? nx_ : -1;
         if (nx_ < ngroups) {
           fence_proxy_async();
-          node_issue<N1>(sm + s * P::STAGE, &bars[s], M, A, nx_, comb);
+          node_issue<N1, VISC>(sm + s * P::STAGE, &bars[s], M, A, nx_, comb);
         } else {
           mbar_arrive(&bars[s]);
         }
@@ -2109,12 +2189,12 @@ __global__ void __launch_bounds__(256, 2) k_stage_node(Mesh M, Phys Ph, StageArg
   if (lane == 0 && wl) atomicAdd(&F->n_limited, wl);
 }
 
-template <int N1, bool FORCE>
+template <int N1, bool FORCE, bool VISC>
 static void launch_node(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
                         cudaStream_t st) {
-  using PL = NodePlan<N1>;
+  using PL = NodePlan<N1, VISC>;
   static int cache = 0;
-  auto kern = k_stage_node<N1, FORCE>;
+  auto kern = k_stage_node<N1, FORCE, VISC>;
   const int groups = (M.n_owned - M.e_lo + PL::G - 1) / PL::G;
   const int grid = grid_for(kern, PL::THREADS, PL::bytes, groups, cache);
   if (grid > 0) kern<<<grid, PL::THREADS, PL::bytes, st>>>(M, P, A, F);
@@ -2217,7 +2297,15 @@ template <int N1>
 static void launch_n(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
                      cudaStream_t st) {
   if constexpr (N1 >= 3) {
-    if (A.fvu) {  // viscous stages always take the half-line kernel
+    if (A.fvu) {  // viscous stages: node-per-thread kernel at N+1 <= SWDG_VISC_NODE_MAX, else half-line
+      const int ovv = variant_override();
+      if constexpr (N1 <= 4) {
+        if (SWDG_VISC_NODE_MAX >= N1 && ovv != 2) {
+          if (A.fh) launch_node<N1, true, true>(M, P, A, F, st);
+          else launch_node<N1, false, true>(M, P, A, F, st);
+          return;
+        }
+      }
       if (A.fh) launch_half<N1, true, true>(M, P, A, F, st);
       else launch_half<N1, false, true>(M, P, A, F, st);
       return;
@@ -2240,8 +2328,8 @@ static void launch_n(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
   if (v == 4 && launch_pl_stage(M, P, A, F, st)) return;
   if constexpr (N1 <= 4) {
     if (v == 5) {
-      if (A.fh) launch_node<N1, true>(M, P, A, F, st);
-      else launch_node<N1, false>(M, P, A, F, st);
+      if (A.fh) launch_node<N1, true, false>(M, P, A, F, st);
+      else launch_node<N1, false, false>(M, P, A, F, st);
       return;
     }
   }

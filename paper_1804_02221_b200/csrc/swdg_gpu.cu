@@ -375,11 +375,13 @@ void allocate(swdg_gpu* c, int K, int n_owned, int N, const std::vector<int4>& e
   c->r_ind = c->dalloc<double>(K);
   ck(cudaMemset(c->eps, 0, K * sizeof(double)), "memset eps");
   if (c->params.visc_enabled) {
-    double* vb = c->dalloc<double>(4 * nn);
+    // padded stride like the state buffers: 16-byte aligned bases and slack for
+    // the node kernel's bulk copies (one double before, one after a group)
+    double* vb = c->dalloc<double>(4 * nnp);
     c->fvu = vb;
-    c->fvv = vb + nn;
-    c->gvu = vb + 2 * nn;
-    c->gvv = vb + 3 * nn;
+    c->fvv = vb + nnp;
+    c->gvu = vb + 2 * nnp;
+    c->gvv = vb + 3 * nnp;
   }
   c->partial = c->dalloc<double>(2 * (size_t)K);
   c->sums = c->dalloc<double>(2);

@@ -9,6 +9,7 @@
 set -x
 O=gpurun_out/prof_r01
 mkdir -p $O
+timeout 900 python -m pytest tests -m gpu -x -q > $O/gputests.txt 2>&1
 timeout 900 python bench.py --steps 10 --warmup 3 > $O/bench_n7.json 2> $O/bench_n7.err
 timeout 600 python bench.py --steps 10 --warmup 3 --viscous --no-sweep > $O/bench_n7_visc.json 2> $O/bench_n7_visc.err
 timeout 600 python bench.py --steps 5 --warmup 3 --distributed --no-sweep --cpu-budget 1 > $O/bench_n7_dist1.json 2> $O/bench_n7_dist1.err
@@ -24,4 +25,7 @@ done
 for n in ${DEGREES:-1 2 3 4 5 6 7 8 9 10 11 12 13 14 15}; do
   timeout 200 python -m paper_1804_02221_b200.profile_stage --degree $n --kx 1000 --steps 3 --time 5 2>&1 | grep "^N="
 done > $O/sweep.txt
+for n in ${DEGREES_VISC:-2 3 4 5 6 7 8 9 10 11 12 13 14 15}; do
+  timeout 300 python -m paper_1804_02221_b200.profile_stage --degree $n --kx 1000 --steps 3 --time 5 --viscous 2>&1 | grep "^N="
+done > $O/sweep_visc.txt
 ls -la $O

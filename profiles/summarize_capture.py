@@ -111,6 +111,7 @@ def main():
             for name, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
                 f.write(f"{name}\t{len(v)}\t{sum(v) / len(v):.1f}\t{sum(v):.1f}\t{sum(v) / tot:.3f}\n")
     for a, b in (("bench_n7.json", "r01_bench_n7.json"), ("sweep.txt", "r01_sweep.txt"),
+                 ("sweep_visc.txt", "r01_sweep_visc.txt"),
                  ("bench_n7_visc.json", "r01_bench_n7_visc.json"),
                  ("bench_n7_dist1.json", "r01_bench_n7_dist1.json"),
                  ("bench_ref.json", "r01_bench_ref.json")):
