@@ -42,6 +42,13 @@
 
 // resident half-line CTAs per SM the register allocation is compiled for
 // (__launch_bounds__ min blocks), per N+1; the -D overrides are for A/B builds
+// viscous pre-kernel: the line kernel up to this N+1 (13, 15 or 16), node-per-thread
+// above.  Measured (viscous ms/stage) after the per-CTA eps atomic and async
+// staging: N=13 28.2 -> 25.9, N=14 50.4 -> 36.0, N=15 47.8 -> 47.2 with the line
+// kernel at N+1 = 14, 15, 16
+#ifndef SWDG_VL_MAX
+#define SWDG_VL_MAX 16
+#endif
 // viscous stages up to this N+1 take the node-per-thread kernel
 #ifndef SWDG_VISC_NODE_MAX
 #define SWDG_VISC_NODE_MAX 3  // measured: N=2 1.224 -> 1.013 ms/stage; N+1 = 4 slower (1.585 -> 1.798)
@@ -2356,9 +2363,9 @@ static void launch_n(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
 int launch_fast_visc_pre(const Mesh& M, const Phys& P, CState S, double* eps, double* fvu,
                          double* fvv, double* gvu, double* gvv, Flags* F, cudaStream_t st) {
   // line-based kernel (one velocity component at a time: ~5 (N+1) doubles per
-  // thread) up to N+1 = 13 (measured 22.5 vs 24.5 ms/stage at N=12), the
-  // node-per-thread kernel above (at N+1 = 16 the line kernel's 212 registers
-  // and 70 KB leave 6 warps/SM: 50.3 vs 47.6 ms); SWDG_VISC_NODE=1 forces it
+  // thread) up to N+1 = SWDG_VL_MAX (measured 22.5 vs 24.5 ms/stage at N=12 against
+  // the node-per-thread kernel; before the per-CTA eps atomic the node kernel won
+  // at N+1 >= 14), the node-per-thread kernel above; SWDG_VISC_NODE=1 forces it
   static const bool node_only = getenv("SWDG_VISC_NODE") != nullptr;
   switch (M.n1) {
 #define SWDG_VL(n)                                                                 \
@@ -2369,7 +2376,17 @@ int launch_fast_visc_pre(const Mesh& M, const Phys& P, CState S, double* eps, do
 #define SWDG_VP(n) \
   case n: launch_visc_pre_n<n>(M, P, S, eps, fvu, fvv, gvu, gvv, F, st); break;
     SWDG_VL(3) SWDG_VL(4) SWDG_VL(5) SWDG_VL(6) SWDG_VL(7) SWDG_VL(8) SWDG_VL(9) SWDG_VL(10)
-    SWDG_VL(11) SWDG_VL(12) SWDG_VL(13) SWDG_VP(14) SWDG_VP(15) SWDG_VP(16)
+    SWDG_VL(11) SWDG_VL(12) SWDG_VL(13)
+#if SWDG_VL_MAX >= 15
+    SWDG_VL(14) SWDG_VL(15)
+#else
+    SWDG_VP(14) SWDG_VP(15)
+#endif
+#if SWDG_VL_MAX >= 16
+    SWDG_VL(16)
+#else
+    SWDG_VP(16)
+#endif
 #undef SWDG_VP
 #undef SWDG_VL
     default: return 0;

@@ -229,7 +229,7 @@ def test_fast_viscous_rhs(name):
             assert np.abs(e_gpu - e_ref).max() <= 1e-13 * max(1e-300, e_ref.max(), 1.0)
 
 
-@pytest.mark.parametrize("degree", [2, 5, 9, 10, 12, 15])
+@pytest.mark.parametrize("degree", [2, 3, 5, 9, 10, 12, 13, 14, 15])
 def test_fast_viscous_all_degrees(degree):
     """The line-based viscous pre-kernel and the viscous stage kernel across the
     degree range (the element configurations differ per degree): one stage within
