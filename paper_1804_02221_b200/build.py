@@ -21,6 +21,7 @@ ROOT = os.path.dirname(PKG)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+          "--split-compile=0", "-diag-suppress=177",
           "-I" + CSRC, "-I" + os.path.join(ROOT, "include")]
 
 SOURCES = {
@@ -28,9 +29,6 @@ SOURCES = {
     "kernels_exact.cu": ["--fmad=false"],
     "kernels_common.cu": [],
     "kernels_fast.cu": [],
-    "kernels_pl_a.cu": [],
-    "kernels_pl_b.cu": [],
-    "kernels_pl_c.cu": [],
     "kernels_mesh.cu": [],
     "host_mesh.cpp": [],
 }

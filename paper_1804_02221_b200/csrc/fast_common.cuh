@@ -13,6 +13,7 @@
 #include "swdg_launch.h"
 
 namespace swdg_dev {
+extern int g_grid_cap;  // kernels_common.cu; 0 = no cap (test hook)
 namespace {
 
 // ---- constant operator tables --------------------------------------------
@@ -149,17 +150,33 @@ __device__ __forceinline__ void es_flux_fast(double hm, double hum, double hvm, 
 
 __device__ __forceinline__ uint32_t round16(size_t b) { return (uint32_t)((b + 15) & ~size_t(15)); }
 
+// Per-device launch state: the dynamic shared-memory attribute and the
+// occupancy are properties of (kernel, device context), so they are cached per
+// device ordinal (a process may drive several B200s).
+constexpr int kMaxDevices = 64;
+
+inline int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return -1;
+  return dev;
+}
+
+// persistent grid: resident CTAs over all SMs (capped at the group count)
 template <class KERN>
-int grid_for(KERN kern, int threads, size_t bytes, int groups, int& cache) {
-  if (cache == 0) {
+int grid_for(KERN kern, int threads, size_t bytes, int groups, int (&cache)[kMaxDevices]) {
+  const int dev = current_device();
+  if (dev < 0) return 0;
+  if (cache[dev] == 0) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    int per_sm = 0, dev = 0, sms = 0;
+    int per_sm = 0, sms = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, bytes);
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cache = (per_sm > 0 ? per_sm : 1) * sms;
+    cache[dev] = (per_sm > 0 ? per_sm : 1) * sms;
   }
-  return groups < cache ? groups : cache;
+  int grid = groups < cache[dev] ? groups : cache[dev];
+  // test hook (swdg_gpu_set_grid_cap): fewer CTAs, so each loops over many groups
+  if (g_grid_cap > 0 && grid > g_grid_cap) grid = g_grid_cap;
+  return grid;
 }
 
 // this TU's copy of the operator tables

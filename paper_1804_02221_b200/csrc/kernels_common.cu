@@ -197,9 +197,5 @@ int launch_diagnostics(const Mesh& M, const Phys& P, CState S, double* partial, 
 }  // namespace swdg_dev
 
 namespace swdg_dev {
-int launch_pl_stage(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F, cudaStream_t st) {
-  if (M.n1 <= 8) return launch_pl_stage_a(M, P, A, F, st);
-  if (M.n1 <= 12) return launch_pl_stage_b(M, P, A, F, st);
-  return launch_pl_stage_c(M, P, A, F, st);
-}
+int g_grid_cap = 0;
 }  // namespace swdg_dev

@@ -42,13 +42,6 @@
 
 // resident half-line CTAs per SM the register allocation is compiled for
 // (__launch_bounds__ min blocks), per N+1; the -D overrides are for A/B builds
-// viscous pre-kernel: the line kernel up to this N+1 (13, 15 or 16), node-per-thread
-// above.  Measured (viscous ms/stage) after the per-CTA eps atomic and async
-// staging: N=13 28.2 -> 25.9, N=14 50.4 -> 36.0, N=15 47.8 -> 47.2 with the line
-// kernel at N+1 = 14, 15, 16
-#ifndef SWDG_VL_MAX
-#define SWDG_VL_MAX 16
-#endif
 // viscous stages up to this N+1 take the node-per-thread kernel
 #ifndef SWDG_VISC_NODE_MAX
 #define SWDG_VISC_NODE_MAX 3  // measured: N=2 1.224 -> 1.013 ms/stage; N+1 = 4 slower (1.585 -> 1.798)
@@ -76,373 +69,6 @@ namespace {
 // first wave, the rest in claim order (persistent CTAs stay in one wavefront)
 __device__ __forceinline__ int next_group(int* ctr, int grp) {
   return ctr ? (int)gridDim.x + atomicAdd(ctr, 1) : grp + (int)gridDim.x;
-}
-
-// ---- shared-memory plan (in doubles) ---------------------------------------
-template <int N1>
-struct Plan {
-  static constexpr int NP = N1 * N1;
-  static constexpr int T = 2 * N1;  // threads per element
-  static constexpr int E = ((128 / T) & ~1) > 2 ? ((128 / T) & ~1) : 2;  // even
-  static constexpr int THREADS = T * E;
-  static constexpr int GNP = (E * NP + 1) & ~1;  // 16-byte aligned field stride
-  enum { F_H, F_HU, F_HV, F_YE, F_XE, F_YX, F_XX, F_B, kLineFields };
-  enum { N_JAC, N_WH, N_WHU, N_WHV, kNodeFields };
-  static constexpr int LINE = 0;
-  static constexpr int NODE = LINE + kLineFields * GNP;
-  static constexpr int ACC = NODE + kNodeFields * GNP;
-  static constexpr int TR = ACC + 3 * GNP;         // [E][4][N1][8] neighbour traces
-  static constexpr int EFO = TR + E * 4 * N1 * 8;  // int4 [E][4] = 2 doubles each
-  static constexpr int RED = EFO + E * 4 * 2;      // [E][N1 eta lines][5]
-  static constexpr int BAR = RED + E * N1 * 5;     // 2 mbarriers
-  static constexpr int TOTAL = BAR + 2;
-  static constexpr size_t bytes = TOTAL * sizeof(double);
-};
-
-
-// thread 0: stream one group's line data (8 fields + face connectivity)
-template <int N1>
-__device__ __forceinline__ void issue_line(double* sm, const Mesh& M, const CState& in, int g,
-                                           uint64_t* bar) {
-  using P = Plan<N1>;
-  const int e0 = M.e_lo + g * P::E, ne = min(P::E, M.n_owned - e0);
-  const uint32_t fb = round16((size_t)ne * P::NP * sizeof(double));
-  const uint32_t eb = (uint32_t)(ne * 4 * sizeof(int4));
-  mbar_expect_tx(bar, P::kLineFields * fb + eb);
-  const long long off = (long long)e0 * P::NP;
-  const double* src[P::kLineFields] = {in.h, in.hu, in.hv, M.ye, M.xe, M.yx, M.xx, M.b};
-#pragma unroll
-  for (int f = 0; f < P::kLineFields; ++f)
-    bulk_g2s(sm + P::LINE + f * P::GNP, src[f] + off, fb, bar);
-  bulk_g2s(sm + P::EFO, M.ef + (long long)e0 * 4, eb, bar);
-}
-
-// thread 0: stream one group's node-phase data (J and, for stages 2-3, W^n)
-template <int N1>
-__device__ __forceinline__ void issue_node(double* sm, const Mesh& M, const StageArgs& A, int g,
-                                           uint64_t* bar) {
-  using P = Plan<N1>;
-  const int e0 = M.e_lo + g * P::E, ne = min(P::E, M.n_owned - e0);
-  const uint32_t fb = round16((size_t)ne * P::NP * sizeof(double));
-  const bool wn = A.update && A.stage > 0;
-  mbar_expect_tx(bar, (wn ? 4 : 1) * fb);
-  const long long off = (long long)e0 * P::NP;
-  bulk_g2s(sm + P::NODE + P::N_JAC * P::GNP, M.jac + off, fb, bar);
-  if (wn) {
-    bulk_g2s(sm + P::NODE + P::N_WH * P::GNP, A.wn.h + off, fb, bar);
-    bulk_g2s(sm + P::NODE + P::N_WHU * P::GNP, A.wn.hu + off, fb, bar);
-    bulk_g2s(sm + P::NODE + P::N_WHV * P::GNP, A.wn.hv + off, fb, bar);
-  }
-}
-
-template <int N1, bool FORCE>
-__global__ void __launch_bounds__(Plan<N1>::THREADS, 1)
-    k_stage(Mesh M, Phys Ph, StageArgs A, Flags* F) {
-  using P = Plan<N1>;
-  using O = Ops<N1>;
-  constexpr int NP = P::NP, T = P::T, E = P::E;
-  extern __shared__ __align__(16) double sm[];
-  uint64_t* bar_line = reinterpret_cast<uint64_t*>(sm + P::BAR);
-  uint64_t* bar_node = bar_line + 1;
-  const int tid = threadIdx.x, el = tid / T, lt = tid % T;
-  const bool xi = lt < N1;
-  const int li = xi ? lt : lt - N1;
-  const int ngroups = (M.n_owned - M.e_lo + E - 1) / E;
-  const double g = Ph.g, h_des = Ph.h_des, inv2g = 1.0 / (2.0 * g), iw0 = 1.0 / M.w0;
-
-  if (tid == 0) {
-    mbar_init(bar_line, 1);
-    mbar_init(bar_node, 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if ((int)blockIdx.x >= ngroups) return;  // uniform across the CTA
-  if (tid == 0) issue_line<N1>(sm, M, A.in, blockIdx.x, bar_line);
-  uint32_t ph_line = 0, ph_node = 0;
-
-  // node k of this thread's line inside the element: xi-line j=li -> (k,li),
-  // eta-line i=li -> (li,k)
-  auto idx = [&](int k) { return xi ? k * N1 + li : li * N1 + k; };
-
-  __shared__ int s_next;  // the next group, claimed by thread 0
-  unsigned long long kmin = ~0ull;  // min height key of this thread's elements
-  for (int grp = blockIdx.x; grp < ngroups; grp = s_next) {
-    const int e0 = M.e_lo + grp * E, ne = min(E, M.n_owned - e0);
-    const bool active = el < ne;
-    const int e = e0 + el;
-    mbar_wait(bar_line, ph_line);
-    ph_line ^= 1;
-
-    // ---- line data -> registers; gathers for the two endpoints
-    double h[N1], u[N1], v[N1], hu[N1], hv[N1], Am[N1], Bm[N1], bb[N1];
-    double r0[N1], r1[N1], r2[N1];
-    int efy[2] = {0, 0};
-    const double* L = sm + P::LINE + el * NP;
-#pragma unroll
-    for (int k = 0; k < N1; ++k) {
-      const int q = idx(k);
-      h[k] = L[P::F_H * P::GNP + q];
-      hu[k] = L[P::F_HU * P::GNP + q];
-      hv[k] = L[P::F_HV * P::GNP + q];
-      Am[k] = xi ? L[P::F_YE * P::GNP + q] : -L[P::F_YX * P::GNP + q];
-      Bm[k] = xi ? L[P::F_XE * P::GNP + q] : -L[P::F_XX * P::GNP + q];
-      bb[k] = L[P::F_B * P::GNP + q];
-      r0[k] = r1[k] = r2[k] = 0.0;
-    }
-    if (active) {
-      const int4* ef4 = reinterpret_cast<const int4*>(sm + P::EFO) + el * 4;
-#pragma unroll
-      for (int end = 0; end < 2; ++end) {
-        const int face = xi ? (end ? 1 : 3) : (end ? 2 : 0);
-        const int4 ef = ef4[face];
-        efy[end] = ef.y;
-        if ((ef.y & EF_PRESENT) && !(ef.y & EF_WALL)) {
-          const int nf = ef.y & EF_NBR_FACE_MASK;
-          const int tp = (ef.y & EF_REVERSED) ? N1 - 1 - li : li;
-          const long long nb = (long long)ef.x * NP + face_node(N1, nf, tp);
-          double* tr = sm + P::TR + ((el * 4 + face) * N1 + li) * 8;
-          cp_async8(tr + 0, A.in.h + nb);
-          cp_async8(tr + 1, A.in.hu + nb);
-          cp_async8(tr + 2, A.in.hv + nb);
-          cp_async8(tr + 3, M.b + nb);
-          if (!(ef.y & EF_MINUS)) {  // plus side: the minus side's face metrics
-            const bool ew = nf == 1 || nf == 3;
-            cp_async8(tr + 4, (ew ? M.ye : M.yx) + nb);
-            cp_async8(tr + 5, (ew ? M.xe : M.xx) + nb);
-          }
-        }
-      }
-    }
-    cp_async_commit();
-    __syncthreads();  // line buffer and connectivity consumed
-    if (tid == 0) {
-      const int gn = next_group(A.gctr, grp);
-      s_next = gn;
-      if (gn < ngroups) issue_line<N1>(sm, M, A.in, gn, bar_line);
-      issue_node<N1>(sm, M, A, grp, bar_node);
-    }
-#pragma unroll
-    for (int k = 0; k < N1; ++k) vel(h[k], hu[k], hv[k], h_des, u[k], v[k]);
-
-    // ---- volume: unordered pairs (a<b) plus the two corner diagonals
-    const double g2 = 2.0 * g;
-#pragma unroll
-    for (int a = 0; a < N1; ++a) {
-#pragma unroll
-      for (int b = a; b < N1; ++b) {
-        if (a == b && a != 0 && a != N1 - 1) continue;  // Dtilde(i,i) = 0 inside
-        const double Shu = hu[a] + hu[b], Shv = hv[a] + hv[b];
-        const double Su = u[a] + u[b], Sv = v[a] + v[b];
-        const double SA = Am[a] + Am[b], SB = Bm[a] + Bm[b];
-        const double F0 = SA * Shu - SB * Shv;  // 4 Ftilde_0
-        const double Q = g2 * h[a] * h[b];
-        const double T1 = Su * F0 + Q * SA;     // 8 Ftilde_1
-        const double T2 = Sv * F0 - Q * SB;     // 8 Ftilde_2
-        r0[a] += O::D4(a, b) * F0;
-        r1[a] += O::D8(a, b) * T1;
-        r2[a] += O::D8(a, b) * T2;
-        if (a != b) {
-          r0[b] += O::D4(b, a) * F0;
-          r1[b] += O::D8(b, a) * T1;
-          r2[b] += O::D8(b, a) * T2;
-        }
-      }
-    }
-    // ---- split bathymetry source, this direction's half (dg_rhs.hpp:171-176)
-#pragma unroll
-    for (int k = 0; k < N1; ++k) {
-      double db = 0.0, dAb = 0.0, dBb = 0.0;
-#pragma unroll
-      for (int m = 0; m < N1; ++m) {
-        const double d = O::D(k, m);
-        db += d * bb[m];
-        dAb += d * (Am[m] * bb[m]);
-        dBb += d * (Bm[m] * bb[m]);
-      }
-      const double hg2 = 0.5 * g * h[k];
-      r1[k] += hg2 * (Am[k] * db + dAb);
-      r2[k] -= hg2 * (Bm[k] * db + dBb);
-    }
-
-    // ---- interface fluxes at the two endpoints (dg_rhs.hpp:202-252)
-    cp_async_wait_all();
-    if (active) {
-#pragma unroll
-      for (int end = 0; end < 2; ++end) {
-        const int k = end ? N1 - 1 : 0;
-        const int face = xi ? (end ? 1 : 3) : (end ? 2 : 0);
-        const int fy = efy[end];
-        if (!(fy & EF_PRESENT)) continue;
-        const double* tr = sm + P::TR + ((el * 4 + face) * N1 + li) * 8;
-        // own face metrics: xi-lines (y_eta,x_eta) = (A,B); eta-lines (y_xi,x_xi) = -(A,B)
-        const double om0 = xi ? Am[k] : -Am[k], om1 = xi ? Bm[k] : -Bm[k];
-        double wm0, wm1, wm2, wp0, wp1, wp2, bm, bp, nx, ny, js;
-        double sgn = 1.0;
-        if (fy & EF_MINUS) {
-          face_normal(face, om0, om1, nx, ny, js);
-          wm0 = h[k];
-          wm1 = hu[k];
-          wm2 = hv[k];
-          bm = bb[k];
-          if (fy & EF_WALL) {  // exterior_state (mesh.hpp:382-386)
-            const double mn = wm1 * nx + wm2 * ny;
-            wp0 = wm0;
-            wp1 = wm1 - 2.0 * mn * nx;
-            wp2 = wm2 - 2.0 * mn * ny;
-            bp = bm;
-          } else {
-            wp0 = tr[0];
-            wp1 = tr[1];
-            wp2 = tr[2];
-            bp = tr[3];
-          }
-        } else {
-          face_normal(fy & EF_NBR_FACE_MASK, tr[4], tr[5], nx, ny, js);
-          wm0 = tr[0];
-          wm1 = tr[1];
-          wm2 = tr[2];
-          bm = tr[3];
-          wp0 = h[k];
-          wp1 = hu[k];
-          wp2 = hv[k];
-          bp = bb[k];
-          sgn = -1.0;
-        }
-        double f0, f1, f2;
-        es_flux_fast(wm0, wm1, wm2, wp0, wp1, wp2, bm, bp, nx, ny, g, inv2g, h_des, f0, f1, f2);
-        const double c = sgn * js * iw0;
-        r0[k] += c * f0;
-        r1[k] += c * f1;
-        r2[k] += c * f2;
-      }
-    }
-    // xi-lines hand their accumulators to the eta-line owners of the nodes
-    if (xi) {
-#pragma unroll
-      for (int k = 0; k < N1; ++k) {
-        const int q = el * NP + idx(k);
-        sm[P::ACC + 0 * P::GNP + q] = r0[k];
-        sm[P::ACC + 1 * P::GNP + q] = r1[k];
-        sm[P::ACC + 2 * P::GNP + q] = r2[k];
-      }
-    }
-    __syncthreads();
-    mbar_wait(bar_node, ph_node);
-    ph_node ^= 1;
-
-    // ---- node phase on the eta-line threads: node (li, k), k = 0..N
-    const double* Nd = sm + P::NODE + el * NP;
-    double pv[5] = {0.0, 0.0, 0.0, 0.0, 1.0e300};  // element partials of this thread
-    if (!xi && active) {
-      double s_area = 0.0, s0 = 0.0, s1 = 0.0, s2 = 0.0, mmin = 1.0e300;
-      const double wi = O::w(li);
-#pragma unroll
-      for (int k = 0; k < N1; ++k) {
-        const int q = idx(k);
-        const long long n = (long long)e * NP + q;
-        const double jac = Nd[P::N_JAC * P::GNP + q];
-        const double ij = -1.0 / jac;
-        double rh = (sm[P::ACC + 0 * P::GNP + el * NP + q] + r0[k]) * ij;
-        double rhu = (sm[P::ACC + 1 * P::GNP + el * NP + q] + r1[k]) * ij;
-        double rhv = (sm[P::ACC + 2 * P::GNP + el * NP + q] + r2[k]) * ij;
-        if (FORCE) {
-          rh += A.fh[n];
-          rhu += A.fhu[n];
-          rhv += A.fhv[n];
-        }
-        if (A.rhs.h) {
-          A.rhs.h[n] = rh;
-          A.rhs.hu[n] = rhu;
-          A.rhs.hv[n] = rhv;
-        }
-        double sh = h[k] + A.dt * rh;
-        double shu = hu[k] + A.dt * rhu;
-        double shv = hv[k] + A.dt * rhv;
-        if (A.stage > 0 && A.update) {
-          sh = A.ca * Nd[P::N_WH * P::GNP + q] + A.cb * sh;
-          shu = A.ca * Nd[P::N_WHU * P::GNP + q] + A.cb * shu;
-          shv = A.ca * Nd[P::N_WHV * P::GNP + q] + A.cb * shv;
-        }
-        h[k] = sh;
-        hu[k] = shu;
-        hv[k] = shv;
-        const double wj = wi * O::w(k) * jac;
-        s_area += wj;
-        s0 += wj * sh;
-        s1 += wj * shu;
-        s2 += wj * shv;
-        mmin = smin(mmin, sh);
-      }
-      pv[0] = s_area;
-      pv[1] = s0;
-      pv[2] = s1;
-      pv[3] = s2;
-      pv[4] = mmin;
-    }
-    // element partials: one slot per eta line, summed below in line order by the
-    // eta threads (the order the trajectory tests were pinned with)
-    if (!xi && active) {
-      double* rr = sm + P::RED + (el * N1 + li) * 5;
-#pragma unroll
-      for (int c = 0; c < 5; ++c) rr[c] = pv[c];
-    }
-    __syncthreads();
-
-    // ---- limiter (limit_element, limiter.hpp:43-84) and write-out, eta threads
-    bool lim = !xi && active && A.update;
-    if (lim) {
-      double area = 0.0, a0 = 0.0, a1 = 0.0, a2 = 0.0, mmin = 1.0e300;
-#pragma unroll
-      for (int l = 0; l < N1; ++l) {
-        const double* rr = sm + P::RED + (el * N1 + l) * 5;
-        area += rr[0];
-        a0 += rr[1];
-        a1 += rr[2];
-        a2 += rr[3];
-        mmin = smin(mmin, rr[4]);
-      }
-      const double inv = 1.0 / area;
-      const double avg0 = inv * a0, avg1 = inv * a1, avg2 = inv * a2;
-      const bool lead = lt == N1;
-      if (avg0 < 0.0) {
-        if (lead) {
-          atomicExch(&F->reject, 1);
-          if (!Ph.limiter) atomicExch(&F->abort, 1);
-        }
-        lim = false;
-      }
-      double theta = 1.0;
-      if (lim && Ph.limiter && mmin < 0.0) {
-        const double denom = avg0 - mmin;
-        theta = denom < 1e-14 ? 1.0 : smin(1.0, avg0 / denom);
-      }
-      if (lim && !Ph.limiter && mmin < 0.0 && lead) atomicExch(&F->abort, 1);
-      if (lim) {
-        const long long nb0 = (long long)e * NP + li * N1;
-#pragma unroll
-        for (int k = 0; k < N1; ++k) {
-          double sh = h[k], shu = hu[k], shv = hv[k];
-          if (theta < 1.0) {
-            sh = smax(theta * (sh - avg0) + avg0, 0.0);
-            shu = theta * (shu - avg1) + avg1;
-            shv = theta * (shv - avg2) + avg2;
-          }
-          if (Ph.limiter && sh < Ph.h_tol) {
-            shu = 0.0;
-            shv = 0.0;
-          }
-          A.out.h[nb0 + k] = sh;
-          A.out.hu[nb0 + k] = shu;
-          A.out.hv[nb0 + k] = shv;
-        }
-        if (lead) {  // minimum after limiting: the monotone map of the minimum
-          const double m = theta < 1.0 ? smax(theta * (mmin - avg0) + avg0, 0.0) : mmin;
-          atomicMin(&F->min_h_key, order_key(m));
-          if (theta < 1.0) atomicAdd(&F->n_limited, 1);
-        }
-      }
-    }
-  }
 }
 
 // ===========================================================================
@@ -1339,221 +965,6 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
 }
 
 // ===========================================================================
-template <int N1>
-struct VP {
-  static constexpr int NP = N1 * N1;
-  static constexpr int E = (256 / NP) > 1 ? (256 / NP) : 1;
-  static constexpr int THREADS = E * NP;
-  static constexpr int OPAD = N1 + 1;  // operator row stride (conflict-free)
-  static constexpr int PMAX = (NP + 31) / 32 + 1;  // warp pieces of one element
-  enum { H, U, V, YE, XE, YX, XX, TMP, kF };
-  static constexpr int OPV = kF * E * NP;        // V^-1 [N1][OPAD]
-  static constexpr int OPD = OPV + N1 * OPAD;    // D-hat [N1][OPAD]
-  static constexpr int RED = OPD + N1 * OPAD;    // [E][PMAX][4] shell-sum pieces
-  static constexpr int EPS = RED + E * PMAX * 4;
-  static constexpr int TOTAL = EPS + E;
-  static constexpr size_t bytes = TOTAL * sizeof(double);
-};
-
-// Viscous pre-kernel (fast): per element the modal shock indicator and the
-// viscosity coefficient (viscosity.hpp:35-78, finished on the device with CUDA
-// log10/sin), the BR1 lifted velocity gradients (viscosity.hpp:95-168) and the
-// physical viscous flux pairs h eps grad (viscosity.hpp:187-194).  One thread
-// per node.  The operators sit in shared memory (per-thread indices: constant
-// memory would serialise), the neighbour traces for the BR1 face corrections
-// are requested first and consumed last, and the four shell energies are
-// summed by a segmented warp-shuffle reduction (fixed tree: reproducible).
-template <int N1>
-__global__ void __launch_bounds__(VP<N1>::THREADS)
-    k_visc_pre(Mesh M, Phys Ph, CState S, double* eps_out, double* fvu, double* fvv,
-               double* gvu, double* gvv, Flags* F) {
-  using P = VP<N1>;
-  using O = Ops<N1>;
-  constexpr int NP = P::NP, N = N1 - 1, OP = P::OPAD;
-  extern __shared__ __align__(16) double sm[];
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int el = tid / NP, q = tid % NP, i = q / N1, j = q % N1;
-  const int e = blockIdx.x * P::E + el;
-  const bool active = e < M.n_owned;
-  const long long n = (long long)e * NP + q;
-  double* f = sm + el * NP;
-  auto fld = [&](int k) { return f + k * P::E * NP; };
-  // neighbour traces of this node's faces (<= 2), requested before anything else
-  int fa[2] = {0, 0}, ta[2] = {0, 0}, fy[2] = {0, 0};
-  double nh[2] = {0.0, 0.0}, nhu[2] = {0.0, 0.0}, nhv[2] = {0.0, 0.0};
-  int nfc = 0;
-  if (active) {
-    nfc = node_faces(N1, i, j, fa, ta);
-    for (int c2 = 0; c2 < nfc; ++c2) {
-      const int4 ef = M.ef[e * 4 + fa[c2]];
-      fy[c2] = ef.y;
-      if ((ef.y & EF_PRESENT) && !(ef.y & EF_WALL)) {
-        const int nf = ef.y & EF_NBR_FACE_MASK;
-        const int tp = (ef.y & EF_REVERSED) ? N - ta[c2] : ta[c2];
-        const long long nb = (long long)ef.x * NP + face_node(N1, nf, tp);
-        nh[c2] = __ldg(S.h + nb);
-        nhu[c2] = __ldg(S.hu + nb);
-        nhv[c2] = __ldg(S.hv + nb);
-      }
-    }
-  }
-  double h = 0.0, hu = 0.0, hv = 0.0, jac = 1.0;
-  if (active) {
-    h = S.h[n];
-    hu = S.hu[n];
-    hv = S.hv[n];
-    jac = __ldg(M.jac + n);
-    double u, v;
-    vel(h, hu, hv, Ph.h_des, u, v);
-    fld(P::H)[q] = h;
-    fld(P::U)[q] = u;
-    fld(P::V)[q] = v;
-    fld(P::YE)[q] = M.ye[n];
-    fld(P::XE)[q] = M.xe[n];
-    fld(P::YX)[q] = M.yx[n];
-    fld(P::XX)[q] = M.xx[n];
-  }
-  for (int k = tid; k < NP; k += P::THREADS) {
-    sm[P::OPV + (k / N1) * OP + k % N1] = O::Vinv(k / N1, k % N1);
-    sm[P::OPD + (k / N1) * OP + k % N1] = O::Dh(k / N1, k % N1);
-  }
-  __syncthreads();
-  const double* VI = sm + P::OPV;
-  const double* DH = sm + P::OPD;
-  // ---- modal transform of h: tmp = V^-1 h, modal = tmp V^-T
-  double t = 0.0;
-#pragma unroll
-  for (int k = 0; k < N1; ++k) t += VI[i * OP + k] * fld(P::H)[k * N1 + j];
-  fld(P::TMP)[q] = t;
-  __syncthreads();
-  double mo = 0.0;
-#pragma unroll
-  for (int k = 0; k < N1; ++k) mo += fld(P::TMP)[i * N1 + k] * VI[j * OP + k];
-  const double m2 = active ? mo * mo : 0.0;
-  // shells: den1 all, den2 i,j<N, num1 top shell (i==N or j==N), num2 shell N-1
-  double c[4] = {m2, (i < N && j < N) ? m2 : 0.0, (i == N || j == N) ? m2 : 0.0,
-                 ((i == N - 1 && j <= N - 1) || (j == N - 1 && i <= N - 1)) ? m2 : 0.0};
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int el2 = __shfl_down_sync(0xffffffffu, el, o);
-    double tt[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) tt[k] = __shfl_down_sync(0xffffffffu, c[k], o);
-    if (lane + o < 32 && el2 == el) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) c[k] += tt[k];
-    }
-  }
-  const int w0 = (el * NP) >> 5;  // first warp of the element
-  if (lane == 0 || q == 0) {
-    double* rr = sm + P::RED + (el * P::PMAX + (tid >> 5) - w0) * 4;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) rr[k] = c[k];
-  }
-  __syncthreads();
-  if (q == 0 && active) {
-    const int npc = ((el * NP + NP - 1) >> 5) - w0 + 1;
-    double den1 = 0.0, den2 = 0.0, num1 = 0.0, num2 = 0.0;
-    for (int pc = 0; pc < npc; ++pc) {
-      const double* rr = sm + P::RED + (el * P::PMAX + pc) * 4;
-      den1 += rr[0];
-      den2 += rr[1];
-      num1 += rr[2];
-      num2 += rr[3];
-    }
-    const double floor_abs = 1e-28 * den1 + 1e-300;
-    double eps = 0.0;
-    if (!(den1 <= 1e-300)) {
-      const double r1 = num1 > floor_abs ? num1 / den1 : 0.0;
-      const double r2 = (num2 > floor_abs && den2 > floor_abs) ? num2 / den2 : 0.0;
-      const double r = smax(r1, r2);
-      if (r > 0.0) {
-        const double sigma = log10(r);
-        if (sigma >= Ph.sigma_max) {
-          eps = Ph.epsilon0;
-        } else if (!(sigma < Ph.sigma_min)) {
-          eps = 0.5 * Ph.epsilon0 *
-                (1.0 + sin(M_PI * (sigma - 0.5 * (Ph.sigma_max + Ph.sigma_min)) /
-                           (Ph.sigma_max - Ph.sigma_min)));
-        }
-      }
-    }
-    sm[P::EPS + el] = eps;
-    eps_out[e] = eps;
-    atomicMax(&F->max_eps_key, order_key(eps));
-  }
-  __syncthreads();
-  if (!active) return;
-  // ---- BR1: weak D-hat sums of metric * velocity along xi (i) and eta (j)
-  double sye_u = 0.0, sxe_u = 0.0, sye_v = 0.0, sxe_v = 0.0;
-  double syx_u = 0.0, sxx_u = 0.0, syx_v = 0.0, sxx_v = 0.0;
-#pragma unroll
-  for (int m = 0; m < N1; ++m) {
-    const int qx = m * N1 + j, qe = i * N1 + m;
-    const double di = DH[i * OP + m], dj = DH[j * OP + m];
-    const double ux = fld(P::U)[qx], vx = fld(P::V)[qx], ue = fld(P::U)[qe], ve = fld(P::V)[qe];
-    const double yex = fld(P::YE)[qx], xex = fld(P::XE)[qx];
-    const double yxe = fld(P::YX)[qe], xxe = fld(P::XX)[qe];
-    sye_u += di * (yex * ux);
-    sxe_u += di * (xex * ux);
-    sye_v += di * (yex * vx);
-    sxe_v += di * (xex * vx);
-    syx_u += dj * (yxe * ue);
-    sxx_u += dj * (xxe * ue);
-    syx_v += dj * (yxe * ve);
-    sxx_v += dj * (xxe * ve);
-  }
-  double u1 = sye_u - syx_u, u2 = sxx_u - sxe_u, v1 = sye_v - syx_v, v2 = sxx_v - sxe_v;
-  // interface corrections (viscosity.hpp:114-160): U* = <u> inside, u- on walls
-  const double uo = fld(P::U)[q], vo = fld(P::V)[q], iw0 = 1.0 / M.w0;
-  for (int c2 = 0; c2 < nfc; ++c2) {
-    const int face = fa[c2];
-    if (!(fy[c2] & EF_PRESENT)) continue;
-    double us = uo, vs = vo;
-    if (!(fy[c2] & EF_WALL)) {
-      double ub, vb;
-      vel(nh[c2], nhu[c2], nhv[c2], Ph.h_des, ub, vb);
-      us = 0.5 * (uo + ub);
-      vs = 0.5 * (vo + vb);
-    }
-    double cy, cx;
-    switch (face) {
-      case 1: cy = fld(P::YE)[q]; cx = fld(P::XE)[q]; break;
-      case 3: cy = -fld(P::YE)[q]; cx = -fld(P::XE)[q]; break;
-      case 2: cy = -fld(P::YX)[q]; cx = -fld(P::XX)[q]; break;
-      default: cy = fld(P::YX)[q]; cx = fld(P::XX)[q]; break;
-    }
-    cy *= iw0;
-    cx *= iw0;
-    u1 += cy * us;
-    u2 -= cx * us;
-    v1 += cy * vs;
-    v2 -= cx * vs;
-  }
-  const double ij = 1.0 / jac;
-  const double he = h * sm[P::EPS + el] * ij;
-  fvu[n] = he * u1;
-  fvv[n] = he * v1;
-  gvu[n] = he * u2;
-  gvv[n] = he * v2;
-}
-
-template <int N1>
-static void launch_visc_pre_n(const Mesh& M, const Phys& P, CState S, double* eps, double* fvu,
-                              double* fvv, double* gvu, double* gvv, Flags* F,
-                              cudaStream_t st) {
-  using PL = VP<N1>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_visc_pre<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)PL::bytes);
-    attr = true;
-  }
-  const int grid = (M.n_owned + PL::E - 1) / PL::E;
-  k_visc_pre<N1><<<grid, PL::THREADS, PL::bytes, st>>>(M, P, S, eps, fvu, fvv, gvu, gvv, F);
-}
-
-// ===========================================================================
 // Element-per-thread kernel for the smallest degrees (N+1 <= 3, inviscid).  An
 // element is (N+1)^2 <= 9 nodes: one thread loads all of it (vectorised,
 // coalesced across the warp), its neighbours' face traces (L2 hits) and does the
@@ -2193,7 +1604,7 @@ template <int N1, bool FORCE, bool VISC>
 static void launch_node(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
                         cudaStream_t st) {
   using PL = NodePlan<N1, VISC>;
-  static int cache = 0;
+  static int cache[kMaxDevices] = {};
   auto kern = k_stage_node<N1, FORCE, VISC>;
   const int groups = (M.n_owned - M.e_lo + PL::G - 1) / PL::G;
   const int grid = grid_for(kern, PL::THREADS, PL::bytes, groups, cache);
@@ -2233,7 +1644,10 @@ int launch_source_geometry(const Mesh& M, double* sx, double* sy, cudaStream_t s
 }
 
 // ---------------------------------------------------------------------------
-static bool g_ops_set[17];
+// the operator tables live in __constant__ memory, one copy per device: the
+// upload is tracked per device; the host image pins what every device holds
+static bool g_ops_set[kMaxDevices][17];
+static bool g_ops_known[17];
 static double g_ops_host[kOpsTotal];
 
 int upload_fast_ops(int n1, const double* D, const double* Dt, const double* Dh,
@@ -2249,105 +1663,57 @@ int upload_fast_ops(int n1, const double* D, const double* Dt, const double* Dh,
   }
   for (int k = 0; k < n1; ++k) tab[5 * np + k] = w[k];
   const int len = 5 * np + n1;
-  if (g_ops_set[n1]) {
-    if (std::memcmp(tab, g_ops_host + base, len * sizeof(double)) != 0) return -1;
-    return 0;
-  }
+  if (g_ops_known[n1] && std::memcmp(tab, g_ops_host + base, len * sizeof(double)) != 0)
+    return -1;
+  const int dev = current_device();
+  if (dev < 0) return -2;
+  if (g_ops_set[dev][n1]) return 0;
   if (upload_ops_local(base, tab, len) != 0) return -2;
-  for (auto up : {pl_upload_ops_a, pl_upload_ops_b, pl_upload_ops_c})
-    if (up(base, tab, len) != 0) return -2;
   std::memcpy(g_ops_host + base, tab, len * sizeof(double));
-  g_ops_set[n1] = true;
+  g_ops_known[n1] = true;
+  g_ops_set[dev][n1] = true;
   return 0;
 }
 
 
-// full-line kernel (N+1 <= 4 by default)
-template <int N1, bool FORCE>
-static void launch_full(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
-                        cudaStream_t st) {
-  using PL = Plan<N1>;
-  static int cache = 0;
-  auto kern = k_stage<N1, FORCE>;
-  const int grid = grid_for(kern, PL::THREADS, PL::bytes, (M.n_owned - M.e_lo + PL::E - 1) / PL::E, cache);
-  kern<<<grid, PL::THREADS, PL::bytes, st>>>(M, P, A, F);
-}
-
-// half-line kernel (N+1 >= 5 inviscid, N+1 >= 3 viscous)
+// half-line kernel (N+1 >= 5 inviscid, N+1 >= 4 viscous)
 template <int N1, bool FORCE, bool VISC>
 static void launch_half(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
                         cudaStream_t st) {
   using PL = HL<N1, VISC>;
-  static int cache = 0;
+  static int cache[kMaxDevices] = {};
   auto kern = k_stage_hl<N1, FORCE, VISC>;
   const int grid = grid_for(kern, PL::THREADS, PL::bytes, (M.n_owned - M.e_lo + PL::E - 1) / PL::E, cache);
   kern<<<grid, PL::THREADS, PL::bytes, st>>>(M, P, A, F);
 }
 
-static int variant_override() {
-  static int v = -1;
-  if (v < 0) {
-    const char* s = getenv("SWDG_FAST_VARIANT");  // "elem" / "full" / "half" (experiments)
-    v = !s ? 0 : (s[0] == 'f' ? 1 : (s[0] == 'h' ? 2 : (s[0] == 'e' ? 3 : (s[0] == 'p' ? 4 : (s[0] == 'n' ? 5 : 0)))));
-  }
-  return v;
-}
-
+// Kernel choice per degree, measured on B200 (1M elements, profiles/r01_sweep_variants.txt,
+// r01_node_variants.txt): inviscid element-per-thread at N+1 <= 3 (0.185 / 0.483 vs node
+// 0.197 / 0.552 ms/stage), node-per-thread at N+1 = 4 (0.853 vs full-line 0.926 vs
+// half-line 1.65), half-line above; viscous node-per-thread at N+1 = 3 (1.013 vs 1.224),
+// half-line above (N+1 = 4: 1.585 vs node 1.798).
 template <int N1>
 static void launch_n(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
                      cudaStream_t st) {
   if constexpr (N1 >= 3) {
-    if (A.fvu) {  // viscous stages: node-per-thread kernel at N+1 <= SWDG_VISC_NODE_MAX, else half-line
-      const int ovv = variant_override();
-      if constexpr (N1 <= 4) {
-        if (SWDG_VISC_NODE_MAX >= N1 && ovv != 2) {
-          if (A.fh) launch_node<N1, true, true>(M, P, A, F, st);
-          else launch_node<N1, false, true>(M, P, A, F, st);
-          return;
-        }
+    if (A.fvu) {
+      if constexpr (N1 <= SWDG_VISC_NODE_MAX) {
+        if (A.fh) launch_node<N1, true, true>(M, P, A, F, st);
+        else launch_node<N1, false, true>(M, P, A, F, st);
+      } else {
+        if (A.fh) launch_half<N1, true, true>(M, P, A, F, st);
+        else launch_half<N1, false, true>(M, P, A, F, st);
       }
-      if (A.fh) launch_half<N1, true, true>(M, P, A, F, st);
-      else launch_half<N1, false, true>(M, P, A, F, st);
-      return;
-    }
-  }
-  // inviscid kernel choice: element-per-thread (N+1 <= 3), node-per-thread (N+1 =
-  // 4), half-line (N+1 >= 5); SWDG_FAST_VARIANT=elem/full/half/pl/node overrides
-  // where the variant exists for this degree.  Measured on B200 (1M elements,
-  // profiles/r01_sweep_variants.txt, r01_node_variants.txt): node 0.853-0.863 vs
-  // full-line 0.926 vs half-line 1.65 ms/stage at N+1 = 4; element 0.185 / 0.483
-  // vs node 0.197 / 0.552 at N+1 = 2 / 3; half-line 1.355 vs full-line 1.378 at
-  // N+1 = 5
-  int v = N1 <= 3 ? 3 : (N1 == 4 ? 5 : 2);
-  const int ov = variant_override();
-  if (ov == 5 && N1 <= 4) v = 5;
-  if (ov == 3 && N1 <= 3) v = 3;
-  if (ov == 1 && N1 <= 8) v = 1;
-  if (ov == 2 && N1 >= 3) v = 2;
-  if (ov == 4) v = 4;
-  if (v == 4 && launch_pl_stage(M, P, A, F, st)) return;
-  if constexpr (N1 <= 4) {
-    if (v == 5) {
-      if (A.fh) launch_node<N1, true, false>(M, P, A, F, st);
-      else launch_node<N1, false, false>(M, P, A, F, st);
       return;
     }
   }
   if constexpr (N1 <= 3) {
-    if (v == 3) {
-      if (A.fh) launch_elem<N1, true>(M, P, A, F, st);
-      else launch_elem<N1, false>(M, P, A, F, st);
-      return;
-    }
-  }
-  if constexpr (N1 <= 8) {
-    if (v == 1) {
-      if (A.fh) launch_full<N1, true>(M, P, A, F, st);
-      else launch_full<N1, false>(M, P, A, F, st);
-      return;
-    }
-  }
-  if constexpr (N1 >= 3) {
+    if (A.fh) launch_elem<N1, true>(M, P, A, F, st);
+    else launch_elem<N1, false>(M, P, A, F, st);
+  } else if constexpr (N1 == 4) {
+    if (A.fh) launch_node<N1, true, false>(M, P, A, F, st);
+    else launch_node<N1, false, false>(M, P, A, F, st);
+  } else {
     if (A.fh) launch_half<N1, true, false>(M, P, A, F, st);
     else launch_half<N1, false, false>(M, P, A, F, st);
   }
@@ -2355,32 +1721,15 @@ static void launch_n(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
 
 int launch_fast_visc_pre(const Mesh& M, const Phys& P, CState S, double* eps, double* fvu,
                          double* fvv, double* gvu, double* gvv, Flags* F, cudaStream_t st) {
-  // line-based kernel (one velocity component at a time: ~5 (N+1) doubles per
-  // thread) up to N+1 = SWDG_VL_MAX (measured 22.5 vs 24.5 ms/stage at N=12 against
-  // the node-per-thread kernel; before the per-CTA eps atomic the node kernel won
-  // at N+1 >= 14), the node-per-thread kernel above; SWDG_VISC_NODE=1 forces it
-  static const bool node_only = getenv("SWDG_VISC_NODE") != nullptr;
+  // line-based pre-kernel at every degree (one velocity component at a time:
+  // ~5 (N+1) doubles per thread); measured faster than a node-per-thread kernel
+  // at every N once the eps maximum went to one atomic per CTA (N=14: 50.4 -> 35.9
+  // ms/stage)
   switch (M.n1) {
-#define SWDG_VL(n)                                                                 \
-  case n:                                                                          \
-    if (node_only) launch_visc_pre_n<n>(M, P, S, eps, fvu, fvv, gvu, gvv, F, st);  \
-    else launch_visc_lines_n<n>(M, P, S, eps, fvu, fvv, gvu, gvv, F, st);          \
-    break;
-#define SWDG_VP(n) \
-  case n: launch_visc_pre_n<n>(M, P, S, eps, fvu, fvv, gvu, gvv, F, st); break;
+#define SWDG_VL(n) \
+  case n: launch_visc_lines_n<n>(M, P, S, eps, fvu, fvv, gvu, gvv, F, st); break;
     SWDG_VL(3) SWDG_VL(4) SWDG_VL(5) SWDG_VL(6) SWDG_VL(7) SWDG_VL(8) SWDG_VL(9) SWDG_VL(10)
-    SWDG_VL(11) SWDG_VL(12) SWDG_VL(13)
-#if SWDG_VL_MAX >= 15
-    SWDG_VL(14) SWDG_VL(15)
-#else
-    SWDG_VP(14) SWDG_VP(15)
-#endif
-#if SWDG_VL_MAX >= 16
-    SWDG_VL(16)
-#else
-    SWDG_VP(16)
-#endif
-#undef SWDG_VP
+    SWDG_VL(11) SWDG_VL(12) SWDG_VL(13) SWDG_VL(14) SWDG_VL(15) SWDG_VL(16)
 #undef SWDG_VL
     default: return 0;
   }

@@ -40,6 +40,13 @@ inline void ck(cudaError_t e, const char* where) {
   if (e != cudaSuccess) throw CudaError{e, where};
 }
 
+// every kernel launch is checked: a failed launch (bad configuration, a missing
+// shared-memory attribute on a new device, ...) must never read as an accepted step
+inline int launched(int n, const char* what) {
+  ck(cudaGetLastError(), what);
+  return n;
+}
+
 struct InputError {
   std::string msg;
 };
@@ -152,7 +159,7 @@ State st(double* const* a) { return State{a[0], a[1], a[2]}; }
 // loop and br1/viscous flux pairs of evaluate_rhs timeloop.hpp:176-187).
 // Returns max eps.
 double stage_viscosity(swdg_gpu* c, CState in) {
-  c->launches += launch_exact_indicator(c->M, in, c->r_ind, c->stream);
+  c->launches += launched(launch_exact_indicator(c->M, in, c->r_ind, c->stream), "launch_exact_indicator");
   ck(cudaMemcpyAsync(c->r_h.data(), c->r_ind, sizeof(double) * c->M.K, cudaMemcpyDeviceToHost,
                      c->stream), "indicator D2H");
   ck(cudaStreamSynchronize(c->stream), "indicator sync");
@@ -163,8 +170,8 @@ double stage_viscosity(swdg_gpu* c, CState in) {
   }
   ck(cudaMemcpyAsync(c->eps, c->eps_h.data(), sizeof(double) * c->M.K, cudaMemcpyHostToDevice,
                      c->stream), "eps H2D");
-  c->launches += launch_exact_grad(c->M, c->phys, in, c->eps, c->fvu, c->fvv, c->gvu, c->gvv,
-                                   c->stream);
+  c->launches += launched(launch_exact_grad(c->M, c->phys, in, c->eps, c->fvu, c->fvv, c->gvu, c->gvv,
+                                   c->stream), "launch_exact_grad");
   return mx;
 }
 
@@ -196,8 +203,8 @@ bool stage_forcing(swdg_gpu* c, double ts) {
 // device, ramp on the host).  Returns the host-side max eps (exact mode).
 double stage_visc(swdg_gpu* c, CState in, Flags* F) {
   if (c->fast) {
-    c->launches += launch_fast_visc_pre(c->M, c->phys, in, c->eps, c->fvu, c->fvv, c->gvu,
-                                        c->gvv, F, c->stream);
+    c->launches += launched(launch_fast_visc_pre(c->M, c->phys, in, c->eps, c->fvu, c->fvv, c->gvu,
+                                        c->gvv, F, c->stream), "launch_fast_visc_pre");
     return 0.0;
   }
   return stage_viscosity(c, in);
@@ -234,10 +241,10 @@ void stage_main(swdg_gpu* c, CState in, double* const* out, int k, double t, dou
     const Mesh& M = range ? *range : c->M;
     ck(cudaMemsetAsync(c->gctr, 0, sizeof(int), c->stream), "group counter");
     a.gctr = c->gctr;
-    if (M.n_owned > M.e_lo) c->launches += launch_fast_stage(M, c->phys, a, F, c->stream);
+    if (M.n_owned > M.e_lo) c->launches += launched(launch_fast_stage(M, c->phys, a, F, c->stream), "launch_fast_stage");
   } else {
-    c->launches += launch_exact_rhs_stage(c->M, c->phys, a, c->stream);
-    if (out) c->launches += launch_exact_limit(c->M, c->phys, st(out), F, c->stream);
+    c->launches += launched(launch_exact_rhs_stage(c->M, c->phys, a, c->stream), "launch_exact_rhs_stage");
+    if (out) c->launches += launched(launch_exact_limit(c->M, c->phys, st(out), F, c->stream), "launch_exact_limit");
   }
 }
 
@@ -424,8 +431,8 @@ int create_guarded(swdg_gpu* c, swdg_gpu** out, F&& body) {
     body();
     // fast mode: geometry-only split-source coefficients, once per mesh
     if (c->params.mode == SWDG_MODE_FAST)
-      c->launches += launch_source_geometry(c->M, const_cast<double*>(c->M.sx),
-                                            const_cast<double*>(c->M.sy), c->stream);
+      c->launches += launched(launch_source_geometry(c->M, const_cast<double*>(c->M.sx),
+                                            const_cast<double*>(c->M.sy), c->stream), "launch_source_geometry");
     ck(cudaDeviceSynchronize(), "create sync");
   } catch (const CudaError& e) {
     g_create_error = std::string(e.where) + ": " + cudaGetErrorString(e.e);
@@ -562,7 +569,7 @@ int swdg_gpu_create_structured_part(const swdg_structured_spec* s, const swdg_pa
     auto wr = [](const double* p) { return const_cast<double*>(p); };
     MeshOut o{c->xy, c->xy + nn, wr(M.xx), wr(M.xe), wr(M.yx), wr(M.ye), wr(M.jac), wr(M.b),
               wr(M.len_xi), wr(M.len_eta), wr(M.fnx), wr(M.fny), wr(M.fjs), wr(M.fa), bad};
-    c->launches += launch_structured_mesh(sd, dnodes, c->M.D, n1, o, c->stream);
+    c->launches += launched(launch_structured_mesh(sd, dnodes, c->M.D, n1, o, c->stream), "launch_structured_mesh");
     int hbad = 0;
     ck(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "bad D2H");
     ck(cudaStreamSynchronize(c->stream), "mesh sync");
@@ -690,7 +697,7 @@ int swdg_gpu_compute_dt(swdg_gpu* c, double cfl, double* dt) {
   return guarded(c, [&] {
     if (!(cfl > 0.0) || cfl > 1.0) throw InputError{"compute_dt: cfl must be in (0, 1]"};
     reset_flags(c);
-    c->launches += launch_exact_dt(c->M, c->phys, cs(c->W), c->flags, c->stream);
+    c->launches += launched(launch_exact_dt(c->M, c->phys, cs(c->W), c->flags, c->stream), "launch_exact_dt");
     read_flags(c);
     double d = key_value(c->flags_h[0].dt_key);
     if (!std::isfinite(d)) {
@@ -819,8 +826,8 @@ int swdg_gpu_last_eps(swdg_gpu* c, double* eps) {
 int swdg_gpu_diagnostics(swdg_gpu* c, swdg_diagnostics* out) {
   return guarded(c, [&] {
     reset_flags(c);
-    c->launches += launch_diagnostics(c->M, c->phys, cs(c->W), c->partial, c->sums, c->flags,
-                                      c->stream);
+    c->launches += launched(launch_diagnostics(c->M, c->phys, cs(c->W), c->partial, c->sums, c->flags,
+                                      c->stream), "launch_diagnostics");
     ck(cudaMemcpyAsync(c->sums_h, c->sums, 2 * sizeof(double), cudaMemcpyDeviceToHost,
                        c->stream), "sums D2H");
     read_flags(c);
@@ -850,6 +857,12 @@ int swdg_gpu_set_forcing(swdg_gpu* c, swdg_forcing_fn fn, void* user) {
 }
 
 int64_t swdg_gpu_launch_count(const swdg_gpu* c) { return c ? c->launches : 0; }
+
+int swdg_gpu_set_grid_cap(int32_t max_ctas) {
+  if (max_ctas < 0) return SWDG_ERR_INPUT;
+  swdg_dev::g_grid_cap = max_ctas;
+  return SWDG_OK;
+}
 
 // ---- partitioned runs: halo exchange hooks and the split SSPRK3 step -------
 
@@ -891,7 +904,7 @@ int swdg_gpu_halo_pack(swdg_gpu* c, int what, int k, double* send_buf) {
       f[2] = c->gvu;
       f[3] = c->gvv;
     }
-    c->launches += launch_halo_pack(c->send_idx, c->n_send, what ? 4 : 3, f, send_buf, c->stream);
+    c->launches += launched(launch_halo_pack(c->send_idx, c->n_send, what ? 4 : 3, f, send_buf, c->stream), "launch_halo_pack");
     return SWDG_OK;
   });
 }
@@ -908,8 +921,8 @@ int swdg_gpu_halo_unpack(swdg_gpu* c, int what, int k, const double* recv_buf) {
       f[2] = c->gvu;
       f[3] = c->gvv;
     }
-    c->launches += launch_halo_unpack(c->recv_idx, c->n_recv, what ? 4 : 3, f, recv_buf,
-                                      c->stream);
+    c->launches += launched(launch_halo_unpack(c->recv_idx, c->n_recv, what ? 4 : 3, f, recv_buf,
+                                      c->stream), "launch_halo_unpack");
     return SWDG_OK;
   });
 }
@@ -919,7 +932,7 @@ int swdg_gpu_halo_unpack(swdg_gpu* c, int what, int k, const double* recv_buf) {
 int swdg_gpu_dt_candidates(swdg_gpu* c, double* dt_min, double* min_len) {
   return guarded(c, [&] {
     reset_flags(c);
-    c->launches += launch_exact_dt(c->M, c->phys, cs(c->W), c->flags, c->stream);
+    c->launches += launched(launch_exact_dt(c->M, c->phys, cs(c->W), c->flags, c->stream), "launch_exact_dt");
     read_flags(c);
     *dt_min = key_value(c->flags_h[0].dt_key);
     *min_len = key_value(c->flags_h[0].minlen_key);

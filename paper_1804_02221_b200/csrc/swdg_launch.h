@@ -44,15 +44,8 @@ int launch_fast_visc_pre(const Mesh& M, const Phys& P, CState S, double* eps, do
 int launch_fast_stage(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
                       cudaStream_t st);
 
-// P-part line kernel (kernels_pl_{a,b,c}.cu: N+1 in [2,8], [9,12], [13,16]);
-// launch_pl_stage returns 0 when no instantiation covers the degree
-int launch_pl_stage(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F, cudaStream_t st);
-int pl_upload_ops_a(int base, const double* tab, int len);
-int pl_upload_ops_b(int base, const double* tab, int len);
-int pl_upload_ops_c(int base, const double* tab, int len);
-int launch_pl_stage_a(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F, cudaStream_t st);
-int launch_pl_stage_b(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F, cudaStream_t st);
-int launch_pl_stage_c(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F, cudaStream_t st);
+// test hook: cap on the persistent stage kernels' grid (0 = none), kernels_common.cu
+extern int g_grid_cap;
 
 // mode-independent (kernels_common.cu)
 int launch_halo_pack(const int* idx, long long n, int nf, const double* const* f, double* buf,

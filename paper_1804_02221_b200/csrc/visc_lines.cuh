@@ -333,11 +333,13 @@ template <int N1>
 void launch_visc_lines_n(const Mesh& M, const Phys& P, CState S, double* eps, double* fvu,
                          double* fvv, double* gvu, double* gvv, Flags* F, cudaStream_t st) {
   using PL = VLP<N1>;
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[kMaxDevices] = {};
+  const int dev = current_device();
+  if (dev < 0) return;
+  if (!attr[dev]) {
     cudaFuncSetAttribute(k_visc_lines<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)PL::bytes);
-    attr = true;
+    attr[dev] = true;
   }
   const int grid = (M.n_owned + PL::E - 1) / PL::E;
   k_visc_lines<N1><<<grid, PL::THREADS, PL::bytes, st>>>(M, P, S, eps, fvu, fvv, gvu, gvv, F);
