@@ -18,6 +18,12 @@
  *                            min_positivity_dt            limiter.hpp:135-166
  *   swdg_gpu_last_eps        TimeIntegrator::last_eps     timeloop.hpp:192
  *   swdg_gpu_set_forcing     TimeIntegrator::forcing      timeloop.hpp:198 (ForcingFn dg_rhs.hpp:255)
+ *   swdg_gpu_set_track_limiter_entropy  TimeIntegrator::track_limiter_entropy timeloop.hpp:199
+ *   swdg_gpu_worst_limiter_entropy_jump TimeIntegrator::worst_limiter_entropy_jump timeloop.hpp:196,
+ *                            limited_entropy_check        limiter.hpp:88-101
+ *   swdg_gpu_step_device     one run_simulation loop body driver.hpp:91-127
+ *                            (try_step + total_mass/total_entropy/min_height/
+ *                            min_positivity_dt + the next compute_dt)
  *
  * Conventions
  *   - Return codes: SWDG_OK; SWDG_ERR_INPUT mirrors SwdgError (core.hpp:63);
@@ -36,6 +42,7 @@
 #ifndef SWDG_GPU_H
 #define SWDG_GPU_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -186,6 +193,28 @@ int swdg_gpu_last_info(swdg_gpu* ctx, swdg_step_info* info);
 int swdg_gpu_last_eps(swdg_gpu* ctx, double* eps);
 int swdg_gpu_diagnostics(swdg_gpu* ctx, swdg_diagnostics* out);
 
+/* TimeIntegrator::track_limiter_entropy (timeloop.hpp:199, post_stage :221-229):
+ * when on, every stage that limits records the worst per-element
+ * (e_after - e_before) / max(1, |e_before|) of limited_entropy_check
+ * (limiter.hpp:88-101); worst_limiter_entropy_jump returns the maximum over the
+ * context's life (starts at 0, timeloop.hpp:261).  Costs one dW/dt write and one
+ * element pass per stage while on. */
+int swdg_gpu_set_track_limiter_entropy(swdg_gpu* ctx, int on);
+int swdg_gpu_worst_limiter_entropy_jump(swdg_gpu* ctx, double* jump);
+
+/* The device-resident driver step (driver.hpp:91-127 without the host State):
+ * try_step of the device state, then, if accepted, the StepDiagnostics fields
+ * of the new state (total_mass, total_entropy, min_height, min_positivity_dt,
+ * field.hpp:39-68, limiter.hpp:135-166) and the next step's compute_dt(cfl)
+ * (timeloop.hpp:53-75).  Fast mode queues the reductions behind the three
+ * stages and synchronises once. */
+typedef struct swdg_step_report {
+  swdg_step_info info;
+  swdg_diagnostics diag; /* valid when info.accepted */
+  double next_dt;        /* compute_dt(new state, cfl); valid when info.accepted */
+} swdg_step_report;
+int swdg_gpu_step_device(swdg_gpu* ctx, double t, double dt, double cfl, swdg_step_report* out);
+
 /* Forcing: a host callback evaluated at the stage times t, t+dt, t+dt/2
  * (ssprk3_stage_times timeloop.hpp:82) and uploaded, or NULL to clear. */
 int swdg_gpu_set_forcing(swdg_gpu* ctx, swdg_forcing_fn fn, void* user);
@@ -264,6 +293,29 @@ int swdg_gpu_stage_visc(swdg_gpu* ctx, int stage, double t, double dt);
 int swdg_gpu_stage_run(swdg_gpu* ctx, int stage, double t, double dt);
 int swdg_gpu_step_flags(swdg_gpu* ctx, int32_t* reject, int32_t* abort);
 int swdg_gpu_step_commit(swdg_gpu* ctx, int accept, swdg_step_info* info);
+
+/* Asynchronous snapshot (driver.hpp:129-135 with the state on the device): copy
+ * the current device state into caller-owned host buffers on a copy stream
+ * (pinned buffers make it truly asynchronous), overlapping the following steps;
+ * the context fences the buffer before it is overwritten.  snapshot_wait blocks
+ * until the last copy has landed in host memory. */
+int swdg_gpu_snapshot_async(swdg_gpu* ctx, double* h, double* hu, double* hv);
+int swdg_gpu_snapshot_wait(swdg_gpu* ctx);
+/* Page-locked host memory for snapshot buffers (NULL on failure). */
+void* swdg_gpu_alloc_pinned(size_t bytes);
+void swdg_gpu_free_pinned(void* p);
+
+/* Stage buffers of the split step: stage k reads W (k = 0), A (k = 1) or B
+ * (k = 2) and writes A (k = 0, 2) or B (k = 1), W^n staying in W.  With
+ * upload_state (W^n) and upload_stage_input a single stage can be run from any
+ * input (step_begin; stage_visc; stage_run) and its kernel-written output --
+ * update, SSPRK3 combine, limiter, dry-node cut -- downloaded; stage_info is
+ * that stage's report (n_limited, min h after limiting, max eps, accepted = no
+ * negative element mean). */
+int swdg_gpu_upload_stage_input(swdg_gpu* ctx, int stage, const double* h, const double* hu,
+                                const double* hv);
+int swdg_gpu_download_stage_output(swdg_gpu* ctx, int stage, double* h, double* hu, double* hv);
+int swdg_gpu_stage_info(swdg_gpu* ctx, int stage, swdg_step_info* info);
 
 /* Overlap of the halo exchange with interior work.  set_interior names an
  * owned element range [lo, hi) none of whose faces touches a ghost element

@@ -8,7 +8,8 @@
 //
 // Same member functions, same return values, same exceptions (SwdgError for
 // bad input, NumericalAbort when the limiter is off and a stage goes
-// negative).  Link with paper_1804_02221_b200/_lib/libswdg_gpu.so.
+// negative), including the public `forcing` and `track_limiter_entropy` members
+// and worst_limiter_entropy_jump().  Link with paper_1804_02221_b200/_lib/libswdg_gpu.so.
 #pragma once
 
 #include <cstring>
@@ -80,8 +81,10 @@ class TimeIntegrator {
   // timeloop.hpp:156-170
   bool try_step(State& w, double t, double dt) {
     sync_forcing();
+    sync_tracking();
     check(swdg_gpu_upload_state(ctx_, w.h.data(), w.hu.data(), w.hv.data()));
     check(swdg_gpu_try_step(ctx_, t, dt, &info_));
+    evaluated();
     if (info_.accepted) check(swdg_gpu_download_state(ctx_, w.h.data(), w.hu.data(), w.hv.data()));
     return info_.accepted != 0;
   }
@@ -92,18 +95,66 @@ class TimeIntegrator {
     out.resize(s.n_elem, s.n1);
     check(swdg_gpu_upload_state(ctx_, s.h.data(), s.hu.data(), s.hv.data()));
     check(swdg_gpu_evaluate_rhs(ctx_, t, out.h.data(), out.hu.data(), out.hv.data()));
+    evaluated();
   }
 
-  const std::vector<double>& last_eps() {
-    eps_.resize(mesh_.n_elements());
-    check(swdg_gpu_last_eps(ctx_, eps_.data()));
+  // timeloop.hpp:192 (const like the reference).  Like the reference's eps_, it
+  // is empty until a viscous evaluation has run (compute_viscosity fills it,
+  // timeloop.hpp:179) and is read back once per evaluation into a cache.
+  const std::vector<double>& last_eps() const {
+    if (eps_stale_) {
+      eps_.resize(mesh_.n_elements());
+      check(swdg_gpu_last_eps(ctx_, eps_.data()));
+      eps_stale_ = false;
+    }
     return eps_;
   }
   int last_limited_count() const { return info_.n_limited; }
   double last_max_eps() const { return info_.max_eps; }
   double last_min_stage_h() const { return info_.min_stage_h; }
+  double worst_limiter_entropy_jump() const {
+    double v = 0.0;
+    check(swdg_gpu_worst_limiter_entropy_jump(ctx_, &v));
+    return v;
+  }
 
-  ForcingFn forcing;  // dg_rhs.hpp:255, evaluated on the host per stage
+  ForcingFn forcing;                   // dg_rhs.hpp:255, evaluated on the host per stage
+  bool track_limiter_entropy = false;  // timeloop.hpp:199 (limited_entropy_check on the device)
+
+  // ---- device-resident surface (no reference counterpart): the state stays on
+  // the device between steps; see swdg_gpu_driver.hpp
+  void upload(const State& w) {
+    check(swdg_gpu_upload_state(ctx_, w.h.data(), w.hu.data(), w.hv.data()));
+  }
+  void download(State& w) const {
+    w.resize(mesh_.n_elements(), mesh_.n1());
+    check(swdg_gpu_download_state(ctx_, w.h.data(), w.hu.data(), w.hv.data()));
+  }
+  double compute_dt_device(double cfl) {
+    double dt = 0.0;
+    check(swdg_gpu_compute_dt(ctx_, cfl, &dt));
+    return dt;
+  }
+  swdg_diagnostics diagnostics_device() {
+    swdg_diagnostics d{};
+    check(swdg_gpu_diagnostics(ctx_, &d));
+    return d;
+  }
+  // try_step of the device state + the new state's diagnostics and next CFL dt
+  swdg_step_report step_device(double t, double dt, double cfl) {
+    sync_forcing();
+    sync_tracking();
+    swdg_step_report r{};
+    check(swdg_gpu_step_device(ctx_, t, dt, cfl, &r));
+    evaluated();
+    info_ = r.info;
+    return r;
+  }
+  void snapshot_async(double* h, double* hu, double* hv) {
+    check(swdg_gpu_snapshot_async(ctx_, h, hu, hv));
+  }
+  void snapshot_wait() { check(swdg_gpu_snapshot_wait(ctx_)); }
+  const Mesh& mesh() const { return mesh_; }
 
  private:
   static void forcing_tramp(void* user, double t, int64_t count, const double* x,
@@ -114,6 +165,17 @@ class TimeIntegrator {
       fh[n] = f.h;
       fhu[n] = f.hu;
       fhv[n] = f.hv;
+    }
+  }
+  // a viscous evaluation refreshed eps on the device (only the ES scheme with
+  // viscosity computes it, timeloop.hpp:178)
+  void evaluated() {
+    if (cfg_.visc.enabled && cfg_.mode == SchemeMode::es) eps_stale_ = true;
+  }
+  void sync_tracking() {
+    if (track_limiter_entropy != tracking_set_) {
+      check(swdg_gpu_set_track_limiter_entropy(ctx_, track_limiter_entropy ? 1 : 0));
+      tracking_set_ = track_limiter_entropy;
     }
   }
   void sync_forcing() {
@@ -128,7 +190,7 @@ class TimeIntegrator {
     if (rc == SWDG_ERR_INPUT) throw SwdgError(msg);
     throw std::runtime_error(std::string("swdg_gpu: ") + msg);
   }
-  void check(int rc) {
+  void check(int rc) const {
     if (rc != SWDG_OK) raise(rc, swdg_gpu_last_error(ctx_));
   }
 
@@ -137,8 +199,10 @@ class TimeIntegrator {
   std::vector<swdg_face> faces_;
   swdg_gpu* ctx_ = nullptr;
   swdg_step_info info_{};
-  std::vector<double> eps_;
+  mutable std::vector<double> eps_;
+  mutable bool eps_stale_ = false;
   bool forcing_set_ = false;
+  bool tracking_set_ = false;
 };
 
 }  // namespace gpu

@@ -87,6 +87,9 @@ def lib():
             "ref_br1_gradients": (C.c_int, [vp, _dp, _dp, _dp, _dp, _dp, _dp]),
             "ref_viscous_lhs": (C.c_int, [vp] + [_dp] * 10),
             "ref_limit_all": (C.c_int, [vp, C.POINTER(Params), _dp, _dp, _dp, C.c_int, _dp]),
+            "ref_mms_error": (C.c_int, [vp, C.POINTER(Params), C.c_double, C.c_double, _dp,
+                                        _dp, C.POINTER(C.c_int64)]),
+            "ref_bench_rough_state": (C.c_int, [C.c_int, C.c_long, _dp, _dp, _dp]),
             "ref_run_simulation": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_double,
                                              C.c_double, _dp, _dp, _dp,
                                              C.POINTER(C.c_int64), _dp]),
@@ -225,6 +228,34 @@ def assemble_rhs(m: RefMesh, p: Params, state, t=0.0, mode=0):
     out = [np.zeros(m.n_nodes) for _ in range(3)]
     check(lib().ref_assemble_rhs(m.handle, C.byref(p), mode, *(ptr(a) for a in state), t,
                                  *(ptr(a) for a in out)))
+    return out
+
+
+def limit_all(m: RefMesh, p: Params, state, zero_dry=True):
+    """limit_element (limiter.hpp:43-84) on every element, in place; returns theta."""
+    theta = np.zeros(m.n_elem)
+    check(lib().ref_limit_all(m.handle, C.byref(p), *(ptr(a) for a in state), int(zero_dry),
+                              ptr(theta)))
+    return theta
+
+
+MMS_WAVE = (2.0, 0.2, 0.7, 0.3, 2.0 * np.pi, 9.81)  # validate.hpp:543-546 (h0, amp, u0, v0, k, g)
+
+
+def mms_error(m: RefMesh, p: Params, cfl=0.4, t_end=0.2, wave=MMS_WAVE):
+    """crit_convergence's run (validate.hpp:560-595) on mesh m: (L2(h) error, steps)."""
+    fp = np.array(wave, np.float64)
+    err, steps = C.c_double(), C.c_int64()
+    check(lib().ref_mms_error(m.handle, C.byref(p), cfl, t_end, ptr(fp), C.byref(err),
+                              C.byref(steps)))
+    return err.value, steps.value
+
+
+def bench_rough_state(degree: int, n_elem: int):
+    """bench.hpp:108-121: the mt19937(20250810) rough field the reference benchmarks on."""
+    n = n_elem * (degree + 1) ** 2
+    out = [np.zeros(n) for _ in range(3)]
+    check(lib().ref_bench_rough_state(degree, n_elem, *(ptr(a) for a in out)))
     return out
 
 

@@ -12,6 +12,7 @@
 #include <string>
 #include <vector>
 
+#include "swdg/bench.hpp"
 #include "swdg/driver.hpp"
 #include "swdg/validate.hpp"
 #include "../include/swdg_gpu.h"
@@ -486,6 +487,69 @@ int ref_run_simulation(const char* id, int kx, int ky, int degree, double final_
     from_state(r.state, h, hu, hv);
     *steps = r.steps;
     *t_out = r.t;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// crit_convergence's run (validate.hpp:560-595) on the mesh `mh`: the traveling
+// wave h0 + amp sin(k(x+y) - omega t), (u0, v0) as the initial state, the
+// reference TimeIntegrator with the manufactured forcing, CFL steps
+// min(compute_dt, t_end - t) to t_end, then the J-weighted L2 error of h.
+int ref_mms_error(void* mh, const swdg_params* p, double cfl, double t_end, const double* fp,
+                  double* err, int64_t* steps) {
+  try {
+    const Mesh& mesh = static_cast<RefMesh*>(mh)->mesh;
+    const RunConfig cfg = make_cfg(mesh, p);
+    const double h0 = fp[0], amp = fp[1], u0 = fp[2], v0 = fp[3], k = fp[4];
+    const double omega = k * (u0 + v0);
+    auto h_exact = [&](double x, double y, double t) {
+      return h0 + amp * std::sin(k * (x + y) - omega * t);
+    };
+    State s;
+    s.resize(mesh.n_elements(), mesh.n1());
+    for (int n = 0; n < s.size(); ++n) {
+      const double h = h_exact(mesh.geom.x[n], mesh.geom.y[n], 0.0);
+      s.set(n, {h, h * u0, h * v0});
+    }
+    TimeIntegrator integ(mesh, cfg);
+    integ.forcing = wave_forcing(fp);
+    double t = 0.0;
+    int64_t n_steps = 0;
+    while (t < t_end - 1e-13) {
+      double dt = std::min(compute_dt(s, mesh, cfg.phys, cfl), t_end - t);
+      if (!integ.try_step(s, t, dt)) throw SwdgError("convergence run: step rejected");
+      t += dt;
+      ++n_steps;
+    }
+    double err2 = 0.0;
+    const int n1 = mesh.n1();
+    for (int e = 0; e < mesh.n_elements(); ++e)
+      for (int i = 0; i < n1; ++i)
+        for (int j = 0; j < n1; ++j) {
+          const int n = mesh.geom.node(e, i, j);
+          const double d = s.h[n] - h_exact(mesh.geom.x[n], mesh.geom.y[n], t);
+          err2 += d * d * mesh.geom.jac[n] * mesh.ops.weights[i] * mesh.ops.weights[j];
+        }
+    *err = std::sqrt(err2);
+    *steps = n_steps;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// The rough synthetic state of the reference's kernel benchmark
+// (bench.hpp:108-121, bench::KernelBuffers::init): std::mt19937(20250810),
+// h ~ U(0.5, 2), hu = h U(-1, 1), hv = h U(-1, 1), node-major over k elements.
+int ref_bench_rough_state(int degree, long k, double* h, double* hu, double* hv) {
+  try {
+    bench::KernelBuffers kb;
+    kb.init(degree, k);
+    std::copy(kb.h.begin(), kb.h.end(), h);
+    std::copy(kb.hu.begin(), kb.hu.end(), hu);
+    std::copy(kb.hv.begin(), kb.hv.end(), hv);
     return 0;
   } catch (const std::exception& e) {
     return fail(e);

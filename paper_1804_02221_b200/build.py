@@ -28,6 +28,7 @@ SOURCES = {
     "swdg_gpu.cu": [],
     "kernels_exact.cu": ["--fmad=false"],
     "kernels_common.cu": [],
+    "kernels_step.cu": ["--fmad=false"],
     "kernels_fast.cu": [],
     "kernels_mesh.cu": [],
     "host_mesh.cpp": [],

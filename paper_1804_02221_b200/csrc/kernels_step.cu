@@ -1,0 +1,348 @@
+// kernels_step.cu — per-step reductions of the device-resident driver, the
+// positivity time-step bound (limiter.hpp:107-166) and the limiter entropy
+// diagnostic, sm_100a FP64, compiled with --fmad=false (every per-node
+// expression rounds like the reference's Release build).
+//
+//   k_step_sums    one coalesced pass over the nodes: total_mass, total_entropy
+//                  (field.hpp:39-61) as fixed-order block partials, min_height
+//                  (field.hpp:63-67) and the compute_dt candidates
+//                  (timeloop.hpp:53-75) as order-independent minima.
+//   k_step_final   the block partials in a fixed tree order (reproducible).
+//   k_limiter_entropy  limited_entropy_check (limiter.hpp:88-101) for the
+//                  elements post_stage limited (timeloop.hpp:221-229): the
+//                  pre-limit stage state is rebuilt from the stage input, W^n
+//                  and the stage's dW/dt with the reference's axpy/combine
+//                  (timeloop.hpp:114-127), theta recomputed as limit_element
+//                  does (limiter.hpp:43-84).
+//
+// The node pass reads h, hu, hv, J, b and the two CFL lengths once (56 B per
+// node, 16-byte vector loads); a grid of a fixed number of CTAs makes the
+// partial sums independent of the device, so a run is bitwise repeatable.
+#include <cuda_runtime.h>
+
+#include "swdg_device.cuh"
+#include "swdg_launch.h"
+
+namespace swdg_dev {
+namespace {
+
+constexpr int kSumThreads = 256;
+constexpr int kSumBlocks = 148 * 8;  // fixed: the partial-sum order must not depend on the device
+
+__device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
+__device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
+
+// phys::velocity (physics.hpp:23-36)
+__device__ __forceinline__ void velocity(double h, double hu, double hv, double h_des,
+                                         double& u, double& v) {
+  if (h >= h_des) {
+    u = hu / h;
+    v = hv / h;
+  } else {
+    u = 0.0;
+    v = 0.0;
+  }
+}
+
+// phys::entropy (physics.hpp:47-62): h(u^2+v^2)/2 + g h^2/2 + g h b
+__device__ __forceinline__ double entropy(double h, double hu, double hv, double b,
+                                          const Phys& P) {
+  double u, v;
+  velocity(h, hu, hv, P.h_des, u, v);
+  const double k = 0.5 * h * (u * u + v * v);
+  return k + 0.5 * P.g * h * h + P.g * h * b;
+}
+
+// fixed-order block sum of two values (valid in thread 0)
+__device__ __forceinline__ void block_sum2(double& a, double& b) {
+  __shared__ double s[2][32];
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_down_sync(0xffffffffu, a, o);
+    b += __shfl_down_sync(0xffffffffu, b, o);
+  }
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+    s[0][w] = a;
+    s[1][w] = b;
+  }
+  __syncthreads();
+  if (w == 0) {
+    a = (int)threadIdx.x < nw ? s[0][threadIdx.x] : 0.0;
+    b = (int)threadIdx.x < nw ? s[1][threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_down_sync(0xffffffffu, a, o);
+      b += __shfl_down_sync(0xffffffffu, b, o);
+    }
+  }
+}
+
+struct NodeAcc {
+  double mass = 0.0, ent = 0.0;
+  unsigned long long kmin = ~0ull, kdt = ~0ull, klen = ~0ull;
+};
+
+__device__ __forceinline__ void node_terms(const Mesh& M, const Phys& P, double order, int n,
+                                           double h, double hu, double hv, double jac,
+                                           double b, double lxi, double leta, NodeAcc& acc) {
+  const int loc = n % M.np, i = loc / M.n1, j = loc - i * M.n1;
+  const double wi = M.w[i], wj = M.w[j];
+  // total_mass: sum += h * J * w_i * w_j; total_entropy: e * J * w_i * w_j
+  acc.mass += h * jac * wi * wj;
+  acc.ent += entropy(h, hu, hv, b, P) * jac * wi * wj;
+  const unsigned long long kh = order_key(h);
+  acc.kmin = kh < acc.kmin ? kh : acc.kmin;
+  // compute_dt per node (timeloop.hpp:58-71), lengths precomputed with glibc hypot
+  double u, v;
+  velocity(h, hu, hv, P.h_des, u, v);
+  const double c = sqrt(P.g * smax(h, 0.0));
+  double dt = __longlong_as_double(0x7ff0000000000000ll);
+  const double lx = fabs(u) + c, ly = fabs(v) + c;
+  if (lx > 1e-14) dt = smin(dt, lxi / (order * lx));
+  if (ly > 1e-14) dt = smin(dt, leta / (order * ly));
+  const unsigned long long a = order_key(dt), l = order_key(smin(lxi, leta));
+  acc.kdt = a < acc.kdt ? a : acc.kdt;
+  acc.klen = l < acc.klen ? l : acc.klen;
+}
+
+__global__ void __launch_bounds__(kSumThreads) k_step_sums(Mesh M, Phys P, CState S,
+                                                           double* partial, Flags* F) {
+  const int nn = M.n_owned * M.np;  // int32 node indices (checked at create)
+  const double order = 2.0 * M.degree + 1.0;
+  NodeAcc acc;
+  // pairs of nodes per thread (16-byte loads): arrays are 16-byte aligned and
+  // every element block has an even length when np is even; odd np takes the
+  // scalar loop
+  const int stride = gridDim.x * blockDim.x;
+  const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
+  if ((M.np & 1) == 0) {
+    const int np2 = nn / 2;
+    for (int q = t0; q < np2; q += stride) {
+      const double2 h = __ldg(reinterpret_cast<const double2*>(S.h) + q);
+      const double2 hu = __ldg(reinterpret_cast<const double2*>(S.hu) + q);
+      const double2 hv = __ldg(reinterpret_cast<const double2*>(S.hv) + q);
+      const double2 j = __ldg(reinterpret_cast<const double2*>(M.jac) + q);
+      const double2 b = __ldg(reinterpret_cast<const double2*>(M.b) + q);
+      const double2 lx = __ldg(reinterpret_cast<const double2*>(M.len_xi) + q);
+      const double2 le = __ldg(reinterpret_cast<const double2*>(M.len_eta) + q);
+      node_terms(M, P, order, 2 * q, h.x, hu.x, hv.x, j.x, b.x, lx.x, le.x, acc);
+      node_terms(M, P, order, 2 * q + 1, h.y, hu.y, hv.y, j.y, b.y, lx.y, le.y, acc);
+    }
+  } else {
+    for (int n = t0; n < nn; n += stride)
+      node_terms(M, P, order, n, __ldg(S.h + n), __ldg(S.hu + n), __ldg(S.hv + n),
+                 __ldg(M.jac + n), __ldg(M.b + n), __ldg(M.len_xi + n), __ldg(M.len_eta + n),
+                 acc);
+  }
+  block_sum2(acc.mass, acc.ent);
+  if (threadIdx.x == 0) {
+    partial[2 * blockIdx.x] = acc.mass;
+    partial[2 * blockIdx.x + 1] = acc.ent;
+  }
+  const unsigned long long kmin = block_min_key(acc.kmin);
+  const unsigned long long kdt = block_min_key(acc.kdt);
+  const unsigned long long klen = block_min_key(acc.klen);
+  if (threadIdx.x == 0) {
+    if (kmin != ~0ull) atomicMin(&F->min_h_key, kmin);
+    if (kdt != ~0ull) atomicMin(&F->dt_key, kdt);
+    if (klen != ~0ull) atomicMin(&F->minlen_key, klen);
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_step_final(const double* partial, int nparts,
+                                                     double* out2) {
+  double a = 0.0, b = 0.0;
+  for (int k = threadIdx.x; k < nparts; k += blockDim.x) {
+    a += partial[2 * k];
+    b += partial[2 * k + 1];
+  }
+  block_sum2(a, b);
+  if (threadIdx.x == 0) {
+    out2[0] = a;
+    out2[1] = b;
+  }
+}
+
+// limited_entropy_check for the elements this stage limited; the worst jump
+// (e1 - e0) / max(1, |e0|) goes to *key (order key, atomicMax).  A rejected
+// stage never reaches the limiter in the reference (post_stage returns first),
+// so nothing is recorded for it.
+__global__ void k_limiter_entropy(Mesh M, Phys P, StageArgs A, const Flags* F,
+                                  unsigned long long* key) {
+  const int e = M.e_lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= M.n_owned || !P.limiter) return;
+  if (*(volatile const int*)&F->reject) return;
+  const int n1 = M.n1, np = M.np;
+  const long long b0 = (long long)e * np;
+  // the pre-limit stage state: W + dt R, then a W^n + b (.) for stages 2-3
+  auto pre = [&](long long n, double& h, double& hu, double& hv) {
+    h = A.in.h[n];
+    hu = A.in.hu[n];
+    hv = A.in.hv[n];
+    h += A.dt * A.rhs.h[n];
+    hu += A.dt * A.rhs.hu[n];
+    hv += A.dt * A.rhs.hv[n];
+    if (A.stage > 0) {
+      h = A.ca * A.wn.h[n] + A.cb * h;
+      hu = A.ca * A.wn.hu[n] + A.cb * hu;
+      hv = A.ca * A.wn.hv[n] + A.cb * hv;
+    }
+  };
+  double area = 0.0, a0 = 0.0, mmin = 0.0;
+  for (int i = 0; i < n1; ++i)
+    for (int j = 0; j < n1; ++j) {
+      const long long n = b0 + i * n1 + j;
+      double h, hu, hv;
+      pre(n, h, hu, hv);
+      const double w = M.jac[n] * M.w[i] * M.w[j];
+      area += w;
+      a0 += w * h;
+      mmin = (i == 0 && j == 0) ? h : smin(mmin, h);
+    }
+  const double avg0 = (1.0 / area) * a0;
+  if (avg0 < 0.0 || !(mmin < 0.0)) return;
+  const double denom = avg0 - mmin;
+  const double theta = denom < 1e-14 ? 1.0 : smin(1.0, avg0 / denom);
+  if (!(theta < 1.0)) return;
+  double e_before = 0.0, e_after = 0.0;
+  for (int i = 0; i < n1; ++i)
+    for (int j = 0; j < n1; ++j) {
+      const long long n = b0 + i * n1 + j;
+      double h, hu, hv;
+      pre(n, h, hu, hv);
+      const double w = M.jac[n] * M.w[i] * M.w[j];
+      const double bn = M.b[n];
+      e_before += w * entropy(h, hu, hv, bn, P);
+      e_after += w * entropy(A.out.h[n], A.out.hu[n], A.out.hv[n], bn, P);
+    }
+  const double jump = (e_after - e_before) / smax(1.0, fabs(e_before));
+  atomicMax(key, order_key(jump));
+}
+
+// positivity_dt_bounds (limiter.hpp:107-130) evaluated by every owned
+// element-face node from its own side (the reference evaluates the minus side
+// and, for interior faces, the plus side with the plus normal: the same set).
+__device__ __forceinline__ double posdt_bound(const Mesh& M, const Phys& P, const CState& S,
+                                               long long idx);
+
+__global__ void k_posdt(Mesh M, Phys P, CState S, Flags* F) {
+  unsigned long long key = ~0ull;
+  const long long nf = (long long)M.n_owned * 4 * M.n1;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < nf;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long k = order_key(posdt_bound(M, P, S, idx));
+    key = k < key ? k : key;
+  }
+  key = block_min_key(key);  // one atomic per block
+  if (threadIdx.x == 0) atomicMin(&F->posdt_key, key);
+}
+
+__device__ __forceinline__ double posdt_bound(const Mesh& M, const Phys& P, const CState& S,
+                                               long long idx) {
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  const int n1 = M.n1;
+  const int t = (int)(idx % n1);
+  const int face = (int)((idx / n1) % 4);
+  const int e = (int)(idx / (4 * n1));
+  const int4 ef = M.ef[e * 4 + face];
+  if (!(ef.y & EF_PRESENT)) return inf;
+  const long long n = (long long)e * M.np + face_node(n1, face, t);
+  const double nx = M.fnx[idx], ny = M.fny[idx], a_scale = M.fa[idx];
+  const double hm = S.h[n], hum = S.hu[n], hvm = S.hv[n];
+  double hp, hup, hvp;
+  if (ef.y & EF_WALL) {
+    const double mn = hum * nx + hvm * ny;
+    hp = hm;
+    hup = hum - 2.0 * mn * nx;
+    hvp = hvm - 2.0 * mn * ny;
+  } else {
+    const int nf = ef.y & EF_NBR_FACE_MASK;
+    const int tp = (ef.y & EF_REVERSED) ? M.degree - t : t;
+    const long long nb = (long long)ef.x * M.np + face_node(n1, nf, tp);
+    hp = S.h[nb];
+    hup = S.hu[nb];
+    hvp = S.hv[nb];
+  }
+  double um, vm, up, vp;
+  velocity(hm, hum, hvm, P.h_des, um, vm);
+  velocity(hp, hup, hvp, P.h_des, up, vp);
+  const double unm = nx * um + ny * vm, unp = nx * up + ny * vp;
+  const double uavg = 0.5 * (unm + unp);
+  const double cavg = 0.5 * (sqrt(P.g * smax(hm, 0.0)) + sqrt(P.g * smax(hp, 0.0)));
+  const double a = fabs(uavg + cavg) + fabs(uavg - cavg);
+  const double bb = fabs(uavg + cavg) - fabs(uavg - cavg);
+  const double den1 = a + 2.0 * uavg;
+  double bound = den1 > 1e-300 ? M.w0 * a_scale / den1 : inf;
+  const double jump = unp - unm;
+  if (hm > 0.0 && bb * jump < 0.0)
+    bound = smin(bound, fabs(M.w0 * a_scale * P.g * hm / (cavg * bb * jump)));
+  return bound;
+}
+
+// total_mass / total_entropy in the reference's own order (field.hpp:39-61: one
+// serial sum over e, i, j): exact mode's diagnostics are then bitwise the
+// reference's.  One warp: the lanes form 32 consecutive terms, lane 0 adds them
+// in node order.
+__global__ void __launch_bounds__(32) k_serial_sums(Mesh M, Phys P, CState S, double* out2) {
+  const int nn = M.n_owned * M.np;
+  const int lane = threadIdx.x;
+  double mass = 0.0, ent = 0.0;
+  for (int base = 0; base < nn; base += 32) {
+    const int n = base + lane;
+    double tm = 0.0, te = 0.0;
+    if (n < nn) {
+      const int loc = n % M.np, i = loc / M.n1, j = loc - i * M.n1;
+      const double jac = M.jac[n], wi = M.w[i], wj = M.w[j], h = S.h[n];
+      tm = h * jac * wi * wj;
+      te = entropy(h, S.hu[n], S.hv[n], M.b[n], P) * jac * wi * wj;
+    }
+    const int cnt = nn - base < 32 ? nn - base : 32;
+    for (int k = 0; k < cnt; ++k) {
+      const double a = __shfl_sync(0xffffffffu, tm, k);
+      const double b = __shfl_sync(0xffffffffu, te, k);
+      mass += a;
+      ent += b;
+    }
+  }
+  if (lane == 0) {
+    out2[0] = mass;
+    out2[1] = ent;
+  }
+}
+
+}  // namespace
+
+int step_sum_partials() { return kSumBlocks; }
+
+int launch_step_sums(const Mesh& M, const Phys& P, CState S, double* partial, double* out2,
+                     Flags* F, cudaStream_t st) {
+  k_step_sums<<<kSumBlocks, kSumThreads, 0, st>>>(M, P, S, partial, F);
+  k_step_final<<<1, 1024, 0, st>>>(partial, kSumBlocks, out2);
+  return 2;
+}
+
+// StepDiagnostics reductions of a state (driver.hpp:117-127): mass, entropy,
+// min h and the CFL candidates, then the positivity bound.  serial = the
+// reference's summation order (exact mode).
+int launch_diagnostics(const Mesh& M, const Phys& P, CState S, double* partial, double* out2,
+                       Flags* F, cudaStream_t st, bool serial) {
+  int n = launch_step_sums(M, P, S, partial, out2, F, st);
+  if (serial) {
+    k_serial_sums<<<1, 32, 0, st>>>(M, P, S, out2);
+    ++n;
+  }
+  const long long nf = (long long)M.n_owned * 4 * M.n1;
+  const long long pb = (nf + 255) / 256;
+  k_posdt<<<(unsigned)(pb < 148 * 16 ? pb : 148 * 16), 256, 0, st>>>(M, P, S, F);
+  return n + 1;
+}
+
+int launch_limiter_entropy(const Mesh& M, const Phys& P, const StageArgs& A, const Flags* F,
+                           unsigned long long* key, cudaStream_t st) {
+  const int ne = M.n_owned - M.e_lo;
+  if (ne <= 0) return 0;
+  k_limiter_entropy<<<(ne + 127) / 128, 128, 0, st>>>(M, P, A, F, key);
+  return 1;
+}
+
+}  // namespace swdg_dev

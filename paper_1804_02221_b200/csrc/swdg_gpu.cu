@@ -50,6 +50,13 @@ inline int launched(int n, const char* what) {
 struct InputError {
   std::string msg;
 };
+
+constexpr int kDiagFlags = 3;  // Flags slot of the step reductions (0-2: stages)
+
+struct Report {
+  Flags f[4];
+  double sums[2];  // total_mass, total_entropy
+};
 }  // namespace
 
 struct swdg_gpu {
@@ -77,10 +84,24 @@ struct swdg_gpu {
   double *partial = nullptr, *sums = nullptr;
   int int_lo = 0, int_hi = 0;   // interior element range (halo overlap), empty by default
   int* gctr = nullptr;          // device group counter of the persistent stage kernels
-  Flags* flags = nullptr;       // device, 3 (one per stage)
-  Flags* flags_init = nullptr;  // device, reset image
-  Flags* flags_h = nullptr;     // pinned host mirror, 3
-  double* sums_h = nullptr;     // pinned
+  // device report: Flags[4] (one per stage + one for the step reductions) and the
+  // mass/entropy sums, contiguous so one copy (one host sync) reads a whole step
+  Report* rep = nullptr;        // device
+  Report* rep_h = nullptr;      // pinned host mirror
+  Flags* flags = nullptr;       // rep->f
+  Flags* flags_init = nullptr;  // device, reset image (4)
+  Flags* flags_h = nullptr;     // rep_h->f
+  double* sums_h = nullptr;     // rep_h->sums
+  // TimeIntegrator::track_limiter_entropy (timeloop.hpp:197): the worst
+  // per-element limiter entropy jump, accumulated over the context's life
+  bool track_entropy = false;
+  unsigned long long* ent_key = nullptr;  // device, order key
+  // asynchronous snapshot: a D2H copy of the state on its own stream, overlapping
+  // the following steps; the buffer it reads is fenced (snap_done) before any
+  // launch or copy writes it again
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t snap_ready = nullptr, snap_done = nullptr;
+  const double* snap_buf = nullptr;  // W[0] when the copy was issued; null when none pending
 
   std::vector<double> x, y, eps_h, r_h, fbuf;
   swdg_forcing_fn forcing = nullptr;
@@ -102,8 +123,10 @@ struct swdg_gpu {
   }
   ~swdg_gpu() {
     for (void* p : allocations) cudaFree(p);
-    if (flags_h) cudaFreeHost(flags_h);
-    if (sums_h) cudaFreeHost(sums_h);
+    if (rep_h) cudaFreeHost(rep_h);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (snap_ready) cudaEventDestroy(snap_ready);
+    if (snap_done) cudaEventDestroy(snap_done);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
 };
@@ -142,14 +165,43 @@ double ramp(double r, const swdg_params& p) {
 }
 
 void reset_flags(swdg_gpu* c) {
-  ck(cudaMemcpyAsync(c->flags, c->flags_init, 3 * sizeof(Flags), cudaMemcpyDeviceToDevice,
+  ck(cudaMemcpyAsync(c->flags, c->flags_init, 4 * sizeof(Flags), cudaMemcpyDeviceToDevice,
                      c->stream), "reset flags");
 }
 
+// the whole device report (stage flags, step reductions, sums): one copy, one sync
 void read_flags(swdg_gpu* c) {
-  ck(cudaMemcpyAsync(c->flags_h, c->flags, 3 * sizeof(Flags), cudaMemcpyDeviceToHost, c->stream),
+  ck(cudaMemcpyAsync(c->rep_h, c->rep, sizeof(Report), cudaMemcpyDeviceToHost, c->stream),
      "read flags");
   ck(cudaStreamSynchronize(c->stream), "sync flags");
+}
+
+// compute_dt's result (timeloop.hpp:72-74) from the reduced candidates in the
+// step-reduction flags: the CFL minimum, or the all-dry fallback
+double cfl_dt(swdg_gpu* c, double cfl) {
+  const Flags& f = c->flags_h[kDiagFlags];
+  double d = key_value(f.dt_key);
+  if (!std::isfinite(d)) {
+    const double order = 2.0 * c->M.degree + 1.0;
+    d = key_value(f.minlen_key) / (order * std::sqrt(c->params.g * std::max(c->params.h_ref, 1e-12)));
+  }
+  return cfl * d;
+}
+
+void diag_out(swdg_gpu* c, swdg_diagnostics* out) {
+  out->mass = c->sums_h[0];
+  out->entropy = c->sums_h[1];
+  out->min_h = key_value(c->flags_h[kDiagFlags].min_h_key);
+  out->positivity_dt = key_value(c->flags_h[kDiagFlags].posdt_key);
+}
+
+// Before anything writes the state buffer `buf` (three fields at one base), the
+// compute stream waits for a pending snapshot copy that reads it.
+void fence_snapshot(swdg_gpu* c, double* const* buf) {
+  if (c->snap_buf && c->snap_buf == buf[0]) {
+    ck(cudaStreamWaitEvent(c->stream, c->snap_done, 0), "snapshot fence");
+    c->snap_buf = nullptr;
+  }
 }
 
 CState cs(double* const* a) { return CState{a[0], a[1], a[2]}; }
@@ -163,9 +215,12 @@ double stage_viscosity(swdg_gpu* c, CState in) {
   ck(cudaMemcpyAsync(c->r_h.data(), c->r_ind, sizeof(double) * c->M.K, cudaMemcpyDeviceToHost,
                      c->stream), "indicator D2H");
   ck(cudaStreamSynchronize(c->stream), "indicator sync");
+  // owned elements only: a partition's ghost elements hold only face traces (their
+  // viscous flux pairs arrive by the halo exchange), so their eps is 0, not a ramp
+  // of stale interior data
   double mx = 0.0;
   for (int e = 0; e < c->M.K; ++e) {
-    c->eps_h[e] = ramp(c->r_h[e], c->params);
+    c->eps_h[e] = e < c->M.n_owned ? ramp(c->r_h[e], c->params) : 0.0;
     mx = std::max(mx, c->eps_h[e]);
   }
   ck(cudaMemcpyAsync(c->eps, c->eps_h.data(), sizeof(double) * c->M.K, cudaMemcpyHostToDevice,
@@ -225,6 +280,9 @@ void stage_main(swdg_gpu* c, CState in, double* const* out, int k, double t, dou
   a.update = out != nullptr;
   if (out) a.out = st(out);
   if (rhs) a.rhs = st(rhs);
+  // limiter entropy tracking needs the stage's dW/dt to rebuild the pre-limit state
+  const bool track = c->track_entropy && out && c->params.limiter_enabled;
+  if (track && !rhs) a.rhs = st(c->R);
   if (viscous) {
     a.eps = c->eps;
     a.fvu = c->fvu;
@@ -237,8 +295,9 @@ void stage_main(swdg_gpu* c, CState in, double* const* out, int k, double t, dou
     a.fhu = c->fhu;
     a.fhv = c->fhv;
   }
+  const Mesh& M = range ? *range : c->M;
+  if (out) fence_snapshot(c, out);
   if (c->fast) {
-    const Mesh& M = range ? *range : c->M;
     ck(cudaMemsetAsync(c->gctr, 0, sizeof(int), c->stream), "group counter");
     a.gctr = c->gctr;
     if (M.n_owned > M.e_lo) c->launches += launched(launch_fast_stage(M, c->phys, a, F, c->stream), "launch_fast_stage");
@@ -246,6 +305,9 @@ void stage_main(swdg_gpu* c, CState in, double* const* out, int k, double t, dou
     c->launches += launched(launch_exact_rhs_stage(c->M, c->phys, a, c->stream), "launch_exact_rhs_stage");
     if (out) c->launches += launched(launch_exact_limit(c->M, c->phys, st(out), F, c->stream), "launch_exact_limit");
   }
+  if (track)
+    c->launches += launched(launch_limiter_entropy(c->fast ? M : c->M, c->phys, a, F, c->ent_key,
+                                                   c->stream), "launch_limiter_entropy");
 }
 
 double stage(swdg_gpu* c, CState in, double* const* out, int k, double t, double dt,
@@ -390,21 +452,29 @@ void allocate(swdg_gpu* c, int K, int n_owned, int N, const std::vector<int4>& e
     c->gvu = vb + 2 * nnp;
     c->gvv = vb + 3 * nnp;
   }
-  c->partial = c->dalloc<double>(2 * (size_t)K);
-  c->sums = c->dalloc<double>(2);
-  c->flags = c->dalloc<Flags>(3);
+  c->partial = c->dalloc<double>(2 * (size_t)std::max(K, step_sum_partials()));
+  c->rep = c->dalloc<Report>(1);
+  c->flags = c->rep->f;
+  c->sums = c->rep->sums;
   c->gctr = c->dalloc<int>(1);
-  c->flags_init = c->dalloc<Flags>(3);
-  ck(cudaMallocHost(&c->flags_h, 3 * sizeof(Flags)), "pinned flags");
-  ck(cudaMallocHost(&c->sums_h, 2 * sizeof(double)), "pinned sums");
+  c->flags_init = c->dalloc<Flags>(4);
+  c->ent_key = c->dalloc<unsigned long long>(1);
+  ck(cudaMallocHost(&c->rep_h, sizeof(Report)), "pinned report");
+  std::memset(c->rep_h, 0, sizeof(Report));
+  c->flags_h = c->rep_h->f;
+  c->sums_h = c->rep_h->sums;
+  {
+    const unsigned long long k0 = order_key(0.0);  // worst jump starts at 0 (timeloop.hpp:261)
+    ck(cudaMemcpy(c->ent_key, &k0, sizeof(k0), cudaMemcpyHostToDevice), "ent key");
+  }
   Flags f{};
   f.min_h_key = ~0ull;
   f.dt_key = ~0ull;
   f.minlen_key = ~0ull;
   f.posdt_key = ~0ull;
   f.max_eps_key = 0ull;  // atomicMax target (eps >= 0)
-  for (int k = 0; k < 3; ++k) c->flags_h[k] = f;
-  ck(cudaMemcpy(c->flags_init, c->flags_h, 3 * sizeof(Flags), cudaMemcpyHostToDevice), "flags");
+  for (int k = 0; k < 4; ++k) c->flags_h[k] = f;
+  ck(cudaMemcpy(c->flags_init, c->flags_h, 4 * sizeof(Flags), cudaMemcpyHostToDevice), "flags");
   c->eps_h.assign(K, 0.0);
   c->r_h.assign(K, 0.0);
 }
@@ -610,6 +680,7 @@ int swdg_gpu_synchronize(swdg_gpu* c) {
 
 int swdg_gpu_upload_state(swdg_gpu* c, const double* h, const double* hu, const double* hv) {
   return guarded(c, [&] {
+    fence_snapshot(c, c->W);
     const double* src[3] = {h, hu, hv};
     for (int k = 0; k < 3; ++k)
       ck(cudaMemcpyAsync(c->W[k], src[k], c->nn * sizeof(double), cudaMemcpyHostToDevice,
@@ -697,15 +768,10 @@ int swdg_gpu_compute_dt(swdg_gpu* c, double cfl, double* dt) {
   return guarded(c, [&] {
     if (!(cfl > 0.0) || cfl > 1.0) throw InputError{"compute_dt: cfl must be in (0, 1]"};
     reset_flags(c);
-    c->launches += launched(launch_exact_dt(c->M, c->phys, cs(c->W), c->flags, c->stream), "launch_exact_dt");
+    c->launches += launched(launch_exact_dt(c->M, c->phys, cs(c->W), c->flags + kDiagFlags,
+                                            c->stream), "launch_exact_dt");
     read_flags(c);
-    double d = key_value(c->flags_h[0].dt_key);
-    if (!std::isfinite(d)) {
-      const double order = 2.0 * c->M.degree + 1.0;
-      d = key_value(c->flags_h[0].minlen_key) /
-          (order * std::sqrt(c->params.g * std::max(c->params.h_ref, 1e-12)));
-    }
-    *dt = cfl * d;
+    *dt = cfl_dt(c, cfl);
     return SWDG_OK;
   });
 }
@@ -728,44 +794,79 @@ static int fold_flags(swdg_gpu* c, swdg_step_info& r, int& code) {
   return 3;
 }
 
+// One SSPRK3 step of the device state (try_step timeloop.hpp:156-170).  With
+// `diag`, the step reductions of the stage-3 output (the next state if the step
+// is accepted) are queued behind the stages, so the device-resident driver reads
+// flags, diagnostics and the next CFL candidate with ONE host synchronisation.
+// Returns the error code; r.accepted says whether W advanced.
+static int try_step_impl(swdg_gpu* c, double t, double dt, swdg_step_info& r, bool diag) {
+  r = swdg_step_info{};
+  r.min_stage_h = std::numeric_limits<double>::infinity();
+  double* const* outs[3] = {c->A, c->B, c->A};
+  CState in = cs(c->W);
+  const bool viscous = c->params.visc_enabled != 0;
+  int code = SWDG_OK;
+  reset_flags(c);
+  if (c->fast && !c->forcing) {
+    // device-resident: three stages back to back, one flag read per step
+    for (int k = 0; k < 3; ++k) {
+      stage(c, in, outs[k], k, t, dt, viscous, nullptr, c->flags + k);
+      in = cs(outs[k]);
+    }
+    if (diag)
+      c->launches += launched(launch_diagnostics(c->M, c->phys, cs(c->A), c->partial, c->sums,
+                                                 c->flags + kDiagFlags, c->stream, !c->fast),
+                              "launch_diagnostics");
+    read_flags(c);
+    r.accepted = fold_flags(c, r, code) == 3 && code == SWDG_OK;
+  } else {
+    for (int k = 0; k < 3; ++k) {
+      const double mx = stage(c, in, outs[k], k, t, dt, viscous, nullptr, c->flags + k);
+      r.max_eps = std::max(r.max_eps, mx);
+      read_flags(c);
+      const Flags& f = c->flags_h[k];
+      if (f.abort) {
+        code = fail(c, SWDG_ERR_ABORT, "negative water height without limiter");
+        break;
+      }
+      if (f.reject) break;
+      if (c->params.limiter_enabled) r.n_limited = f.n_limited;
+      r.min_stage_h = std::min(r.min_stage_h, key_value(f.min_h_key));
+      in = cs(outs[k]);
+      if (k == 2) r.accepted = 1;
+    }
+    if (diag && r.accepted) {
+      c->launches += launched(launch_diagnostics(c->M, c->phys, cs(c->A), c->partial, c->sums,
+                                                 c->flags + kDiagFlags, c->stream, !c->fast),
+                              "launch_diagnostics");
+      read_flags(c);
+    }
+  }
+  if (r.accepted)
+    for (int k = 0; k < 3; ++k) std::swap(c->W[k], c->A[k]);
+  c->last = r;
+  return code;
+}
+
 int swdg_gpu_try_step(swdg_gpu* c, double t, double dt, swdg_step_info* info) {
   return guarded(c, [&] {
     swdg_step_info r{};
-    r.min_stage_h = std::numeric_limits<double>::infinity();
-    double* const* outs[3] = {c->A, c->B, c->A};
-    CState in = cs(c->W);
-    const bool viscous = c->params.visc_enabled != 0;
-    int code = SWDG_OK;
-    reset_flags(c);
-    if (c->fast && !c->forcing) {
-      // device-resident: three stages back to back, one flag read per step
-      for (int k = 0; k < 3; ++k) {
-        stage(c, in, outs[k], k, t, dt, viscous, nullptr, c->flags + k);
-        in = cs(outs[k]);
-      }
-      read_flags(c);
-      r.accepted = fold_flags(c, r, code) == 3 && code == SWDG_OK;
-    } else {
-      for (int k = 0; k < 3; ++k) {
-        const double mx = stage(c, in, outs[k], k, t, dt, viscous, nullptr, c->flags + k);
-        r.max_eps = std::max(r.max_eps, mx);
-        read_flags(c);
-        const Flags& f = c->flags_h[k];
-        if (f.abort) {
-          code = fail(c, SWDG_ERR_ABORT, "negative water height without limiter");
-          break;
-        }
-        if (f.reject) break;
-        if (c->params.limiter_enabled) r.n_limited = f.n_limited;
-        r.min_stage_h = std::min(r.min_stage_h, key_value(f.min_h_key));
-        in = cs(outs[k]);
-        if (k == 2) r.accepted = 1;
-      }
-    }
-    if (r.accepted)
-      for (int k = 0; k < 3; ++k) std::swap(c->W[k], c->A[k]);
-    c->last = r;
+    const int code = try_step_impl(c, t, dt, r, false);
     if (info) *info = r;
+    return code;
+  });
+}
+
+int swdg_gpu_step_device(swdg_gpu* c, double t, double dt, double cfl, swdg_step_report* out) {
+  return guarded(c, [&] {
+    if (!(cfl > 0.0) || cfl > 1.0) throw InputError{"compute_dt: cfl must be in (0, 1]"};
+    swdg_step_report rep{};
+    const int code = try_step_impl(c, t, dt, rep.info, true);
+    if (rep.info.accepted) {
+      diag_out(c, &rep.diag);
+      rep.next_dt = cfl_dt(c, cfl);
+    }
+    if (out) *out = rep;
     return code;
   });
 }
@@ -826,15 +927,11 @@ int swdg_gpu_last_eps(swdg_gpu* c, double* eps) {
 int swdg_gpu_diagnostics(swdg_gpu* c, swdg_diagnostics* out) {
   return guarded(c, [&] {
     reset_flags(c);
-    c->launches += launched(launch_diagnostics(c->M, c->phys, cs(c->W), c->partial, c->sums, c->flags,
-                                      c->stream), "launch_diagnostics");
-    ck(cudaMemcpyAsync(c->sums_h, c->sums, 2 * sizeof(double), cudaMemcpyDeviceToHost,
-                       c->stream), "sums D2H");
+    c->launches += launched(launch_diagnostics(c->M, c->phys, cs(c->W), c->partial, c->sums,
+                                               c->flags + kDiagFlags, c->stream, !c->fast),
+                            "launch_diagnostics");
     read_flags(c);
-    out->mass = c->sums_h[0];
-    out->entropy = c->sums_h[1];
-    out->min_h = key_value(c->flags_h[0].min_h_key);
-    out->positivity_dt = key_value(c->flags_h[0].posdt_key);
+    diag_out(c, out);
     return SWDG_OK;
   });
 }
@@ -864,6 +961,109 @@ int swdg_gpu_set_grid_cap(int32_t max_ctas) {
   return SWDG_OK;
 }
 
+// ---- stage buffers, per-stage report, limiter entropy tracking ------------
+
+static double* const* stage_input(swdg_gpu* c, int k) {
+  return k == 0 ? c->W : (k == 1 ? c->A : c->B);
+}
+static double* const* stage_output(swdg_gpu* c, int k) { return k == 1 ? c->B : c->A; }
+
+int swdg_gpu_upload_stage_input(swdg_gpu* c, int k, const double* h, const double* hu,
+                                const double* hv) {
+  return guarded(c, [&] {
+    if (k < 0 || k > 2) throw InputError{"upload_stage_input: bad stage"};
+    const double* src[3] = {h, hu, hv};
+    double* const* dst = stage_input(c, k);
+    fence_snapshot(c, dst);
+    for (int f = 0; f < 3; ++f)
+      ck(cudaMemcpyAsync(dst[f], src[f], c->nn * sizeof(double), cudaMemcpyHostToDevice,
+                         c->stream), "upload stage input");
+    ck(cudaStreamSynchronize(c->stream), "upload stage sync");
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_download_stage_output(swdg_gpu* c, int k, double* h, double* hu, double* hv) {
+  return guarded(c, [&] {
+    if (k < 0 || k > 2) throw InputError{"download_stage_output: bad stage"};
+    double* dst[3] = {h, hu, hv};
+    double* const* src = stage_output(c, k);
+    for (int f = 0; f < 3; ++f)
+      ck(cudaMemcpyAsync(dst[f], src[f], c->nn * sizeof(double), cudaMemcpyDeviceToHost,
+                         c->stream), "download stage output");
+    ck(cudaStreamSynchronize(c->stream), "download stage sync");
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_stage_info(swdg_gpu* c, int k, swdg_step_info* info) {
+  return guarded(c, [&] {
+    if (k < 0 || k > 2) throw InputError{"stage_info: bad stage"};
+    read_flags(c);
+    const Flags& f = c->flags_h[k];
+    swdg_step_info r{};
+    r.min_stage_h = key_value(f.min_h_key);
+    r.max_eps = c->fast ? key_value(f.max_eps_key) : c->split_max_eps;
+    r.n_limited = f.n_limited;
+    r.accepted = !(f.reject || f.abort);
+    *info = r;
+    return f.abort ? fail(c, SWDG_ERR_ABORT, "negative water height without limiter") : SWDG_OK;
+  });
+}
+
+int swdg_gpu_snapshot_async(swdg_gpu* c, double* h, double* hu, double* hv) {
+  return guarded(c, [&] {
+    if (!c->copy_stream) {
+      ck(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "copy stream");
+      ck(cudaEventCreateWithFlags(&c->snap_ready, cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&c->snap_done, cudaEventDisableTiming), "event");
+    }
+    if (c->snap_buf) ck(cudaStreamWaitEvent(c->stream, c->snap_done, 0), "snapshot fence");
+    ck(cudaEventRecord(c->snap_ready, c->stream), "snapshot ready");
+    ck(cudaStreamWaitEvent(c->copy_stream, c->snap_ready, 0), "snapshot wait");
+    double* dst[3] = {h, hu, hv};
+    for (int f = 0; f < 3; ++f)
+      ck(cudaMemcpyAsync(dst[f], c->W[f], c->nn * sizeof(double), cudaMemcpyDeviceToHost,
+                         c->copy_stream), "snapshot D2H");
+    ck(cudaEventRecord(c->snap_done, c->copy_stream), "snapshot done");
+    c->snap_buf = c->W[0];
+    return SWDG_OK;
+  });
+}
+
+void* swdg_gpu_alloc_pinned(size_t bytes) {
+  void* p = nullptr;
+  return cudaMallocHost(&p, bytes) == cudaSuccess ? p : nullptr;
+}
+
+void swdg_gpu_free_pinned(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+int swdg_gpu_snapshot_wait(swdg_gpu* c) {
+  return guarded(c, [&] {
+    if (c->snap_done) ck(cudaEventSynchronize(c->snap_done), "snapshot sync");
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_set_track_limiter_entropy(swdg_gpu* c, int on) {
+  return guarded(c, [&] {
+    c->track_entropy = on != 0;
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_worst_limiter_entropy_jump(swdg_gpu* c, double* out) {
+  return guarded(c, [&] {
+    unsigned long long k = 0;
+    ck(cudaMemcpyAsync(&k, c->ent_key, sizeof(k), cudaMemcpyDeviceToHost, c->stream), "ent D2H");
+    ck(cudaStreamSynchronize(c->stream), "ent sync");
+    *out = key_value(k);
+    return SWDG_OK;
+  });
+}
+
 // ---- partitioned runs: halo exchange hooks and the split SSPRK3 step -------
 
 int swdg_gpu_halo_setup(swdg_gpu* c, int64_t n_send, const int32_t* send_idx, int64_t n_recv,
@@ -885,11 +1085,6 @@ int swdg_gpu_halo_setup(swdg_gpu* c, int64_t n_send, const int32_t* send_idx, in
     return SWDG_OK;
   });
 }
-
-static double* const* stage_input(swdg_gpu* c, int k) {
-  return k == 0 ? c->W : (k == 1 ? c->A : c->B);
-}
-static double* const* stage_output(swdg_gpu* c, int k) { return k == 1 ? c->B : c->A; }
 
 // what: 0 = state of stage k's input (3 fields), 1 = viscous flux pairs (4 fields)
 int swdg_gpu_halo_pack(swdg_gpu* c, int what, int k, double* send_buf) {

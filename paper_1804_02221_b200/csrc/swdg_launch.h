@@ -44,6 +44,15 @@ int launch_fast_visc_pre(const Mesh& M, const Phys& P, CState S, double* eps, do
 int launch_fast_stage(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
                       cudaStream_t st);
 
+// per-step reductions (kernels_step.cu, --fmad=false): mass/entropy partials
+// (step_sum_partials() pairs), min h and CFL candidates into F, sums into out2
+int step_sum_partials();
+int launch_step_sums(const Mesh& M, const Phys& P, CState S, double* partial, double* out2,
+                     Flags* F, cudaStream_t st);
+// limited_entropy_check of the elements a stage limited (A.rhs holds its dW/dt)
+int launch_limiter_entropy(const Mesh& M, const Phys& P, const StageArgs& A, const Flags* F,
+                           unsigned long long* key, cudaStream_t st);
+
 // test hook: cap on the persistent stage kernels' grid (0 = none), kernels_common.cu
 extern int g_grid_cap;
 
@@ -53,6 +62,6 @@ int launch_halo_pack(const int* idx, long long n, int nf, const double* const* f
 int launch_halo_unpack(const int* idx, long long n, int nf, double* const* f, const double* buf,
                        cudaStream_t st);
 int launch_diagnostics(const Mesh& M, const Phys& P, CState S, double* partial, double* out2,
-                       Flags* F, cudaStream_t st);
+                       Flags* F, cudaStream_t st, bool serial);
 
 }  // namespace swdg_dev

@@ -73,6 +73,10 @@ class DiagnosticsC(C.Structure):
                 ("positivity_dt", C.c_double)]
 
 
+class StepReportC(C.Structure):
+    _fields_ = [("info", StepInfoC), ("diag", DiagnosticsC), ("next_dt", C.c_double)]
+
+
 class StructuredSpecC(C.Structure):
     _fields_ = [("kind", C.c_int32), ("degree", C.c_int32), ("kx", C.c_int32), ("ky", C.c_int32),
                 ("periodic_x", C.c_int32), ("periodic_y", C.c_int32),
@@ -161,6 +165,17 @@ def lib():
                                                      C.POINTER(ParamsC), C.c_int,
                                                      C.POINTER(vp)]),
             "swdg_gpu_download_geometry": (C.c_int, [vp, C.c_char_p, _dp]),
+            "swdg_gpu_step_device": (C.c_int, [vp, C.c_double, C.c_double, C.c_double,
+                                               C.POINTER(StepReportC)]),
+            "swdg_gpu_set_track_limiter_entropy": (C.c_int, [vp, C.c_int]),
+            "swdg_gpu_worst_limiter_entropy_jump": (C.c_int, [vp, _dp]),
+            "swdg_gpu_upload_stage_input": (C.c_int, [vp, C.c_int, _dp, _dp, _dp]),
+            "swdg_gpu_download_stage_output": (C.c_int, [vp, C.c_int, _dp, _dp, _dp]),
+            "swdg_gpu_stage_info": (C.c_int, [vp, C.c_int, C.POINTER(StepInfoC)]),
+            "swdg_gpu_step_begin": (C.c_int, [vp]),
+            "swdg_gpu_stage_visc": (C.c_int, [vp, C.c_int, C.c_double, C.c_double]),
+            "swdg_gpu_stage_run": (C.c_int, [vp, C.c_int, C.c_double, C.c_double]),
+            "swdg_gpu_set_grid_cap": (C.c_int, [C.c_int32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -475,9 +490,62 @@ class TimeIntegrator:
         self._check(lib().swdg_gpu_diagnostics(self._h, C.byref(d)))
         return d
 
-    def run_steps(self, nsteps: int, t: float, dt: float):
-        """Device-resident SSPRK3 steps with fixed dt (no host synchronisation)."""
+    def run_steps(self, nsteps: int, t: float, dt: float) -> bool:
+        """Device-resident SSPRK3 steps with fixed dt (no host synchronisation).
+
+        Returns True when every stage of every step kept all element means
+        nonnegative.  On False the device state is UNDEFINED (the steps after the
+        rejecting one ran on from its output): re-upload before reusing it."""
         self._check(lib().swdg_gpu_run_steps(self._h, nsteps, t, dt))
+        return bool(self.last_info().accepted)
+
+    def step_device(self, t: float, dt: float, cfl: float):
+        """One run_simulation loop body on the device state (driver.hpp:91-127):
+        try_step, then, if accepted, the step diagnostics of the new state and its
+        compute_dt(cfl), with one host synchronisation in fast mode.  Returns the
+        StepReportC (info, diag, next_dt); `info.accepted` False leaves W^n."""
+        self._sync_forcing()
+        r = StepReportC()
+        self._check(lib().swdg_gpu_step_device(self._h, t, dt, cfl, C.byref(r)))
+        self._info = r.info
+        return r
+
+    # -- track_limiter_entropy (timeloop.hpp:196-199)
+    @property
+    def track_limiter_entropy(self) -> bool:
+        return bool(getattr(self, "_track", False))
+
+    @track_limiter_entropy.setter
+    def track_limiter_entropy(self, on: bool):
+        self._check(lib().swdg_gpu_set_track_limiter_entropy(self._h, int(bool(on))))
+        self._track = bool(on)
+
+    def worst_limiter_entropy_jump(self) -> float:
+        v = C.c_double()
+        self._check(lib().swdg_gpu_worst_limiter_entropy_jump(self._h, C.byref(v)))
+        return v.value
+
+    # -- one stage of the split step (parity tests, partitioned runs)
+    def run_stage(self, k: int, wn: State, w_in: State | None, t: float, dt: float) -> State:
+        """Run SSPRK3 stage k (0, 1, 2) of a step at time t with W^n = `wn` and stage
+        input `w_in` (None: W^n, stage 0) through the fused stage kernels and return
+        the kernel-written stage output (update, combine, limiter, dry-node cut)."""
+        L = lib()
+        self._sync_forcing()
+        self.upload(wn)
+        if k > 0:
+            self._check(L.swdg_gpu_upload_stage_input(self._h, k, *(_ptr(a) for a in w_in.arrays())))
+        self._check(L.swdg_gpu_step_begin(self._h))
+        self._check(L.swdg_gpu_stage_visc(self._h, k, t, dt))
+        self._check(L.swdg_gpu_stage_run(self._h, k, t, dt))
+        out = State(*(np.empty(self.mesh.n_nodes) for _ in range(3)))
+        self._check(L.swdg_gpu_download_stage_output(self._h, k, *(_ptr(a) for a in out.arrays())))
+        return out
+
+    def stage_info(self, k: int) -> StepInfoC:
+        info = StepInfoC()
+        self._check(lib().swdg_gpu_stage_info(self._h, k, C.byref(info)))
+        return info
 
     def last_info(self) -> StepInfoC:
         info = StepInfoC()
@@ -533,6 +601,12 @@ class TimeIntegrator:
         self._check(lib().swdg_gpu_device_state(self._h, C.byref(hp), C.byref(hup),
                                                 C.byref(hvp)))
         return [C.cast(p, C.c_void_p).value for p in (hp, hup, hvp)]
+
+
+def set_grid_cap(max_ctas: int):
+    """Test hook: cap the persistent stage kernels' grid (0 = resident slots)."""
+    if lib().swdg_gpu_set_grid_cap(int(max_ctas)) != SWDG_OK:
+        raise SwdgError("grid cap must be >= 0")
 
 
 # ---------------------------------------------------------------- free functions

@@ -1,0 +1,103 @@
+"""The drop-in at the driver level (VERDICT r1 "make the drop-in real").
+
+* The INTEGRATION.md patch (tests/cpp/patch_reference.sh) applied to build-time
+  copies of the reference's driver.hpp and validate.hpp compiles with
+  swdg::gpu::TimeIntegrator swapped in (built here, where the reference exists).
+* On the B200 the patched reference run_simulation (driver.hpp:62-142), and the
+  device-resident swdg::gpu::run_simulation (include/swdg_gpu_driver.hpp), write
+  the reference's files (io.hpp snapshots + diagnostics, config hash) byte for
+  byte identical to the unmodified reference's, with track_limiter_entropy on.
+* validate.hpp's criteria that construct a TimeIntegrator (wellbalanced :139,
+  glitch :266, wetdry :328 -- track_limiter_entropy --, convergence :541 with
+  forcing, scenarios :637 with on_step) pass through the GPU integrator with the
+  reference's own detail strings, digit for digit.
+"""
+import filecmp
+import os
+import subprocess
+
+import pytest
+
+from tests.conftest import ROOT, gpu_available
+
+B = os.path.join(ROOT, "tests", "cpp", "_build")
+REF_INC = "/root/reference/proj/include"
+
+
+def _bin(name):
+    p = os.path.join(B, name)
+    if not os.path.exists(p):
+        pytest.skip(f"{name} not built (needs the reference headers at build time)")
+    return p
+
+
+def test_patch_hits_every_integrator_site(tmp_path):
+    if not os.path.isdir(os.path.join(REF_INC, "swdg")):
+        pytest.skip("reference headers absent (GPU box)")
+    subprocess.run(["sh", os.path.join(ROOT, "tests", "cpp", "patch_reference.sh"), REF_INC,
+                    str(tmp_path)], check=True)
+    drv = (tmp_path / "swdg" / "driver.hpp").read_text()
+    assert "SWDG_INTEGRATOR integ(mesh, cfg);" in drv
+    assert "const SWDG_INTEGRATOR&)> on_step" in drv
+    assert "TimeIntegrator integ(" not in drv.replace("SWDG_INTEGRATOR integ(", "")
+
+
+gpu = [pytest.mark.gpu, pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
+
+
+def _run(exe, args, cwd):
+    r = subprocess.run([exe, *args], capture_output=True, text=True, timeout=600, cwd=cwd)
+    assert r.returncode == 0, r.stdout + r.stderr
+    return r.stdout.strip()
+
+
+@pytest.mark.parametrize("sid,k,T,snap", [("wetdry_dambreak", "12", "0.2", "0.1"),
+                                          ("parabolic_dam_dry", "8", "0.1", "0.05")])
+@pytest.mark.gpu
+@pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")
+def test_driver_files_byte_identical(tmp_path, sid, k, T, snap):
+    outs = {}
+    for name in ("run_driver_ref", "run_driver_patched", "run_driver_device"):
+        d = tmp_path / name
+        d.mkdir()
+        outs[name] = (_run(_bin(name), [sid, k, T, str(d), snap, "1"], str(tmp_path)), d)
+    ref_line, ref_dir = outs["run_driver_ref"]
+    files = sorted(os.listdir(ref_dir))
+    assert "diagnostics.txt" in files and len(files) >= 3
+    for name in ("run_driver_patched", "run_driver_device"):
+        line, d = outs[name]
+        assert line == ref_line, (name, line, ref_line)  # steps, FNV, t, worst jump
+        assert sorted(os.listdir(d)) == files
+        match, mismatch, errors = filecmp.cmpfiles(ref_dir, d, files, shallow=False)
+        assert not mismatch and not errors, (name, mismatch, errors)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")
+def test_device_driver_fast_mode(tmp_path):
+    """The fused fast kernels through the device-resident driver: the same files
+    and the same step count on this non-chaotic run."""
+    (tmp_path / "r").mkdir()
+    (tmp_path / "f").mkdir()
+    ref_line = _run(_bin("run_driver_ref"), ["oscillating_lake", "12", "0.1",
+                                             str(tmp_path / "r"), "0.05"], str(tmp_path))
+    line = _run(_bin("run_driver_device"), ["oscillating_lake", "12", "0.1",
+                                            str(tmp_path / "f"), "0.05", "0", "1"], str(tmp_path))
+    assert line.split()[0] == ref_line.split()[0]  # step count
+    assert sorted(os.listdir(tmp_path / "f")) == sorted(os.listdir(tmp_path / "r"))
+
+
+CRITERIA = ["wellbalanced", "glitch", "wetdry", "convergence", "scenarios"]
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")
+def test_validate_criteria_through_gpu_integrator():
+    ref = subprocess.run([_bin("validate_ref"), *CRITERIA], capture_output=True, text=True,
+                         timeout=1200)
+    got = subprocess.run([_bin("validate_gpu"), *CRITERIA], capture_output=True, text=True,
+                         timeout=1200)
+    assert got.returncode == 0, got.stdout + got.stderr
+    assert f"ran={len(CRITERIA)} failed=0" in got.stdout
+    # exact mode: the same trajectories, so the same numbers in every detail string
+    assert got.stdout == ref.stdout
