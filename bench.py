@@ -45,27 +45,38 @@ def frozen_counts(N: int, viscous: bool):
 
 
 def stage_kernel(N: int, viscous: bool) -> str:
-    """the fused stage kernel launch_fast_stage picks for this degree"""
+    """the fused stage kernel(s) launch_fast_stage / launch_fast_visc_pre pick for
+    this degree (kernels_fast.cu launch_n)"""
     n1 = N + 1
     if viscous:
-        return "k_stage_hl<%d,..,visc> (half-line) + k_visc_pre<%d>" % (n1, n1)
+        main = ("k_stage_node<%d,..,visc> (node per thread)" % n1 if n1 <= 3
+                else "k_stage_hl<%d,..,visc> (half-line)" % n1)
+        return main + " + k_visc_lines<%d> (viscous pre-kernel)" % n1
     if n1 <= 3:
         return "k_stage_elem<%d> (element per thread)" % n1
-    if n1 <= 4:
-        return "k_stage<%d> (full-line)" % n1
+    if n1 == 4:
+        return "k_stage_node<%d> (node per thread)" % n1
     return "k_stage_hl<%d> (half-line)" % n1
 
 
+NCU_TRAFFIC_FILES = ("r02_ncu_traffic.json", "r01_ncu_traffic.json")
+
+
 def ncu_traffic(N: int, viscous: bool):
-    """DRAM bytes per launch of the stage kernel from the committed ncu --set full
-    capture of this configuration (profiles/r01_ncu_traffic.json), or None"""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
-            d = json.load(f)
+    """DRAM bytes per launch of the stage kernel from the newest committed ncu
+    --set full capture of this configuration (profiles/r0*_ncu_traffic.json; the
+    captured launch is a stage-2 launch, which reads W^n: 120 B/node
+    algorithmic, +128 viscous), or None"""
+    for name in NCU_TRAFFIC_FILES:
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                d = json.load(f)
+        except Exception:
+            continue
         e = d.get("%s_N%d" % ("visc" if viscous else "inv", N))
-        return None if e is None else float(e["dram_bytes_per_launch"])
-    except Exception:
-        return None
+        if e is not None:
+            return float(e["dram_bytes_per_launch"]), name
+    return None, None
 
 
 def peaks():
@@ -195,27 +206,36 @@ def measure_gpu(N: int, steps: int, warmup: int, viscous: bool, rank: int, world
     integ.upload(st)
     dt = 0.1 * integ.compute_dt_device(0.5)
 
-    # warm-up, then K timed device-resident steps
-    integ.run_steps(warmup, 0.0, dt)
+    # warm-up, then K timed device-resident steps: the metric as BASELINE.md
+    # defines it (every step: 3 stages + the per-step dt and diagnostics
+    # reductions on the device), then the same K steps stages-only (the stage
+    # kernels' own time, what the roofline fraction is computed from)
+    integ.run_steps(warmup, 0.0, dt, reductions=True)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     l0 = integ.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device()) as clk:
         ev0.record(stream)
-        integ.run_steps(steps, warmup * dt, dt)
+        ok = integ.run_steps(steps, warmup * dt, dt, reductions=True)
         ev1.record(stream)
         torch.cuda.synchronize()
-    launches = integ.launch_count() - l0
+        launches = integ.launch_count() - l0
+        ok2 = integ.run_steps(1, (warmup + steps) * dt, dt)  # re-warm the stages-only path
+        ev2.record(stream)
+        ok2 = integ.run_steps(steps, (warmup + steps + 1) * dt, dt) and ok2
+        ev3.record(stream)
+        torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
-    info = integ.last_info()
-    if not info.accepted:
+    ms_stages = ev2.elapsed_time(ev3)
+    if not (ok and ok2):
         raise RuntimeError("a stage was rejected during the timed run (invalid measurement)")
     if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([ms, ms_stages], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+        ms, ms_stages = float(t[0].item()), float(t[1].item())
 
     # e2e through the public driver API (driver.run_simulation_device, the
     # run_simulation loop of driver.hpp:62-142 with the state resident on the
@@ -232,7 +252,7 @@ def measure_gpu(N: int, steps: int, warmup: int, viscous: bool, rank: int, world
                                         keep_series=False)
         torch.cuda.synchronize()
         e2e_s = (time.perf_counter() - t0) / res_run.steps
-        # per step: dt, the accept flag, step info and diagnostics (~100 B) + the
+        # per step: the step report (flags, diagnostics, next dt: ~100 B) + the
         # state upload/download amortised over the run
         h2d = (3 * nn * 8) // res_run.steps
         d2h = (3 * nn * 8) // res_run.steps + 128
@@ -243,7 +263,8 @@ def measure_gpu(N: int, steps: int, warmup: int, viscous: bool, rank: int, world
             integ.try_step(st, s * dt, dt)
         torch.cuda.synchronize()
         e2e_host_s = (time.perf_counter() - t0) / 2
-    res = dict(ms=ms, dofs=dofs, nn=nn, launches=launches, clocks=clk.summary(),
+    res = dict(ms=ms, ms_stages=ms_stages, dofs=dofs, nn=nn, launches=launches,
+               clocks=clk.summary(),
                e2e_s=e2e_s, h2d=h2d, d2h=d2h, e2e_host_s=e2e_host_s, e2e_steps=e2e_steps)
     integ.close()
     return res
@@ -309,7 +330,8 @@ def measure_gpu_distributed(N: int, steps: int, warmup: int, viscous: bool, rank
                 h2d=3 * nn_local * 8, d2h=3 * nn_local * 8, halo_peers=len(b.plan.peers))
 
 
-def cpu_reference(N: int, viscous: bool, budget_s: float = 15.0, kx: int = 64, steps=None):
+def cpu_reference(N: int, viscous: bool, budget_s: float = 15.0, kx: int = 64, steps=None,
+                  warmup: int = 0):
     """The reference's own try_step (oracle/_ref, single-threaded like the reference) on
     a bounded sample of the C5 workload: the same mesh family, state and params on a
     kx*kx element patch.  Returns DOF-updates/s per stage."""
@@ -324,10 +346,12 @@ def cpu_reference(N: int, viscous: bool, budget_s: float = 15.0, kx: int = 64, s
     integ = ref.Integrator(m, p)
     L = ref.lib()
     runner = L.ref_runner_create(integ.h, *(ref.ptr(a) for a in st))
+    if warmup:
+        assert L.ref_runner_steps(runner, warmup, 0.0, dt) == warmup, "reference rejected a step"
     t0 = time.perf_counter()
     n = 0
     while True:
-        acc = L.ref_runner_steps(runner, 1, n * dt, dt)
+        acc = L.ref_runner_steps(runner, 1, (warmup + n) * dt, dt)
         assert acc == 1, "reference rejected a step"
         n += 1
         el = time.perf_counter() - t0
@@ -339,19 +363,20 @@ def cpu_reference(N: int, viscous: bool, budget_s: float = 15.0, kx: int = 64, s
 
 
 def _ref_worker(args):
-    N, viscous, steps, budget, barrier = args
+    N, viscous, steps, budget, barrier, warmup = args
     barrier.wait()
     if steps is None:
-        return cpu_reference(N, viscous, budget_s=budget)
-    return cpu_reference(N, viscous, steps=steps)
+        return cpu_reference(N, viscous, budget_s=budget, warmup=warmup)
+    return cpu_reference(N, viscous, steps=steps, warmup=warmup)
 
 
-def cpu_reference_parallel(N: int, viscous: bool, steps, procs: int, budget_s: float = 15.0):
+def cpu_reference_parallel(N: int, viscous: bool, steps, procs: int, budget_s: float = 15.0,
+                           warmup: int = 0):
     """P concurrent processes of cpu_reference (each its own patch, released
     together by a barrier): the aggregate DOF-updates/s of the host."""
     if procs <= 1:
-        r = (cpu_reference(N, viscous, budget_s=budget_s) if steps is None
-             else cpu_reference(N, viscous, steps=steps))
+        r = (cpu_reference(N, viscous, budget_s=budget_s, warmup=warmup) if steps is None
+             else cpu_reference(N, viscous, steps=steps, warmup=warmup))
         r["procs"] = 1
         return r
     import multiprocessing as mp
@@ -359,21 +384,29 @@ def cpu_reference_parallel(N: int, viscous: bool, steps, procs: int, budget_s: f
     with ctx.Manager() as man:
         barrier = man.Barrier(procs)
         with ctx.Pool(procs) as pool:
-            rs = pool.map(_ref_worker, [(N, viscous, steps, budget_s, barrier)] * procs)
+            rs = pool.map(_ref_worker, [(N, viscous, steps, budget_s, barrier, warmup)] * procs)
     secs = max(r["seconds"] for r in rs)
     return dict(value=sum(r["value"] for r in rs), seconds=secs, steps=rs[0]["steps"],
                 kx=rs[0]["kx"], dofs=rs[0]["dofs"], procs=procs)
 
 
 def cpu_model():
+    """The host CPU as /proc/cpuinfo reports it (a VM may hide the marketing name:
+    family/model/stepping and the vector ISA are added)."""
+    info = {}
     try:
         with open("/proc/cpuinfo") as f:
             for line in f:
-                if line.startswith("model name"):
-                    return line.split(":", 1)[1].strip()
+                if ":" in line:
+                    k, v = line.split(":", 1)
+                    info.setdefault(k.strip(), v.strip())
     except Exception:
-        pass
-    return "unknown"
+        return "unknown"
+    flags = info.get("flags", "").split()
+    isa = [f for f in ("avx512f", "avx2", "fma") if f in flags]
+    return (f"{info.get('model name', 'unknown')} (family {info.get('cpu family', '?')}, model "
+            f"{info.get('model', '?')}, stepping {info.get('stepping', '?')}; "
+            f"{'/'.join(isa)}; {os.cpu_count()} logical CPUs)")
 
 
 def main():
@@ -408,11 +441,18 @@ def main():
             return
         # the reference is single-threaded: on all host cores it is P independent
         # processes, each stepping its own patch of the workload at the same time
-        steps = max(1, args.steps // 10) + args.warmup
+        # W untimed warm-up steps, then K timed steps (the same K, W as our arm)
         P = int(os.environ.get("SWDG_REF_PROCS", "0")) or max(1, len(os.sched_getaffinity(0)))
-        r = cpu_reference_parallel(N, args.viscous, steps, P)
+        r = cpu_reference_parallel(N, args.viscous, args.steps, P, warmup=args.warmup)
+        config = dict(config, workload=(
+            f"C5 synthetic wavy curvilinear mesh, N={N}, "
+            f"{'viscous' if args.viscous else 'inviscid'} ES-DGSEM SSPRK3 stage: the reference "
+            f"CPU solver on {r['procs']} concurrent {r['kx']}x{r['kx']}-element patches "
+            f"({r['procs'] * r['kx'] ** 2} elements; the 1000x1000 mesh would take ~80 GB and "
+            f"minutes per step on one core), {r['steps']} steps each"),
+            elements=r["procs"] * r["kx"] ** 2, elements_per_gpu=None)
         line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
-                "n_gpus": args.gpus, "steps": r["steps"], "warmup": 0,
+                "n_gpus": args.gpus, "steps": r["steps"], "warmup": args.warmup,
                 "ms_per_step": 1e3 * r["seconds"] / r["steps"], "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": config,
@@ -421,7 +461,8 @@ def main():
                                  "sample": f"{r['procs']} concurrent single-threaded processes of the "
                                            f"reference TimeIntegrator::try_step (oracle/_ref), each on "
                                            f"a {r['kx']}x{r['kx']} patch of the same mesh family, "
-                                           f"{r['steps']} steps, {r['seconds']:.1f} s, {cpu_model()}"},
+                                           f"{r['steps']} steps, {r['seconds']:.1f} s",
+                                 "cpu": cpu_model()},
                 "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -443,13 +484,19 @@ def main():
                       scaling="strong: the same 1M-element mesh for every N")
     else:
         r = measure_gpu(N, args.steps, args.warmup, args.viscous, rank, world)
+    # value: DOF-updates of the whole job per second, per-step dt + diagnostics
+    # amortised over the step's 3 stages (BASELINE.md "Metric")
     stage_s = r["ms"] * 1e-3 / (3 * args.steps)
-    # value: DOF-updates of the whole job per second
     value = (r["dofs"] if distributed else world * r["dofs"]) / stage_s
+    # the stage kernels alone (roofline): stages-only timing of the same steps
+    kstage_s = r.get("ms_stages", r["ms"]) * 1e-3 / (3 * args.steps)
+    value_stages = (r["dofs"] if distributed else world * r["dofs"]) / kstage_s
     bytes_node, flops_node = frozen_counts(N, args.viscous)
     pk = peaks()
-    achieved_gbs = bytes_node * r["nn"] / stage_s / 1e9
-    achieved_tf = flops_node * r["nn"] / stage_s / 1e12
+    achieved_gbs = bytes_node * r["nn"] / kstage_s / 1e9
+    achieved_tf = flops_node * r["nn"] / kstage_s / 1e12
+    traffic, traffic_src = ncu_traffic(N, args.viscous)
+    stage2_bytes = (120.0 + (128.0 if args.viscous else 0.0)) * r["nn"]
     roof_dofs = min(pk["hbm_gbs"] * 1e9 / (bytes_node / 3.0),
                     pk["fp64_tflops"] * 1e12 / (flops_node / 3.0))
     bound = "hbm" if pk["hbm_gbs"] * 1e9 / (bytes_node / 3.0) <= \
@@ -462,6 +509,8 @@ def main():
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": config,
+        "value_stages_only": value_stages,
+        "ms_per_step_stages_only": r.get("ms_stages", r["ms"]) / args.steps,
         "roofline": {
             "bound": bound,
             "achieved": achieved_gbs if bound == "hbm" else achieved_tf,
@@ -469,13 +518,19 @@ def main():
             "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
             "frac": (achieved_gbs / pk["hbm_gbs"]) if bound == "hbm"
             else achieved_tf / pk["fp64_tflops"],
-            "traffic": ncu_traffic(N, args.viscous),
-            "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, one launch, cold L2)",
+            "traffic": traffic,
+            "traffic_unit": "bytes per launch (ncu dram__bytes_read+write of one stage-2 "
+                            "launch, cold L2)",
+            "traffic_source": traffic_src and "profiles/" + traffic_src,
+            "traffic_vs_same_stage_algorithmic": traffic / stage2_bytes if traffic else None,
             "algorithmic_bytes_per_launch": bytes_node * r["nn"],
+            "algorithmic_bytes_stage2_launch": stage2_bytes,
+            "timing": "achieved = stage-average algorithmic bytes / the stage kernels' own "
+                      "time per stage (CUDA events over K stages-only steps)",
             "kernel": stage_kernel(N, args.viscous),
             "algorithmic_bytes_per_node": bytes_node, "algorithmic_flops_per_node": flops_node,
             "achieved_fp64_tflops": achieved_tf, "achieved_gbs": achieved_gbs,
-            "roof_dof_per_s": roof_dofs, "frac_of_roof": value / world / roof_dofs,
+            "roof_dof_per_s": roof_dofs, "frac_of_roof": value_stages / world / roof_dofs,
             "peak_sources": {"hbm": pk["hbm_src"], "fp64": pk["fp64_src"]},
         },
         "clocks": r["clocks"],
@@ -485,8 +540,9 @@ def main():
                 "path": ("per rank: swdg_gpu_upload_state + split-step C ABI with NCCL halos + "
                          "download (pinned)") if distributed else
                         (f"driver.run_simulation_device, {r['e2e_steps']} steps: state uploaded "
-                         "from pinned memory once, per step compute_dt + try_step + diagnostics "
-                         "(D2H), final state downloaded; bytes amortised per step"),
+                         "from pinned memory once, per step one swdg_gpu_step_device (3 stages + "
+                         "diagnostics + next compute_dt, one D2H of the step report), final "
+                         "state downloaded; bytes amortised per step"),
                 **({} if distributed else {
                     "host_state_per_step": {
                         "value": 3 * r["dofs"] / r["e2e_host_s"], "unit": UNIT,
@@ -502,12 +558,16 @@ def main():
     if rank == 0:
         procs = int(os.environ.get("SWDG_REF_PROCS", "0")) or max(1, len(os.sched_getaffinity(0)))
         cb = cpu_reference_parallel(N, args.viscous, None, procs, budget_s=args.cpu_budget)
+        c1 = cpu_reference(N, args.viscous, budget_s=min(5.0, args.cpu_budget))
         out["cpu_baseline"] = {
             "value": cb["value"], "unit": UNIT, "cores": cb["procs"], "kind": "reference",
             "sample": f"{cb['procs']} concurrent single-threaded processes of oracle/_ref "
                       f"TimeIntegrator::try_step, each on a {cb['kx']}x{cb['kx']} patch of the "
-                      f"same mesh family, {cb['steps']} steps in {cb['seconds']:.1f} s, "
-                      f"{cpu_model()}"}
+                      f"same mesh family, {cb['steps']} steps in {cb['seconds']:.1f} s",
+            "value_1core": c1["value"],
+            "sample_1core": f"one process, {c1['kx']}x{c1['kx']} patch, {c1['steps']} steps in "
+                            f"{c1['seconds']:.1f} s (the reference is single-threaded)",
+            "cpu": cpu_model()}
         if args.sweep and not distributed:
             sweep, roof, frac = {}, {}, {}
             for n in range(1, 16):

@@ -188,6 +188,13 @@ int swdg_gpu_try_step(swdg_gpu* ctx, double t, double dt, swdg_step_info* info);
  * no host synchronisation (reject flags accumulate on the device; read them
  * with swdg_gpu_last_info). */
 int swdg_gpu_run_steps(swdg_gpu* ctx, int nsteps, double t, double dt);
+/* run_steps with options: SWDG_RUN_STEP_REDUCTIONS also queues, after every
+ * step, the per-step reductions a driver needs (the StepDiagnostics sums and
+ * minima and the next compute_dt candidate, driver.hpp:92, :117-127) on the
+ * device -- the throughput metric "with dt and diagnostics amortised".  After a
+ * rejected run (last_info accepted = 0) the device state is undefined. */
+#define SWDG_RUN_STEP_REDUCTIONS 1
+int swdg_gpu_run_steps_ex(swdg_gpu* ctx, int nsteps, double t, double dt, int flags);
 int swdg_gpu_last_info(swdg_gpu* ctx, swdg_step_info* info);
 
 int swdg_gpu_last_eps(swdg_gpu* ctx, double* eps);

@@ -871,14 +871,16 @@ int swdg_gpu_step_device(swdg_gpu* c, double t, double dt, double cfl, swdg_step
   });
 }
 
-int swdg_gpu_run_steps(swdg_gpu* c, int nsteps, double t, double dt) {
+int swdg_gpu_run_steps_ex(swdg_gpu* c, int nsteps, double t, double dt, int flags) {
   return guarded(c, [&] {
     const bool viscous = c->params.visc_enabled != 0;
+    const bool reductions = (flags & SWDG_RUN_STEP_REDUCTIONS) != 0;
     if (!(c->fast && !c->forcing)) {
       for (int s = 0; s < nsteps; ++s) {
         swdg_step_info r{};
-        const int rc = swdg_gpu_try_step(c, t + s * dt, dt, &r);
+        const int rc = try_step_impl(c, t + s * dt, dt, r, reductions);
         if (rc) return rc;
+        if (!r.accepted) return SWDG_OK;  // c->last holds the reject
       }
       return SWDG_OK;
     }
@@ -892,6 +894,12 @@ int swdg_gpu_run_steps(swdg_gpu* c, int nsteps, double t, double dt) {
         stage(c, in, outs[k], k, t + s * dt, dt, viscous, nullptr, c->flags + k);
         in = cs(outs[k]);
       }
+      // the per-step StepDiagnostics reductions and the next CFL candidate of the
+      // new state, as the driver needs them every step (driver.hpp:92, 117-127)
+      if (reductions)
+        c->launches += launched(launch_diagnostics(c->M, c->phys, cs(c->A), c->partial, c->sums,
+                                                   c->flags + kDiagFlags, c->stream, false),
+                                "launch_diagnostics");
       for (int k = 0; k < 3; ++k) std::swap(c->W[k], c->A[k]);
     }
     read_flags(c);
@@ -902,6 +910,10 @@ int swdg_gpu_run_steps(swdg_gpu* c, int nsteps, double t, double dt) {
     c->last = r;
     return code;
   });
+}
+
+int swdg_gpu_run_steps(swdg_gpu* c, int nsteps, double t, double dt) {
+  return swdg_gpu_run_steps_ex(c, nsteps, t, dt, 0);
 }
 
 int swdg_gpu_last_info(swdg_gpu* c, swdg_step_info* info) {

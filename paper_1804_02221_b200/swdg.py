@@ -176,6 +176,7 @@ def lib():
             "swdg_gpu_stage_visc": (C.c_int, [vp, C.c_int, C.c_double, C.c_double]),
             "swdg_gpu_stage_run": (C.c_int, [vp, C.c_int, C.c_double, C.c_double]),
             "swdg_gpu_set_grid_cap": (C.c_int, [C.c_int32]),
+            "swdg_gpu_run_steps_ex": (C.c_int, [vp, C.c_int, C.c_double, C.c_double, C.c_int]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -490,13 +491,15 @@ class TimeIntegrator:
         self._check(lib().swdg_gpu_diagnostics(self._h, C.byref(d)))
         return d
 
-    def run_steps(self, nsteps: int, t: float, dt: float) -> bool:
-        """Device-resident SSPRK3 steps with fixed dt (no host synchronisation).
+    def run_steps(self, nsteps: int, t: float, dt: float, reductions: bool = False) -> bool:
+        """Device-resident SSPRK3 steps with fixed dt (no host synchronisation);
+        `reductions` adds the per-step StepDiagnostics reductions and the next CFL
+        candidate on the device after every step.
 
         Returns True when every stage of every step kept all element means
         nonnegative.  On False the device state is UNDEFINED (the steps after the
         rejecting one ran on from its output): re-upload before reusing it."""
-        self._check(lib().swdg_gpu_run_steps(self._h, nsteps, t, dt))
+        self._check(lib().swdg_gpu_run_steps_ex(self._h, nsteps, t, dt, 1 if reductions else 0))
         return bool(self.last_info().accepted)
 
     def step_device(self, t: float, dt: float, cfl: float):
