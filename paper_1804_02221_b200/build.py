@@ -21,17 +21,21 @@ ROOT = os.path.dirname(PKG)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-          "--split-compile=0", "-diag-suppress=177",
+          "-diag-suppress=177",
           "-I" + CSRC, "-I" + os.path.join(ROOT, "include")]
 
+# object name -> (source, extra flags).  kernels_fast.cu is compiled once per
+# degree range (SWDG_PART) so the three heavy objects build in parallel.
 SOURCES = {
-    "swdg_gpu.cu": [],
-    "kernels_exact.cu": ["--fmad=false"],
-    "kernels_common.cu": [],
-    "kernels_step.cu": ["--fmad=false"],
-    "kernels_fast.cu": [],
-    "kernels_mesh.cu": [],
-    "host_mesh.cpp": [],
+    "swdg_gpu": ("swdg_gpu.cu", []),
+    "kernels_exact": ("kernels_exact.cu", ["--fmad=false"]),
+    "kernels_common": ("kernels_common.cu", []),
+    "kernels_step": ("kernels_step.cu", ["--fmad=false"]),
+    "kernels_fast_p0": ("kernels_fast.cu", ["-DSWDG_PART=0", "-DSWDG_N1_LO=2", "-DSWDG_N1_HI=7"]),
+    "kernels_fast_p1": ("kernels_fast.cu", ["-DSWDG_PART=1", "-DSWDG_N1_LO=8", "-DSWDG_N1_HI=11"]),
+    "kernels_fast_p2": ("kernels_fast.cu", ["-DSWDG_PART=2", "-DSWDG_N1_LO=12", "-DSWDG_N1_HI=16"]),
+    "kernels_mesh": ("kernels_mesh.cu", []),
+    "host_mesh": ("host_mesh.cpp", []),
 }
 
 
@@ -53,11 +57,11 @@ def build(verbose: bool = False, force: bool = False, ptxas_v: bool = False) -> 
     os.makedirs(OBJ_DIR, exist_ok=True)
     objs, cmds = [], []
     hdrs = _headers()
-    for src, extra in SOURCES.items():
+    for name, (src, extra) in SOURCES.items():
         path = os.path.join(CSRC, src)
         if not os.path.exists(path):
             continue
-        obj = os.path.join(OBJ_DIR, os.path.splitext(src)[0] + ".o")
+        obj = os.path.join(OBJ_DIR, name + ".o")
         objs.append(obj)
         if force or _stale(obj, [path] + hdrs):
             cmd = [NVCC, *ARCH, *COMMON, *extra, "-c", path, "-o", obj]
@@ -72,6 +76,10 @@ def build(verbose: bool = False, force: bool = False, ptxas_v: bool = False) -> 
     with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
         for f in [ex.submit(run, c) for c in cmds]:
             f.result()
+    # objects of sources no longer in the build must not be linked
+    for f in os.listdir(OBJ_DIR):
+        if f.endswith(".o") and os.path.join(OBJ_DIR, f) not in objs:
+            os.remove(os.path.join(OBJ_DIR, f))
     if force or _stale(LIB, objs):
         cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs]
         if verbose:

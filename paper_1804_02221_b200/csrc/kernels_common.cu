@@ -68,4 +68,42 @@ int launch_halo_unpack(const int* idx, long long n, int nf, double* const* f, co
 
 namespace swdg_dev {
 int g_grid_cap = 0;
+
+// fast-mode dispatch over the degree-range objects of kernels_fast.cu
+static int fast_part(int n1) { return n1 <= 7 ? 0 : (n1 <= 11 ? 1 : 2); }
+
+bool fast_stage_supported(int n1) { return n1 >= 2 && n1 <= 16; }
+
+int upload_fast_ops(int n1, const double* D, const double* Dt, const double* Dh,
+                    const double* Vinv, const double* w) {
+  // every object has its own table; all get the degree (the source-geometry
+  // kernel of part 0 serves every degree)
+  for (auto up : {upload_fast_ops_p0, upload_fast_ops_p1, upload_fast_ops_p2}) {
+    const int rc = up(n1, D, Dt, Dh, Vinv, w);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+int launch_source_geometry(const Mesh& M, double* sx, double* sy, cudaStream_t st) {
+  return launch_source_geometry_p0(M, sx, sy, st);
+}
+
+int launch_fast_visc_pre(const Mesh& M, const Phys& P, CState S, double* eps, double* fvu,
+                         double* fvv, double* gvu, double* gvv, Flags* F, cudaStream_t st) {
+  switch (fast_part(M.n1)) {
+    case 0: return launch_fast_visc_pre_p0(M, P, S, eps, fvu, fvv, gvu, gvv, F, st);
+    case 1: return launch_fast_visc_pre_p1(M, P, S, eps, fvu, fvv, gvu, gvv, F, st);
+    default: return launch_fast_visc_pre_p2(M, P, S, eps, fvu, fvv, gvu, gvv, F, st);
+  }
+}
+
+int launch_fast_stage(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
+                      cudaStream_t st) {
+  switch (fast_part(M.n1)) {
+    case 0: return launch_fast_stage_p0(M, P, A, F, st);
+    case 1: return launch_fast_stage_p1(M, P, A, F, st);
+    default: return launch_fast_stage_p2(M, P, A, F, st);
+  }
+}
 }  // namespace swdg_dev

@@ -40,6 +40,23 @@
 
 #include "fast_common.cuh"
 
+// The file is compiled once per degree range (build.py: SWDG_PART = 0, 1, 2 ->
+// N+1 in [2,7], [8,11], [12,16]) so the three objects build in parallel; each
+// object has its own constant operator table and exports its launchers with a
+// _p<part> suffix (the dispatch is in kernels_common.cu).
+#ifndef SWDG_PART
+#define SWDG_PART 0
+#define SWDG_N1_LO 2
+#define SWDG_N1_HI 16
+#endif
+#if SWDG_PART == 0
+#define SWDG_EXPORT(name) name##_p0
+#elif SWDG_PART == 1
+#define SWDG_EXPORT(name) name##_p1
+#else
+#define SWDG_EXPORT(name) name##_p2
+#endif
+
 // resident half-line CTAs per SM the register allocation is compiled for
 // (__launch_bounds__ min blocks), per N+1; the -D overrides are for A/B builds
 // viscous stages up to this N+1 take the node-per-thread kernel
@@ -1637,7 +1654,7 @@ __global__ void k_source_geometry(Mesh M, double* sx, double* sy) {
 
 }  // namespace
 
-int launch_source_geometry(const Mesh& M, double* sx, double* sy, cudaStream_t st) {
+int SWDG_EXPORT(launch_source_geometry)(const Mesh& M, double* sx, double* sy, cudaStream_t st) {
   const long long nn = (long long)M.K * M.np;
   k_source_geometry<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(M, sx, sy);
   return 1;
@@ -1650,7 +1667,7 @@ static bool g_ops_set[kMaxDevices][17];
 static bool g_ops_known[17];
 static double g_ops_host[kOpsTotal];
 
-int upload_fast_ops(int n1, const double* D, const double* Dt, const double* Dh,
+int SWDG_EXPORT(upload_fast_ops)(int n1, const double* D, const double* Dt, const double* Dh,
                     const double* Vinv, const double* w) {
   const int base = ops_offset(n1), np = n1 * n1;
   double tab[5 * 256 + 16];
@@ -1719,15 +1736,21 @@ static void launch_n(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
   }
 }
 
-int launch_fast_visc_pre(const Mesh& M, const Phys& P, CState S, double* eps, double* fvu,
-                         double* fvv, double* gvu, double* gvv, Flags* F, cudaStream_t st) {
+int SWDG_EXPORT(launch_fast_visc_pre)(const Mesh& M, const Phys& P, CState S, double* eps,
+                                      double* fvu, double* fvv, double* gvu, double* gvv,
+                                      Flags* F, cudaStream_t st) {
   // line-based pre-kernel at every degree (one velocity component at a time:
   // ~5 (N+1) doubles per thread); measured faster than a node-per-thread kernel
   // at every N once the eps maximum went to one atomic per CTA (N=14: 50.4 -> 35.9
   // ms/stage)
   switch (M.n1) {
-#define SWDG_VL(n) \
-  case n: launch_visc_lines_n<n>(M, P, S, eps, fvu, fvv, gvu, gvv, F, st); break;
+#define SWDG_VL(n)                                                                \
+  case n:                                                                         \
+    if constexpr (n >= SWDG_N1_LO && n <= SWDG_N1_HI)                             \
+      launch_visc_lines_n<n>(M, P, S, eps, fvu, fvv, gvu, gvv, F, st);            \
+    else                                                                          \
+      return 0;                                                                   \
+    break;
     SWDG_VL(3) SWDG_VL(4) SWDG_VL(5) SWDG_VL(6) SWDG_VL(7) SWDG_VL(8) SWDG_VL(9) SWDG_VL(10)
     SWDG_VL(11) SWDG_VL(12) SWDG_VL(13) SWDG_VL(14) SWDG_VL(15) SWDG_VL(16)
 #undef SWDG_VL
@@ -1736,26 +1759,19 @@ int launch_fast_visc_pre(const Mesh& M, const Phys& P, CState S, double* eps, do
   return 1;
 }
 
-bool fast_stage_supported(int n1) { return n1 >= 2 && n1 <= 16; }
-
-int launch_fast_stage(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
-                      cudaStream_t st) {
+int SWDG_EXPORT(launch_fast_stage)(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
+                                   cudaStream_t st) {
   switch (M.n1) {
-    case 2: launch_n<2>(M, P, A, F, st); break;
-    case 3: launch_n<3>(M, P, A, F, st); break;
-    case 4: launch_n<4>(M, P, A, F, st); break;
-    case 5: launch_n<5>(M, P, A, F, st); break;
-    case 6: launch_n<6>(M, P, A, F, st); break;
-    case 7: launch_n<7>(M, P, A, F, st); break;
-    case 8: launch_n<8>(M, P, A, F, st); break;
-    case 9: launch_n<9>(M, P, A, F, st); break;
-    case 10: launch_n<10>(M, P, A, F, st); break;
-    case 11: launch_n<11>(M, P, A, F, st); break;
-    case 12: launch_n<12>(M, P, A, F, st); break;
-    case 13: launch_n<13>(M, P, A, F, st); break;
-    case 14: launch_n<14>(M, P, A, F, st); break;
-    case 15: launch_n<15>(M, P, A, F, st); break;
-    case 16: launch_n<16>(M, P, A, F, st); break;
+#define SWDG_ST(n)                                                                \
+  case n:                                                                         \
+    if constexpr (n >= SWDG_N1_LO && n <= SWDG_N1_HI)                             \
+      launch_n<n>(M, P, A, F, st);                                                \
+    else                                                                          \
+      return 0;                                                                   \
+    break;
+    SWDG_ST(2) SWDG_ST(3) SWDG_ST(4) SWDG_ST(5) SWDG_ST(6) SWDG_ST(7) SWDG_ST(8) SWDG_ST(9)
+    SWDG_ST(10) SWDG_ST(11) SWDG_ST(12) SWDG_ST(13) SWDG_ST(14) SWDG_ST(15) SWDG_ST(16)
+#undef SWDG_ST
     default: return 0;
   }
   return 1;

@@ -34,7 +34,8 @@ int launch_exact_rhs_stage(const Mesh& M, const Phys& P, const StageArgs& A, cud
 int launch_exact_limit(const Mesh& M, const Phys& P, State S, Flags* F, cudaStream_t st);
 int launch_exact_dt(const Mesh& M, const Phys& P, CState S, Flags* F, cudaStream_t st);
 
-// fast mode (kernels_fast.cu)
+// fast mode: dispatch (kernels_common.cu) over the three degree-range objects of
+// kernels_fast.cu (SWDG_PART 0/1/2: N+1 in [2,7], [8,11], [12,16])
 int upload_fast_ops(int n1, const double* D, const double* Dt, const double* Dh,
                     const double* Vinv, const double* w);
 bool fast_stage_supported(int n1);
@@ -43,6 +44,19 @@ int launch_fast_visc_pre(const Mesh& M, const Phys& P, CState S, double* eps, do
                          double* fvv, double* gvu, double* gvv, Flags* F, cudaStream_t st);
 int launch_fast_stage(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
                       cudaStream_t st);
+#define SWDG_FAST_PART_DECL(p)                                                              \
+  int upload_fast_ops_##p(int n1, const double* D, const double* Dt, const double* Dh,      \
+                          const double* Vinv, const double* w);                             \
+  int launch_source_geometry_##p(const Mesh& M, double* sx, double* sy, cudaStream_t st);   \
+  int launch_fast_visc_pre_##p(const Mesh& M, const Phys& P, CState S, double* eps,         \
+                               double* fvu, double* fvv, double* gvu, double* gvv, Flags* F, \
+                               cudaStream_t st);                                            \
+  int launch_fast_stage_##p(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,     \
+                            cudaStream_t st);
+SWDG_FAST_PART_DECL(p0)
+SWDG_FAST_PART_DECL(p1)
+SWDG_FAST_PART_DECL(p2)
+#undef SWDG_FAST_PART_DECL
 
 // per-step reductions (kernels_step.cu, --fmad=false): mass/entropy partials
 // (step_sum_partials() pairs), min h and CFL candidates into F, sums into out2

@@ -56,11 +56,16 @@ def _run(exe, args, cwd):
 @pytest.mark.gpu
 @pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")
 def test_driver_files_byte_identical(tmp_path, sid, k, T, snap):
+    # config_hash covers cfg.out_dir (config.hpp:211): every run writes to the
+    # same directory, moved aside afterwards
     outs = {}
+    work = tmp_path / "out"
     for name in ("run_driver_ref", "run_driver_patched", "run_driver_device"):
+        work.mkdir()
+        line = _run(_bin(name), [sid, k, T, str(work), snap, "1"], str(tmp_path))
         d = tmp_path / name
-        d.mkdir()
-        outs[name] = (_run(_bin(name), [sid, k, T, str(d), snap, "1"], str(tmp_path)), d)
+        work.rename(d)
+        outs[name] = (line, d)
     ref_line, ref_dir = outs["run_driver_ref"]
     files = sorted(os.listdir(ref_dir))
     assert "diagnostics.txt" in files and len(files) >= 3
@@ -77,14 +82,22 @@ def test_driver_files_byte_identical(tmp_path, sid, k, T, snap):
 def test_device_driver_fast_mode(tmp_path):
     """The fused fast kernels through the device-resident driver: the same files
     and the same step count on this non-chaotic run."""
-    (tmp_path / "r").mkdir()
-    (tmp_path / "f").mkdir()
-    ref_line = _run(_bin("run_driver_ref"), ["oscillating_lake", "12", "0.1",
-                                             str(tmp_path / "r"), "0.05"], str(tmp_path))
-    line = _run(_bin("run_driver_device"), ["oscillating_lake", "12", "0.1",
-                                            str(tmp_path / "f"), "0.05", "0", "1"], str(tmp_path))
+    work = tmp_path / "out"
+    work.mkdir()
+    ref_line = _run(_bin("run_driver_ref"), ["oscillating_lake", "12", "0.1", str(work), "0.05"],
+                    str(tmp_path))
+    work.rename(tmp_path / "r")
+    work.mkdir()
+    line = _run(_bin("run_driver_device"), ["oscillating_lake", "12", "0.1", str(work), "0.05",
+                                            "0", "1"], str(tmp_path))
     assert line.split()[0] == ref_line.split()[0]  # step count
-    assert sorted(os.listdir(tmp_path / "f")) == sorted(os.listdir(tmp_path / "r"))
+    assert sorted(os.listdir(work)) == sorted(os.listdir(tmp_path / "r"))
+    # the headers (config hash, time) and the diagnostics step/t/dt columns agree
+    with open(work / "diagnostics.txt") as f, open(tmp_path / "r" / "diagnostics.txt") as g:
+        a, b = f.read().splitlines(), g.read().splitlines()
+    assert a[:2] == b[:2] and len(a) == len(b)
+    for la, lb in zip(a[2:], b[2:]):
+        assert la.split(";")[:3] == lb.split(";")[:3]
 
 
 CRITERIA = ["wellbalanced", "glitch", "wetdry", "convergence", "scenarios"]
