@@ -229,6 +229,17 @@ int swdg_gpu_set_forcing(swdg_gpu* ctx, swdg_forcing_fn fn, void* user);
 /* Number of kernels this context has launched (instrumentation). */
 int64_t swdg_gpu_launch_count(const swdg_gpu* ctx);
 
+/* ---- the paper's §5 kernel comparison (bench.hpp:133-157, 255-291) --------
+ * One pass of the split-form volume kernel (kind 0: Dtilde flux differencing
+ * with the entropy-conservative two-point flux, kernels::split_volume_element
+ * dg_rhs.hpp:23-71) or the standard one (kind 1: pointwise contravariant
+ * fluxes times D, standard_volume_element dg_rhs.hpp:75-117) over k elements of
+ * DEVICE arrays in[7] = (h, hu, hv, y_eta, x_eta, y_xi, x_xi) with out[3] +=
+ * the volume term, on `stream` (a cudaStream_t, NULL = legacy default).  The
+ * harness kernels of the paper's table, not the stage path. */
+int swdg_gpu_volume_kernel(int kind, int degree, int64_t k, const double* const* in,
+                           double* const* out, double g, void* stream);
+
 /* ---- standalone inputs (no reference headers needed) -------------------- */
 
 /* make_operators (operators.hpp:148-188): LGL nodes/weights, D, Dtilde, Dhat,

@@ -89,6 +89,9 @@ def lib():
             "ref_limit_all": (C.c_int, [vp, C.POINTER(Params), _dp, _dp, _dp, C.c_int, _dp]),
             "ref_mms_error": (C.c_int, [vp, C.POINTER(Params), C.c_double, C.c_double, _dp,
                                         _dp, C.POINTER(C.c_int64)]),
+            "ref_volume_kernel": (C.c_int, [C.c_int, C.c_int, C.c_long, C.POINTER(_dp),
+                                            C.POINTER(_dp), C.c_double]),
+            "ref_count_ops": (C.c_int, [C.c_int, C.c_long, C.POINTER(C.c_uint64)]),
             "ref_bench_rough_state": (C.c_int, [C.c_int, C.c_long, _dp, _dp, _dp]),
             "ref_run_simulation": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_double,
                                              C.c_double, _dp, _dp, _dp,
@@ -249,6 +252,22 @@ def mms_error(m: RefMesh, p: Params, cfl=0.4, t_end=0.2, wave=MMS_WAVE):
     check(lib().ref_mms_error(m.handle, C.byref(p), cfl, t_end, ptr(fp), C.byref(err),
                               C.byref(steps)))
     return err.value, steps.value
+
+
+def volume_kernel(kind: int, degree: int, k: int, inputs, g=9.81):
+    """the reference's split (0) / standard (1) volume kernel, out = 0 + term"""
+    ins = (_dp * 7)(*(ptr(a) for a in inputs))
+    out = [np.zeros(k * (degree + 1) ** 2) for _ in range(3)]
+    outs = (_dp * 3)(*(ptr(a) for a in out))
+    check(lib().ref_volume_kernel(kind, degree, k, ins, outs, g))
+    return out
+
+
+def count_ops(degree: int, k: int):
+    """bench::count_ops: (evals_split, evals_std, flops_split, flops_std)"""
+    o = (C.c_uint64 * 4)()
+    check(lib().ref_count_ops(degree, k, o))
+    return tuple(int(x) for x in o)
 
 
 def bench_rough_state(degree: int, n_elem: int):

@@ -540,6 +540,51 @@ int ref_mms_error(void* mh, const swdg_params* p, double cfl, double t_end, cons
   }
 }
 
+// The reference's volume kernels of the paper's comparison (bench.hpp:133-157)
+// over k elements of host arrays: kind 0 split_volume_element with Dtilde,
+// kind 1 standard_volume_element with D (dg_rhs.hpp:23-117); out += the term.
+int ref_volume_kernel(int kind, int degree, long k, const double* const* in, double* const* out,
+                      double g) {
+  try {
+    const Operators1D ops = make_operators(degree);
+    const int n1 = degree + 1, np = n1 * n1;
+    std::vector<double> scratch(6 * np);
+    for (long e = 0; e < k; ++e) {
+      const long o = e * np;
+      if (kind == 0)
+        kernels::split_volume_element<double>(
+            n1, g, 1e-8, in[0] + o, in[1] + o, in[2] + o, in[3] + o, in[4] + o, in[5] + o,
+            in[6] + o, ops.deriv_modified.data(), scratch.data(), scratch.data() + np,
+            out[0] + o, out[1] + o, out[2] + o);
+      else
+        kernels::standard_volume_element<double>(
+            n1, g, 1e-8, in[0] + o, in[1] + o, in[2] + o, in[3] + o, in[4] + o, in[5] + o,
+            in[6] + o, ops.deriv.data(), scratch.data(), scratch.data() + 3 * np, out[0] + o,
+            out[1] + o, out[2] + o);
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// bench::count_ops (bench.hpp:160-192): CountReal flux evaluations and flops of
+// both volume kernels over k elements -> out[4] = evals_split, evals_std,
+// flops_split, flops_std.
+int ref_count_ops(int degree, long k, uint64_t* out) {
+  try {
+    std::uint64_t a, b, c, d;
+    bench::count_ops(degree, k, a, b, c, d);
+    out[0] = a;
+    out[1] = b;
+    out[2] = c;
+    out[3] = d;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 // The rough synthetic state of the reference's kernel benchmark
 // (bench.hpp:108-121, bench::KernelBuffers::init): std::mt19937(20250810),
 // h ~ U(0.5, 2), hu = h U(-1, 1), hv = h U(-1, 1), node-major over k elements.

@@ -161,19 +161,30 @@ inline int current_device() {
   return dev;
 }
 
-// persistent grid: resident CTAs over all SMs (capped at the group count)
+inline int device_sms(int dev) {
+  static int sms[kMaxDevices] = {};
+  if (sms[dev] == 0) cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+  return sms[dev];
+}
+
+// persistent grid: resident CTAs over all SMs (capped at the group count).
+// `reserve_sms` SMs are left free for concurrent work (the halo exchange's
+// NCCL kernels while a partition's interior runs).
 template <class KERN>
-int grid_for(KERN kern, int threads, size_t bytes, int groups, int (&cache)[kMaxDevices]) {
+int grid_for(KERN kern, int threads, size_t bytes, int groups, int (&cache)[kMaxDevices],
+             int reserve_sms = 0) {
   const int dev = current_device();
   if (dev < 0) return 0;
-  if (cache[dev] == 0) {
+  if (cache[dev] == 0) {  // resident CTAs per SM
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    int per_sm = 0, sms = 0;
+    int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, bytes);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cache[dev] = (per_sm > 0 ? per_sm : 1) * sms;
+    cache[dev] = per_sm > 0 ? per_sm : 1;
   }
-  int grid = groups < cache[dev] ? groups : cache[dev];
+  const int sms = device_sms(dev);
+  const int use = reserve_sms > 0 && reserve_sms < sms ? sms - reserve_sms : sms;
+  int grid = cache[dev] * use;
+  if (groups < grid) grid = groups;
   // test hook (swdg_gpu_set_grid_cap): fewer CTAs, so each loops over many groups
   if (g_grid_cap > 0 && grid > g_grid_cap) grid = g_grid_cap;
   return grid;

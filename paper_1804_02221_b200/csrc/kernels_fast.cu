@@ -1624,7 +1624,7 @@ static void launch_node(const Mesh& M, const Phys& P, const StageArgs& A, Flags*
   static int cache[kMaxDevices] = {};
   auto kern = k_stage_node<N1, FORCE, VISC>;
   const int groups = (M.n_owned - M.e_lo + PL::G - 1) / PL::G;
-  const int grid = grid_for(kern, PL::THREADS, PL::bytes, groups, cache);
+  const int grid = grid_for(kern, PL::THREADS, PL::bytes, groups, cache, A.reserve_sms);
   if (grid > 0) kern<<<grid, PL::THREADS, PL::bytes, st>>>(M, P, A, F);
 }
 
@@ -1700,7 +1700,8 @@ static void launch_half(const Mesh& M, const Phys& P, const StageArgs& A, Flags*
   using PL = HL<N1, VISC>;
   static int cache[kMaxDevices] = {};
   auto kern = k_stage_hl<N1, FORCE, VISC>;
-  const int grid = grid_for(kern, PL::THREADS, PL::bytes, (M.n_owned - M.e_lo + PL::E - 1) / PL::E, cache);
+  const int grid = grid_for(kern, PL::THREADS, PL::bytes, (M.n_owned - M.e_lo + PL::E - 1) / PL::E,
+                            cache, A.reserve_sms);
   kern<<<grid, PL::THREADS, PL::bytes, st>>>(M, P, A, F);
 }
 

@@ -52,6 +52,9 @@ struct InputError {
 };
 
 constexpr int kDiagFlags = 3;  // Flags slot of the step reductions (0-2: stages)
+// SMs a partition's interior stage leaves to the concurrent halo exchange (NCCL
+// P2P kernels: one or two CTAs per peer and direction)
+constexpr int kHaloReserveSms = 8;
 
 struct Report {
   Flags f[4];
@@ -83,6 +86,7 @@ struct swdg_gpu {
   double *fh = nullptr, *fhu = nullptr, *fhv = nullptr;
   double *partial = nullptr, *sums = nullptr;
   int int_lo = 0, int_hi = 0;   // interior element range (halo overlap), empty by default
+  int reserve_sms = 0;          // SMs the next stage launch leaves free
   int* gctr = nullptr;          // device group counter of the persistent stage kernels
   // device report: Flags[4] (one per stage + one for the step reductions) and the
   // mass/entropy sums, contiguous so one copy (one host sync) reads a whole step
@@ -296,6 +300,7 @@ void stage_main(swdg_gpu* c, CState in, double* const* out, int k, double t, dou
     a.fhv = c->fhv;
   }
   const Mesh& M = range ? *range : c->M;
+  a.reserve_sms = c->reserve_sms;
   if (out) fence_snapshot(c, out);
   if (c->fast) {
     ck(cudaMemsetAsync(c->gctr, 0, sizeof(int), c->stream), "group counter");
@@ -1205,7 +1210,9 @@ int swdg_gpu_stage_run_part(swdg_gpu* c, int k, double t, double dt, int part) {
     if (part == 1) {
       r.e_lo = c->int_lo;
       r.n_owned = c->int_hi;
+      c->reserve_sms = kHaloReserveSms;  // the exchange runs concurrently
       stage_main(c, in, out, k, t, dt, visc, nullptr, c->flags + k, &r);
+      c->reserve_sms = 0;
     } else {
       r.e_lo = 0;
       r.n_owned = c->int_lo;

@@ -24,6 +24,9 @@ struct StageArgs {
   // before each launch) so the CTAs sweep the mesh as one wavefront and the
   // neighbour face traces they gather are still in L2 when reused
   int* gctr;
+  // SMs the persistent stage kernels leave free (0: use all): a partition's
+  // interior launch runs while NCCL moves the halo, whose kernels need SMs
+  int reserve_sms;
 };
 
 // exact mode (kernels_exact.cu)

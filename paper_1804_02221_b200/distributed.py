@@ -38,6 +38,7 @@ class Backend:
     def step_flags(self): ...
     def step_commit(self, accept: bool): ...
     def dt_candidates(self): ...
+    def step_report(self) -> dict: ...  # REPORT_KEYS of the owned elements, this rank
 
 
 def _offsets(plan, which):
@@ -103,6 +104,14 @@ class TorchExchanger:
 
     def all_min(self, vals):
         return [-v for v in self.all_max([-v for v in vals])]
+
+    def all_gather(self, vals):
+        """every rank's `vals`, in rank order (for order-fixed sums)"""
+        torch = self.torch
+        t = torch.tensor(vals, dtype=torch.float64, device=self.send.device)
+        out = [torch.empty_like(t) for _ in range(torch.distributed.get_world_size())]
+        torch.distributed.all_gather(out, t)
+        return [o.tolist() for o in out]
 
 
 class LoopbackExchanger:
@@ -218,6 +227,73 @@ def try_step_loopback(bs, ex: LoopbackExchanger, t: float, dt: float) -> bool:
     for b in bs:
         b.step_commit(accept)
     return accept
+
+
+# StepDiagnostics fields a step produces per rank (driver.hpp:115-127)
+REPORT_KEYS = ("mass", "entropy", "min_h", "positivity_dt", "n_limited", "min_stage_h",
+               "max_eps")
+
+
+def combine_reports(rows) -> dict:
+    """sums of mass, entropy and n_limited (in rank order, so the
+    result is independent of the collective's reduction order), minima of min_h,
+    the positivity bound and min_stage_h, maximum of max_eps."""
+    cols = list(zip(*rows))
+    out = {}
+    for k, col in zip(REPORT_KEYS, cols):
+        if k in ("mass", "entropy", "n_limited"):
+            acc = 0.0
+            for v in col:
+                acc += v
+            out[k] = int(acc) if k == "n_limited" else acc
+        elif k == "max_eps":
+            out[k] = max(col)
+        else:
+            out[k] = min(col)
+    return out
+
+
+def step_report_distributed(b: Backend, ex) -> dict:
+    """The step diagnostics of the whole partitioned mesh (field.hpp:39-68,
+    limiter.hpp:135-166 and the try_step report timeloop.hpp:192-195).  The
+    positivity bound of a cut face needs the neighbour's NEW state: the committed
+    state's halo is exchanged first (the ghosts still hold stage-3 inputs)."""
+    ex.exchange(0, 0)
+    loc = b.step_report()
+    return combine_reports(ex.all_gather([float(loc[k]) for k in REPORT_KEYS]))
+
+
+def step_report_loopback(bs, ex) -> dict:
+    ex.exchange_all(0, 0)
+    return combine_reports([[float(b.step_report()[k]) for k in REPORT_KEYS] for b in bs])
+
+
+def run_simulation_distributed(b: Backend, ex, final_time: float, cfl: float, degree: int,
+                               phys, max_steps=None, keep_series=True):
+    """run_simulation's loop (driver.hpp:91-138) over the ranks: the global CFL dt,
+    reject-and-halve in lock step, and the global step diagnostics per step."""
+    t, steps, series = 0.0, 0, []
+    t_eps = 1e-12 * max(1.0, final_time)
+    while t < final_time - t_eps:
+        if max_steps is not None and steps >= max_steps:
+            break
+        dt = compute_dt_distributed(b, ex, cfl, degree, phys)
+        hit = False
+        if t + dt >= final_time - t_eps:
+            dt, hit = final_time - t, True
+        rej = 0
+        while not try_step_distributed(b, ex, t, dt):
+            dt *= 0.5
+            hit = False
+            rej += 1
+            if rej >= 10:
+                raise swdg.NumericalAbort(f"step rejected 10 times at t={t}")
+        t = final_time if hit else t + dt
+        steps += 1
+        rep = step_report_distributed(b, ex)
+        if keep_series:
+            series.append(dict(step=steps, t=t, dt=dt, **rep))
+    return t, steps, series
 
 
 def compute_dt_distributed(b: Backend, ex, cfl: float, degree: int, phys) -> float:
@@ -337,3 +413,11 @@ class GpuPartition(Backend):
         d, m = C.c_double(), C.c_double()
         self._chk(self.L.swdg_gpu_dt_candidates(self.integ._h, C.byref(d), C.byref(m)))
         return d.value, m.value
+
+    def step_report(self):
+        """this rank's owned-element diagnostics of the committed state and its
+        stage report (reduced over ranks by step_report_distributed)"""
+        d = self.integ.diagnostics_device()
+        return dict(mass=d.mass, entropy=d.entropy, min_h=d.min_h,
+                    positivity_dt=d.positivity_dt, n_limited=self.info.n_limited,
+                    min_stage_h=self.info.min_stage_h, max_eps=self.info.max_eps)

@@ -55,6 +55,8 @@ class PortPartition(Backend):
 
     def step_begin(self):
         self.stage_flags = []
+        self.stage_nl = []
+        self.stage_mh = []
         self.max_eps = 0.0
 
     def stage_visc(self, k, t, dt):
@@ -78,6 +80,8 @@ class PortPartition(Backend):
             out.append(np.ascontiguousarray(o))
         ok, nl, mh = port.post_stage(self.view, self.p, out)
         self.stage_flags.append(ok)
+        self.stage_nl.append(nl)
+        self.stage_mh.append(mh)
         if k == 1:
             self.B = out
         else:
@@ -94,3 +98,10 @@ class PortPartition(Backend):
     def step_commit(self, accept):
         if accept:
             self.W = [a.copy() for a in self.A]
+
+    def step_report(self):
+        d = port.diagnostics(self.view, self.p, self.W)
+        return dict(mass=d.mass, entropy=d.entropy, min_h=d.min_h,
+                    positivity_dt=d.positivity_dt,
+                    n_limited=self.stage_nl[-1] if self.p.limiter_enabled else 0,
+                    min_stage_h=min(self.stage_mh), max_eps=self.max_eps)

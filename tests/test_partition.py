@@ -117,6 +117,40 @@ def test_loopback_reversed_faces():
     assert beq(_gather(lms, bs, m.n_nodes), want)
 
 
+@pytest.mark.parametrize("name,P,visc", [("wavy_N4", 3, True), ("cart_N3_walls", 2, True)])
+def test_loopback_step_reports_match_global(name, P, visc):
+    """SURVEY §8(e) per-step reductions: mass/entropy/n_limited sums, min h /
+    positivity / min stage h minima, max eps maximum over the partitions equal the
+    single-mesh step report (sums to rounding: a different summation order)."""
+    from paper_1804_02221_b200.distributed import step_report_loopback
+    m = build(name)
+    N = m.degree
+    smin = -(4.0 + 4.25 * np.log10(N)) - 1.0
+    p = ref.params(g=9.81, visc=visc, epsilon0=0.1, sigma_min=smin, sigma_max=smin + 2.0)
+    st = random_state(m.n_nodes, np.random.default_rng(4), h=(0.0, 1.5), vel=0.5, dry_prob=0.1)
+    dt = 0.1 * port.compute_dt(m, p, st, 0.5)
+    lms = [part.local_mesh(m, P, r) for r in range(P)]
+    bs = [PortPartition(lm, p) for lm in lms]
+    for lm, b in zip(lms, bs):
+        b.upload(part.scatter_state(st, lm))
+    ex = LoopbackExchanger(bs, lambda n: np.zeros(n))
+    s = [a.copy() for a in st]
+    for k in range(3):
+        info = port.try_step(m, p, s, k * dt, dt)
+        assert try_step_loopback(bs, ex, k * dt, dt) == bool(info.accepted)
+        if not info.accepted:  # the driver reads the report of accepted steps only
+            continue
+        rep = step_report_loopback(bs, ex)
+        d = port.diagnostics(m, p, s)
+        assert rep["n_limited"] == info.n_limited
+        assert rep["min_stage_h"] == info.min_stage_h
+        assert rep["max_eps"] == info.max_eps
+        assert rep["min_h"] == d.min_h
+        assert rep["positivity_dt"] == d.positivity_dt
+        assert abs(rep["mass"] - d.mass) <= 1e-13 * abs(d.mass)
+        assert abs(rep["entropy"] - d.entropy) <= 1e-13 * abs(d.entropy)
+
+
 def _gloo_worker(rank, world, port_no, result_path):
     import torch
     import torch.distributed as dist
@@ -129,11 +163,15 @@ def _gloo_worker(rank, world, port_no, result_path):
     b = PortPartition(lm, p)
     b.upload(part.scatter_state(st, lm))
     ex = TorchExchanger(b, "cpu")
-    acc = [try_step_distributed(b, ex, k * dt, dt) for k in range(4)]
+    from paper_1804_02221_b200.distributed import step_report_distributed
+    acc, reps = [], []
+    for k in range(4):
+        acc.append(try_step_distributed(b, ex, k * dt, dt))
+        reps.append(step_report_distributed(b, ex))
     np_ = lm.n1 * lm.n1
     mine = np.stack([w[: lm.n_owned * np_] for w in b.W])
     gathered = [None] * world
-    dist.all_gather_object(gathered, (lm.global_ids[: lm.n_owned].tolist(), mine, acc))
+    dist.all_gather_object(gathered, (lm.global_ids[: lm.n_owned].tolist(), mine, acc, reps))
     if rank == 0:
         np.save(result_path, np.array(gathered, dtype=object), allow_pickle=True)
     dist.destroy_process_group()
@@ -155,11 +193,19 @@ def test_gloo_two_ranks_bitwise(tmp_path):
     p, cfg = scenario_params("wetdry_dambreak")
     dt = port.compute_dt(m, p, st, cfg["cfl"])
     want = [a.copy() for a in st]
-    acc_ref = [bool(port.try_step(m, p, want, k * dt, dt).accepted) for k in range(4)]
+    acc_ref, infos = [], []
+    for k in range(4):
+        info = port.try_step(m, p, want, k * dt, dt)
+        acc_ref.append(bool(info.accepted))
+        infos.append((info.n_limited, info.min_stage_h, port.diagnostics(m, p, want)))
     np_ = m.n1 * m.n1
     got = [np.zeros(m.n_nodes) for _ in range(3)]
-    for gids, mine, acc in res:
+    for gids, mine, acc, reps in res:
         assert acc == acc_ref
+        for rep, (nl, msh, d) in zip(reps, infos):  # the same report on every rank
+            assert rep["n_limited"] == nl and rep["min_stage_h"] == msh
+            assert rep["min_h"] == d.min_h and rep["positivity_dt"] == d.positivity_dt
+            assert abs(rep["mass"] - d.mass) <= 1e-13 * abs(d.mass)
         sel = (np.array(gids)[:, None] * np_ + np.arange(np_)).ravel()
         for j in range(3):
             got[j][sel] = mine[j]
