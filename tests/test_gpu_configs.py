@@ -42,6 +42,7 @@ CA = (0.0, 3.0 / 4.0, 1.0 / 3.0)  # ssprk3_combination (timeloop.hpp:79-80)
 CB = (1.0, 1.0 / 4.0, 2.0 / 3.0)
 CT = (0.0, 1.0, 0.5)              # ssprk3_stage_times (timeloop.hpp:81)
 KX = 128
+CAPPED = [0]  # the grid cap in force (recorded with the measured errors)
 
 
 @functools.lru_cache(maxsize=1)
@@ -94,30 +95,51 @@ def ref_stage(ri, m, p, wn, w_in, k, t, dt):
     return s, int(np.count_nonzero(theta < 1.0))
 
 
+def ref_stages(ri, m, p, wn, stages, dt):
+    """the reference's outputs of `stages`, each from the previous one's output;
+    dt is halved until every stage keeps its element means nonnegative, as
+    run_simulation's reject-and-halve does (driver.hpp:101-111): the CFL step
+    ignores the viscous (parabolic) limit, which the rough field with eps0 = 0.1
+    exceeds"""
+    for _ in range(30):
+        try:
+            outs, w_in = [], [a.copy() for a in wn]
+            for k in stages:
+                want, nlim = ref_stage(ri, m, p, wn, w_in, k, 0.0, dt)
+                outs.append((w_in, want, nlim))
+                w_in = want
+            return dt, outs
+        except RuntimeError as e:  # limit_element: negative element mean (a reject)
+            assert "negative element mean" in str(e)
+            dt *= 0.5
+    raise AssertionError("no accepted step")
+
+
 def check_stage(N, viscous, kind, stages=(0,)):
     m = c5_mesh(N)
     p = c5_params(N, viscous)
     gi, ri = c5_context(N, viscous)
     wn = c5_state(m, kind)
-    # the C5 workload's step (bench.py): dt = 0.1 compute_dt(cfl 0.5).
-    # At the full CFL step the rough field's stage-1 input is already a rejected
-    # (negative-mean) state for the reference at several N
-    dt = 0.1 * ref.compute_dt(m, p, wn, 0.5)
-    w_in = [a.copy() for a in wn]
+    # the C5 workload's step (SURVEY §8(d), bench.py): dt = 0.1 compute_dt(cfl 0.5)
+    dt, outs = ref_stages(ri, m, p, wn, stages, 0.1 * ref.compute_dt(m, p, wn, 0.5))
     errs = []
-    for k in stages:
-        want, nlim = ref_stage(ri, m, p, wn, w_in, k, 0.0, dt)
+    for k, (w_in, want, nlim) in zip(stages, outs):
         got = gi.run_stage(k, swdg.State(*wn), swdg.State(*w_in), 0.0, dt)
         info = gi.stage_info(k)
         err = normwise(got.arrays(), want)
         errs.append(err)
+        log = os.environ.get("SWDG_PARITY_LOG")
+        if log:  # measured errors, for profiles/ (the bar stays 1e-12)
+            with open(log, "a") as f:
+                f.write(json.dumps(dict(N=N, viscous=viscous, state=kind, stage=k, dt=dt,
+                                        err=err, n_limited=int(info.n_limited),
+                                        grid_cap=CAPPED[0])) + "\n")
         assert err <= TOL_STAGE, (N, viscous, kind, k, err)
         assert info.accepted
         assert info.n_limited == nlim, (info.n_limited, nlim)
         mref = float(np.min(want[0]))
         assert abs(info.min_stage_h - mref) <= TOL_STAGE * float(np.max(np.abs(want[0]))), \
             (info.min_stage_h, mref)
-        w_in = want  # next stage from the reference's output
     return errs
 
 
@@ -138,10 +160,12 @@ def test_c5_viscous_stage(N):
 def test_c5_stage_few_ctas(N, viscous):
     """Every persistent kernel family on 5 CTAs: each CTA claims hundreds of groups."""
     swdg.set_grid_cap(5)
+    CAPPED[0] = 5
     try:
         check_stage(N, viscous, "rough", stages=(0, 1))
     finally:
         swdg.set_grid_cap(0)
+        CAPPED[0] = 0
 
 
 def test_c5_fused_step_diagnostics():
