@@ -3,10 +3,11 @@
 // diagnostic, sm_100a FP64, compiled with --fmad=false (every per-node
 // expression rounds like the reference's Release build).
 //
-//   k_step_sums    one coalesced pass over the nodes: total_mass, total_entropy
-//                  (field.hpp:39-61) as fixed-order block partials, min_height
-//                  (field.hpp:63-67) and the compute_dt candidates
-//                  (timeloop.hpp:53-75) as order-independent minima.
+//   k_step_diag    tile by tile: total_mass, total_entropy (field.hpp:39-61) as
+//                  fixed-order block partials, min_height (field.hpp:63-67), the
+//                  compute_dt candidates (timeloop.hpp:53-75) and the
+//                  min_positivity_dt bounds (limiter.hpp:107-166) as
+//                  order-independent minima.
 //   k_step_final   the block partials in a fixed tree order (reproducible).
 //   k_limiter_entropy  limited_entropy_check (limiter.hpp:88-101) for the
 //                  elements post_stage limited (timeloop.hpp:221-229): the
@@ -16,8 +17,10 @@
 //                  does (limiter.hpp:43-84).
 //
 // The node pass reads h, hu, hv, J, b and the two CFL lengths once (56 B per
-// node, 16-byte vector loads); a grid of a fixed number of CTAs makes the
-// partial sums independent of the device, so a run is bitwise repeatable.
+// node), the face pass the face arrays (n_x, n_y, a: 12 B per node at N=7) and
+// the traces; a grid of a fixed number of CTAs with a static tile assignment
+// makes the partial sums independent of the device and of timing, so a run is
+// bitwise repeatable.
 #include <cuda_runtime.h>
 
 #include "swdg_device.cuh"
@@ -105,50 +108,6 @@ __device__ __forceinline__ void node_terms(const Mesh& M, const Phys& P, double 
   acc.klen = l < acc.klen ? l : acc.klen;
 }
 
-__global__ void __launch_bounds__(kSumThreads) k_step_sums(Mesh M, Phys P, CState S,
-                                                           double* partial, Flags* F) {
-  const int nn = M.n_owned * M.np;  // int32 node indices (checked at create)
-  const double order = 2.0 * M.degree + 1.0;
-  NodeAcc acc;
-  // pairs of nodes per thread (16-byte loads): arrays are 16-byte aligned and
-  // every element block has an even length when np is even; odd np takes the
-  // scalar loop
-  const int stride = gridDim.x * blockDim.x;
-  const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
-  if ((M.np & 1) == 0) {
-    const int np2 = nn / 2;
-    for (int q = t0; q < np2; q += stride) {
-      const double2 h = __ldg(reinterpret_cast<const double2*>(S.h) + q);
-      const double2 hu = __ldg(reinterpret_cast<const double2*>(S.hu) + q);
-      const double2 hv = __ldg(reinterpret_cast<const double2*>(S.hv) + q);
-      const double2 j = __ldg(reinterpret_cast<const double2*>(M.jac) + q);
-      const double2 b = __ldg(reinterpret_cast<const double2*>(M.b) + q);
-      const double2 lx = __ldg(reinterpret_cast<const double2*>(M.len_xi) + q);
-      const double2 le = __ldg(reinterpret_cast<const double2*>(M.len_eta) + q);
-      node_terms(M, P, order, 2 * q, h.x, hu.x, hv.x, j.x, b.x, lx.x, le.x, acc);
-      node_terms(M, P, order, 2 * q + 1, h.y, hu.y, hv.y, j.y, b.y, lx.y, le.y, acc);
-    }
-  } else {
-    for (int n = t0; n < nn; n += stride)
-      node_terms(M, P, order, n, __ldg(S.h + n), __ldg(S.hu + n), __ldg(S.hv + n),
-                 __ldg(M.jac + n), __ldg(M.b + n), __ldg(M.len_xi + n), __ldg(M.len_eta + n),
-                 acc);
-  }
-  block_sum2(acc.mass, acc.ent);
-  if (threadIdx.x == 0) {
-    partial[2 * blockIdx.x] = acc.mass;
-    partial[2 * blockIdx.x + 1] = acc.ent;
-  }
-  const unsigned long long kmin = block_min_key(acc.kmin);
-  const unsigned long long kdt = block_min_key(acc.kdt);
-  const unsigned long long klen = block_min_key(acc.klen);
-  if (threadIdx.x == 0) {
-    if (kmin != ~0ull) atomicMin(&F->min_h_key, kmin);
-    if (kdt != ~0ull) atomicMin(&F->dt_key, kdt);
-    if (klen != ~0ull) atomicMin(&F->minlen_key, klen);
-  }
-}
-
 __global__ void __launch_bounds__(1024) k_step_final(const double* partial, int nparts,
                                                      double* out2) {
   double a = 0.0, b = 0.0;
@@ -225,18 +184,6 @@ __global__ void k_limiter_entropy(Mesh M, Phys P, StageArgs A, const Flags* F,
 __device__ __forceinline__ double posdt_bound(const Mesh& M, const Phys& P, const CState& S,
                                                long long idx);
 
-__global__ void k_posdt(Mesh M, Phys P, CState S, Flags* F) {
-  unsigned long long key = ~0ull;
-  const long long nf = (long long)M.n_owned * 4 * M.n1;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < nf;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const unsigned long long k = order_key(posdt_bound(M, P, S, idx));
-    key = k < key ? k : key;
-  }
-  key = block_min_key(key);  // one atomic per block
-  if (threadIdx.x == 0) atomicMin(&F->posdt_key, key);
-}
-
 __device__ __forceinline__ double posdt_bound(const Mesh& M, const Phys& P, const CState& S,
                                                long long idx) {
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
@@ -279,6 +226,53 @@ __device__ __forceinline__ double posdt_bound(const Mesh& M, const Phys& P, cons
   return bound;
 }
 
+// All StepDiagnostics reductions in one pass, element tile by element tile: a
+// CTA owns a fixed (static) set of tiles of T elements; per tile it first runs
+// the node terms (mass, entropy, min h, CFL candidates; coalesced loads) and then
+// the tile's face-node positivity bounds, whose own-side state was just read
+// (L1/L2 hits) and whose neighbour traces are mostly L2 hits (the tiles of all
+// CTAs advance together).  Partial sums are per CTA in a fixed order.
+template <int T>
+__global__ void __launch_bounds__(kSumThreads) k_step_diag(Mesh M, Phys P, CState S,
+                                                           double* partial, Flags* F) {
+  const int np = M.np, n1 = M.n1;
+  const int ntiles = (M.n_owned + T - 1) / T;
+  const double order = 2.0 * M.degree + 1.0;
+  NodeAcc acc;
+  unsigned long long kpos = ~0ull;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int e0 = tile * T, ne = min(T, M.n_owned - e0);
+    const int n0 = e0 * np, nn = ne * np;
+    for (int r = threadIdx.x; r < nn; r += blockDim.x) {
+      const int n = n0 + r;
+      node_terms(M, P, order, n, __ldg(S.h + n), __ldg(S.hu + n), __ldg(S.hv + n),
+                 __ldg(M.jac + n), __ldg(M.b + n), __ldg(M.len_xi + n), __ldg(M.len_eta + n),
+                 acc);
+    }
+    const long long f0 = (long long)e0 * 4 * n1;
+    const int nf = ne * 4 * n1;
+    for (int r = threadIdx.x; r < nf; r += blockDim.x) {
+      const unsigned long long k = order_key(posdt_bound(M, P, S, f0 + r));
+      kpos = k < kpos ? k : kpos;
+    }
+  }
+  block_sum2(acc.mass, acc.ent);
+  if (threadIdx.x == 0) {
+    partial[2 * blockIdx.x] = acc.mass;
+    partial[2 * blockIdx.x + 1] = acc.ent;
+  }
+  const unsigned long long kmin = block_min_key(acc.kmin);
+  const unsigned long long kdt = block_min_key(acc.kdt);
+  const unsigned long long klen = block_min_key(acc.klen);
+  const unsigned long long kp = block_min_key(kpos);
+  if (threadIdx.x == 0) {
+    if (kmin != ~0ull) atomicMin(&F->min_h_key, kmin);
+    if (kdt != ~0ull) atomicMin(&F->dt_key, kdt);
+    if (klen != ~0ull) atomicMin(&F->minlen_key, klen);
+    if (kp != ~0ull) atomicMin(&F->posdt_key, kp);
+  }
+}
+
 // total_mass / total_entropy in the reference's own order (field.hpp:39-61: one
 // serial sum over e, i, j): exact mode's diagnostics are then bitwise the
 // reference's.  One warp: the lanes form 32 consecutive terms, lane 0 adds them
@@ -314,27 +308,26 @@ __global__ void __launch_bounds__(32) k_serial_sums(Mesh M, Phys P, CState S, do
 
 int step_sum_partials() { return kSumBlocks; }
 
-int launch_step_sums(const Mesh& M, const Phys& P, CState S, double* partial, double* out2,
-                     Flags* F, cudaStream_t st) {
-  k_step_sums<<<kSumBlocks, kSumThreads, 0, st>>>(M, P, S, partial, F);
-  k_step_final<<<1, 1024, 0, st>>>(partial, kSumBlocks, out2);
-  return 2;
-}
 
 // StepDiagnostics reductions of a state (driver.hpp:117-127): mass, entropy,
 // min h and the CFL candidates, then the positivity bound.  serial = the
 // reference's summation order (exact mode).
 int launch_diagnostics(const Mesh& M, const Phys& P, CState S, double* partial, double* out2,
                        Flags* F, cudaStream_t st, bool serial) {
-  int n = launch_step_sums(M, P, S, partial, out2, F, st);
-  if (serial) {
-    k_serial_sums<<<1, 32, 0, st>>>(M, P, S, out2);
-    ++n;
+  // tiles of ~1024 nodes (4 per thread): T = 1024 / (N+1)^2 elements
+  const int T = M.np <= 16 ? 64 : M.np <= 64 ? 16 : M.np <= 128 ? 8 : 4;
+  switch (T) {
+    case 64: k_step_diag<64><<<kSumBlocks, kSumThreads, 0, st>>>(M, P, S, partial, F); break;
+    case 16: k_step_diag<16><<<kSumBlocks, kSumThreads, 0, st>>>(M, P, S, partial, F); break;
+    case 8: k_step_diag<8><<<kSumBlocks, kSumThreads, 0, st>>>(M, P, S, partial, F); break;
+    default: k_step_diag<4><<<kSumBlocks, kSumThreads, 0, st>>>(M, P, S, partial, F); break;
   }
-  const long long nf = (long long)M.n_owned * 4 * M.n1;
-  const long long pb = (nf + 255) / 256;
-  k_posdt<<<(unsigned)(pb < 148 * 16 ? pb : 148 * 16), 256, 0, st>>>(M, P, S, F);
-  return n + 1;
+  k_step_final<<<1, 1024, 0, st>>>(partial, kSumBlocks, out2);
+  if (serial) {  // exact mode: the reference's serial summation order
+    k_serial_sums<<<1, 32, 0, st>>>(M, P, S, out2);
+    return 3;
+  }
+  return 2;
 }
 
 int launch_limiter_entropy(const Mesh& M, const Phys& P, const StageArgs& A, const Flags* F,

@@ -62,10 +62,8 @@ SWDG_FAST_PART_DECL(p2)
 #undef SWDG_FAST_PART_DECL
 
 // per-step reductions (kernels_step.cu, --fmad=false): mass/entropy partials
-// (step_sum_partials() pairs), min h and CFL candidates into F, sums into out2
+// (step_sum_partials() pairs) for launch_diagnostics
 int step_sum_partials();
-int launch_step_sums(const Mesh& M, const Phys& P, CState S, double* partial, double* out2,
-                     Flags* F, cudaStream_t st);
 // limited_entropy_check of the elements a stage limited (A.rhs holds its dW/dt)
 int launch_limiter_entropy(const Mesh& M, const Phys& P, const StageArgs& A, const Flags* F,
                            unsigned long long* key, cudaStream_t st);
