@@ -34,7 +34,7 @@ SOURCES = {
     "kernels_fast_p0": ("kernels_fast.cu", ["-DSWDG_PART=0", "-DSWDG_N1_LO=2", "-DSWDG_N1_HI=7"]),
     "kernels_fast_p1": ("kernels_fast.cu", ["-DSWDG_PART=1", "-DSWDG_N1_LO=8", "-DSWDG_N1_HI=11"]),
     "kernels_fast_p2": ("kernels_fast.cu", ["-DSWDG_PART=2", "-DSWDG_N1_LO=12", "-DSWDG_N1_HI=16"]),
-    "kernels_mesh": ("kernels_mesh.cu", []),
+    "kernels_mesh": ("kernels_mesh.cu", ["--fmad=false"]),
     "kernels_bench": ("kernels_bench.cu", []),
     "host_mesh": ("host_mesh.cpp", []),
 }

@@ -1,11 +1,12 @@
 // kernels_mesh.cu — device generation of the structured curvilinear meshes
-// (mesh.hpp:114-232, 294-379) straight into the context's geometry arrays, so
-// the 1M-element throughput meshes never touch host memory.
-// Same algorithm as the reference (transfinite blend of the four mapped edge
-// curves sampled at LGL nodes, metrics by differentiating the nodal
-// coordinate polynomials, normals/J_surf from the face metrics); FMA and CUDA
-// libm make it agree with the host build to rounding, not bitwise — the
-// parity tests use reference-built meshes.
+// (mesh.hpp:114-232, 294-379) for the 1M-element throughput meshes (SURVEY §8d,
+// C5): the transfinite blend of the four mapped edge curves sampled at the LGL
+// nodes and the metrics by differentiating the nodal coordinate polynomials, in
+// the reference's expression order.  Compiled with --fmad=false and free of
+// device libm (the wavy map's sines come from a host table, glibc), so x, y,
+// the metrics, J and the polynomial bathymetries are bitwise the reference's
+// host build; the host (swdg_gpu.cu) finishes the hypot- and sin-dependent
+// fields with glibc, as the reference does.
 #include <cuda_runtime.h>
 
 #include "swdg_device.cuh"
@@ -18,7 +19,8 @@ struct Pt {
   double x, y;
 };
 
-__device__ Pt map_point(const MeshSpecDev& s, double u, double v) {
+// su, sv: sin(2 pi u), sin(2 pi v) of this (u, v) from the host tables (wavy only)
+__device__ Pt map_point(const MeshSpecDev& s, double u, double v, double su, double sv) {
   Pt p;
   switch (s.kind) {
     case 0:  // cartesian (mesh.hpp:342-349)
@@ -35,7 +37,7 @@ __device__ Pt map_point(const MeshSpecDev& s, double u, double v) {
       break;
     }
     default: {  // wavy (mesh.hpp:370-379)
-      const double w = sin(2.0 * M_PI * u) * sin(2.0 * M_PI * v);
+      const double w = su * sv;
       p.x = s.x0 + (u + s.extra * w) * (s.x1 - s.x0);
       p.y = s.y0 + (v - 0.75 * s.extra * w) * (s.y1 - s.y0);
       break;
@@ -44,20 +46,24 @@ __device__ Pt map_point(const MeshSpecDev& s, double u, double v) {
   return p;
 }
 
-__device__ Pt curve(const MeshSpecDev& s, double u0, double v0, double u1, double v1, double r) {
+// BoundaryCurve of structured_mesh (mesh.hpp:313-318): map(u0 + t (u1 - u0),
+// v0 + t (v1 - v0)), t = (1 + r) / 2.  A curve varies u (south/north: su = the
+// table entry of sample k, sv fixed) or v (west/east).
+__device__ Pt curve(const MeshSpecDev& s, double u0, double v0, double u1, double v1, double r,
+                    double su, double sv) {
   const double t = 0.5 * (1.0 + r);
-  return map_point(s, u0 + t * (u1 - u0), v0 + t * (v1 - v0));
+  return map_point(s, u0 + t * (u1 - u0), v0 + t * (v1 - v0), su, sv);
 }
 
+// the closures of oracle/ref_capi.cpp ref_mesh_bathymetry without libm; kinds 4
+// and 6 (sines) are sampled on the host
 __device__ double bathymetry(const MeshSpecDev& s, double x, double y) {
   const double* p = s.bathy;
   switch (s.bathy_kind) {
     case 1: return p[0];
     case 2: return p[0] * x + p[1] * y + p[2];
     case 3: return p[0] * (x * x + y * y);
-    case 4: return 0.1 + 0.05 * sin(2.0 * M_PI * x) * sin(2.0 * M_PI * y);
     case 5: return x < p[0] ? p[1] : p[2];
-    case 6: return p[0] + p[1] * sin(p[2] * x) * sin(p[2] * y);
     default: return 0.0;
   }
 }
@@ -74,10 +80,22 @@ __global__ void k_coords(MeshSpecDev s, const double* nodes, int n1, long long n
   const double u0 = (double)ex / s.kx, u1 = (double)(ex + 1) / s.kx;
   const double v0 = (double)ey / s.ky, v1 = (double)(ey + 1) / s.ky;
   const double xi = nodes[i], eta = nodes[j];
-  const Pt S = curve(s, u0, v0, u1, v0, xi), Nn = curve(s, u0, v1, u1, v1, xi);
-  const Pt W = curve(s, u0, v0, u0, v1, eta), E = curve(s, u1, v0, u1, v1, eta);
-  const Pt sw = curve(s, u0, v0, u1, v0, -1.0), se = curve(s, u0, v0, u1, v0, 1.0);
-  const Pt nw = curve(s, u0, v1, u1, v1, -1.0), ne = curve(s, u0, v1, u1, v1, 1.0);
+  const bool wavy = s.kind == 2;
+  const int n2 = n1 + 2;
+  // table entries: u samples along south/north (k = i, corners n1, n1 + 1), the
+  // fixed u0 / u1 of west/east; likewise v
+  auto SU = [&](int k) { return wavy ? s.sin_u[ex * n2 + k] : 0.0; };
+  auto SV = [&](int k) { return wavy ? s.sin_v[ey * n2 + k] : 0.0; };
+  const double su0 = wavy ? s.sin_ue[ex] : 0.0, su1 = wavy ? s.sin_ue[ex + 1] : 0.0;
+  const double sv0 = wavy ? s.sin_ve[ey] : 0.0, sv1 = wavy ? s.sin_ve[ey + 1] : 0.0;
+  const Pt S = curve(s, u0, v0, u1, v0, xi, SU(i), sv0);
+  const Pt Nn = curve(s, u0, v1, u1, v1, xi, SU(i), sv1);
+  const Pt W = curve(s, u0, v0, u0, v1, eta, su0, SV(j));
+  const Pt E = curve(s, u1, v0, u1, v1, eta, su1, SV(j));
+  const Pt sw = curve(s, u0, v0, u1, v0, -1.0, SU(n1), sv0);
+  const Pt se = curve(s, u0, v0, u1, v0, 1.0, SU(n1 + 1), sv0);
+  const Pt nw = curve(s, u0, v1, u1, v1, -1.0, SU(n1), sv1);
+  const Pt ne = curve(s, u0, v1, u1, v1, 1.0, SU(n1 + 1), sv1);
   const double a00 = 0.25 * (1.0 - xi) * (1.0 - eta), a10 = 0.25 * (1.0 + xi) * (1.0 - eta);
   const double a01 = 0.25 * (1.0 - xi) * (1.0 + eta), a11 = 0.25 * (1.0 + xi) * (1.0 + eta);
   x[n] = 0.5 * (1.0 - eta) * S.x + 0.5 * (1.0 + eta) * Nn.x + 0.5 * (1.0 - xi) * W.x +
@@ -109,35 +127,8 @@ __global__ void k_metrics(MeshSpecDev s, const double* D, int n1, long long nn, 
   o.y_xi[n] = yxi;
   o.y_eta[n] = yeta;
   o.jac[n] = jac;
-  o.b[n] = bathymetry(s, x[n], y[n]);
-  o.len_xi[n] = 2.0 * jac / hypot(xeta, yeta);
-  o.len_eta[n] = 2.0 * jac / hypot(xxi, yxi);
+  if (!bathy_needs_libm(s.bathy_kind)) o.b[n] = bathymetry(s, x[n], y[n]);
   if (!(jac > 0.0)) atomicExch(o.bad_jac, 1);
-}
-
-// compute_metrics face part (mesh.hpp:192-218), one thread per face node
-__global__ void k_faces(int n1, long long nfn, MeshOut o) {
-  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= nfn) return;
-  const int t = (int)(idx % n1), face = (int)((idx / n1) % 4);
-  const long long e = idx / (4 * n1);
-  const long long n = e * n1 * n1 + face_node(n1, face, t);
-  double js, nx, ny;
-  if (face == 1 || face == 3) {
-    js = hypot(o.y_eta[n], o.x_eta[n]);
-    const double sg = face == 1 ? 1.0 : -1.0;
-    nx = sg * o.y_eta[n] / js;
-    ny = -sg * o.x_eta[n] / js;
-  } else {
-    js = hypot(o.y_xi[n], o.x_xi[n]);
-    const double sg = face == 0 ? 1.0 : -1.0;
-    nx = sg * o.y_xi[n] / js;
-    ny = -sg * o.x_xi[n] / js;
-  }
-  o.fjs[idx] = js;
-  o.fnx[idx] = nx;
-  o.fny[idx] = ny;
-  o.fa[idx] = o.jac[n] / js;
 }
 
 }  // namespace
@@ -145,11 +136,9 @@ __global__ void k_faces(int n1, long long nfn, MeshOut o) {
 int launch_structured_mesh(const MeshSpecDev& s, const double* nodes, const double* D, int n1,
                            const MeshOut& o, cudaStream_t st) {
   const long long nn = s.n_elem * n1 * n1;
-  const long long nfn = s.n_elem * 4 * n1;
   k_coords<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(s, nodes, n1, nn, o.x, o.y);
   k_metrics<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(s, D, n1, nn, o.x, o.y, o);
-  k_faces<<<(unsigned)((nfn + 255) / 256), 256, 0, st>>>(n1, nfn, o);
-  return 3;
+  return 2;
 }
 
 }  // namespace swdg_dev

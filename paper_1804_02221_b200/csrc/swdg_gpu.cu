@@ -10,6 +10,7 @@
 #include <cstring>
 #include <limits>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/swdg_gpu.h"
@@ -484,6 +485,104 @@ void allocate(swdg_gpu* c, int K, int n_owned, int N, const std::vector<int4>& e
   c->r_h.assign(K, 0.0);
 }
 
+// The libm-dependent geometry of a device-generated mesh, with the host's glibc
+// as the reference computes it: the face arrays (compute_metrics mesh.hpp:192-218:
+// hypot, normals, J_surf, a = J / J_surf), the compute_dt lengths 2J/hypot
+// (timeloop.hpp:62-65) and the sine bathymetries (sample_bathymetry :223-232).
+// Chunks of elements, threads over elements; the polynomial work stays on the
+// device.
+void finish_mesh_on_host(swdg_gpu* c, const swdg_structured_spec& spec, int n1) {
+  const Mesh& M = c->M;
+  const int np = n1 * n1, K = M.K;
+  const bool bathy = bathy_needs_libm(spec.bathy_kind);
+  const int chunk = std::max(1, (1 << 22) / np);  // ~4M nodes per chunk
+  std::vector<double> ye, xe, yx, xx, jac, x, y, lx, le, b, fj, fx, fy, fa;
+  auto dl = [&](std::vector<double>& h, const double* d, long long off, long long n) {
+    h.resize(n);
+    ck(cudaMemcpy(h.data(), d + off, n * sizeof(double), cudaMemcpyDeviceToHost), "geometry D2H");
+  };
+  auto ul = [&](double* d, const std::vector<double>& h, long long off) {
+    ck(cudaMemcpy(d + off, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice),
+       "geometry H2D");
+  };
+  const unsigned nthreads = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  for (int e0 = 0; e0 < K; e0 += chunk) {
+    const int ne = std::min(chunk, K - e0);
+    const long long n0 = (long long)e0 * np, nn = (long long)ne * np;
+    const long long f0 = (long long)e0 * 4 * n1, nf = (long long)ne * 4 * n1;
+    dl(ye, M.ye, n0, nn);
+    dl(xe, M.xe, n0, nn);
+    dl(yx, M.yx, n0, nn);
+    dl(xx, M.xx, n0, nn);
+    dl(jac, M.jac, n0, nn);
+    if (bathy) {
+      dl(x, c->xy, n0, nn);
+      dl(y, c->xy + c->nn, n0, nn);
+      b.resize(nn);
+    }
+    lx.resize(nn);
+    le.resize(nn);
+    fj.resize(nf);
+    fx.resize(nf);
+    fy.resize(nf);
+    fa.resize(nf);
+    const double* p = spec.bathy;
+    auto work = [&](int t) {
+      for (int el = t; el < ne; el += (int)nthreads) {
+        const long long a = (long long)el * np;
+        for (int q = 0; q < np; ++q) {
+          const long long n = a + q;
+          lx[n] = 2.0 * jac[n] / std::hypot(xe[n], ye[n]);
+          le[n] = 2.0 * jac[n] / std::hypot(xx[n], yx[n]);
+          if (bathy)
+            b[n] = spec.bathy_kind == 4
+                       ? 0.1 + 0.05 * std::sin(2.0 * M_PI * x[n]) * std::sin(2.0 * M_PI * y[n])
+                       : p[0] + p[1] * std::sin(p[2] * x[n]) * std::sin(p[2] * y[n]);
+        }
+        for (int face = 0; face < 4; ++face)
+          for (int tt = 0; tt < n1; ++tt) {
+            const long long n = a + face_node(n1, face, tt);
+            const long long f = ((long long)el * 4 + face) * n1 + tt;
+            double js, nx, ny;
+            if (face == 1) {  // east
+              js = std::hypot(ye[n], xe[n]);
+              nx = ye[n] / js;
+              ny = -xe[n] / js;
+            } else if (face == 3) {  // west
+              js = std::hypot(ye[n], xe[n]);
+              nx = -ye[n] / js;
+              ny = xe[n] / js;
+            } else if (face == 2) {  // north
+              js = std::hypot(yx[n], xx[n]);
+              nx = -yx[n] / js;
+              ny = xx[n] / js;
+            } else {  // south
+              js = std::hypot(yx[n], xx[n]);
+              nx = yx[n] / js;
+              ny = -xx[n] / js;
+            }
+            fj[f] = js;
+            fx[f] = nx;
+            fy[f] = ny;
+            fa[f] = jac[n] / js;
+          }
+      }
+    };
+    std::vector<std::thread> pool;
+    for (unsigned t = 1; t < nthreads; ++t) pool.emplace_back(work, (int)t);
+    work(0);
+    for (auto& th : pool) th.join();
+    auto wr = [](const double* q) { return const_cast<double*>(q); };
+    ul(wr(M.len_xi), lx, n0);
+    ul(wr(M.len_eta), le, n0);
+    ul(wr(M.fjs), fj, f0);
+    ul(wr(M.fnx), fx, f0);
+    ul(wr(M.fny), fy, f0);
+    ul(wr(M.fa), fa, f0);
+    if (bathy) ul(wr(M.b), b, n0);
+  }
+}
+
 swdg_gpu* new_context(const swdg_params* p, int device) {
   auto* c = new swdg_gpu;
   c->device = device;
@@ -639,7 +738,39 @@ int swdg_gpu_create_structured_part(const swdg_structured_spec* s, const swdg_pa
       ck(cudaMemcpy(gid, local_to_global, n_local * sizeof(int), cudaMemcpyHostToDevice), "gid");
     }
     MeshSpecDev sd{s->kind, s->kx, s->ky, s->bathy_kind, s->x0, s->x1, s->y0, s->y1, s->extra,
-                   {s->bathy[0], s->bathy[1], s->bathy[2], s->bathy[3]}, gid, Kl};
+                   {s->bathy[0], s->bathy[1], s->bathy[2], s->bathy[3]}, gid, Kl,
+                   nullptr, nullptr, nullptr, nullptr};
+    if (s->kind == SWDG_MESH_WAVY) {
+      // sin(2 pi u) of every u the edge curves sample, with the host's libm
+      // (build_wavy_mesh mesh.hpp:370-379 via structured_mesh :313-327)
+      auto table = [&](int k, std::vector<double>& samp, std::vector<double>& edge) {
+        samp.assign((size_t)k * (n1 + 2), 0.0);
+        edge.assign((size_t)k + 1, 0.0);
+        for (int e = 0; e <= k; ++e) edge[e] = std::sin(2.0 * M_PI * (static_cast<double>(e) / k));
+        for (int e = 0; e < k; ++e) {
+          const double a = static_cast<double>(e) / k, b = static_cast<double>(e + 1) / k;
+          for (int q = 0; q < n1 + 2; ++q) {
+            const double r = q < n1 ? nodes[q] : (q == n1 ? -1.0 : 1.0);
+            const double t = 0.5 * (1.0 + r);
+            samp[(size_t)e * (n1 + 2) + q] = std::sin(2.0 * M_PI * (a + t * (b - a)));
+          }
+        }
+      };
+      std::vector<double> su, sue, sv, sve;
+      table(s->kx, su, sue);
+      table(s->ky, sv, sve);
+      double* tb = c->dalloc<double>(su.size() + sue.size() + sv.size() + sve.size());
+      size_t off = 0;
+      for (const std::vector<double>* v : {&su, &sue, &sv, &sve}) {
+        ck(cudaMemcpy(tb + off, v->data(), v->size() * sizeof(double), cudaMemcpyHostToDevice),
+           "sin table");
+        off += v->size();
+      }
+      sd.sin_u = tb;
+      sd.sin_ue = tb + su.size();
+      sd.sin_v = sd.sin_ue + sue.size();
+      sd.sin_ve = sd.sin_v + sv.size();
+    }
     const Mesh& M = c->M;
     auto wr = [](const double* p) { return const_cast<double*>(p); };
     MeshOut o{c->xy, c->xy + nn, wr(M.xx), wr(M.xe), wr(M.yx), wr(M.ye), wr(M.jac), wr(M.b),
@@ -649,6 +780,7 @@ int swdg_gpu_create_structured_part(const swdg_structured_spec* s, const swdg_pa
     ck(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "bad D2H");
     ck(cudaStreamSynchronize(c->stream), "mesh sync");
     if (hbad) throw InputError{"mesh rejected: nonpositive Jacobian"};
+    finish_mesh_on_host(c, *s, n1);
   });
 }
 

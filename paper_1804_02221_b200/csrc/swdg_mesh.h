@@ -11,7 +11,16 @@ struct MeshSpecDev {
   double bathy[4];
   const int* gid;  // local -> global element id (partitions), nullptr = identity
   long long n_elem;  // elements generated
+  // wavy map: the host's sin(2 pi u) of every u the edge curves sample
+  // (mesh.hpp:370-379), so the coordinates are bitwise the reference's:
+  // sin_u[ex * (n1 + 2) + k] at u = u0 + t_k (u1 - u0), k < n1 the LGL nodes,
+  // k = n1, n1 + 1 the corners t = 0, 1; sin_ue[ex] at u = ex / kx.  Same for v.
+  const double *sin_u, *sin_ue, *sin_v, *sin_ve;
 };
+
+// bathymetry kinds whose closure calls libm: sampled on the host (glibc), like the
+// reference, from the device coordinates
+__host__ __device__ inline bool bathy_needs_libm(int kind) { return kind == 4 || kind == 6; }
 
 struct MeshOut {
   double *x, *y, *x_xi, *x_eta, *y_xi, *y_eta, *jac, *b, *len_xi, *len_eta;
@@ -19,6 +28,9 @@ struct MeshOut {
   int* bad_jac;
 };
 
+// coordinates, metrics, J and the polynomial bathymetries on the device (no
+// FMA, no libm: bitwise the reference); the libm-dependent fields (CFL lengths
+// and face arrays via hypot, sine bathymetries) are finished by the host
 int launch_structured_mesh(const MeshSpecDev& s, const double* nodes, const double* D, int n1,
                            const MeshOut& o, cudaStream_t st);
 
