@@ -88,6 +88,7 @@ struct swdg_gpu {
   double *partial = nullptr, *sums = nullptr;
   int int_lo = 0, int_hi = 0;   // interior element range (halo overlap), empty by default
   int reserve_sms = 0;          // SMs the next stage launch leaves free
+  bool no_graphs = std::getenv("SWDG_NO_GRAPHS") != nullptr;  // A/B: eager launches
   int* gctr = nullptr;          // device group counter of the persistent stage kernels
   // device report: Flags[4] (one per stage + one for the step reductions) and the
   // mass/entropy sums, contiguous so one copy (one host sync) reads a whole step
@@ -107,6 +108,16 @@ struct swdg_gpu {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t snap_ready = nullptr, snap_done = nullptr;
   const double* snap_buf = nullptr;  // W[0] when the copy was issued; null when none pending
+  // CUDA graph of two device-resident steps (the W/A ping-pong returns to its
+  // starting assignment after two) for fixed-dt stepping: one launch per two
+  // steps instead of ~2 x (3 stage kernels + 3 counter memsets + reductions)
+  cudaStream_t graph_stream = nullptr;
+  cudaEvent_t graph_in = nullptr, graph_out = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  double graph_dt = 0.0;
+  bool graph_red = false;
+  const double* graph_w0 = nullptr;
+  int64_t graph_launches = 0;  // kernels per replay
 
   std::vector<double> x, y, eps_h, r_h, fbuf;
   swdg_forcing_fn forcing = nullptr;
@@ -130,6 +141,10 @@ struct swdg_gpu {
     for (void* p : allocations) cudaFree(p);
     if (rep_h) cudaFreeHost(rep_h);
     if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (graph) cudaGraphExecDestroy(graph);
+    if (graph_stream) cudaStreamDestroy(graph_stream);
+    if (graph_in) cudaEventDestroy(graph_in);
+    if (graph_out) cudaEventDestroy(graph_out);
     if (snap_ready) cudaEventDestroy(snap_ready);
     if (snap_done) cudaEventDestroy(snap_done);
     if (own_stream && stream) cudaStreamDestroy(stream);
@@ -1025,10 +1040,10 @@ int swdg_gpu_run_steps_ex(swdg_gpu* c, int nsteps, double t, double dt, int flag
     // over the run in the per-stage flags and are folded at the end
     reset_flags(c);
     double* const* outs[3] = {c->A, c->B, c->A};
-    for (int s = 0; s < nsteps; ++s) {
+    auto one_step = [&](double ts) {
       CState in = cs(c->W);
       for (int k = 0; k < 3; ++k) {
-        stage(c, in, outs[k], k, t + s * dt, dt, viscous, nullptr, c->flags + k);
+        stage(c, in, outs[k], k, ts, dt, viscous, nullptr, c->flags + k);
         in = cs(outs[k]);
       }
       // the per-step StepDiagnostics reductions and the next CFL candidate of the
@@ -1038,7 +1053,70 @@ int swdg_gpu_run_steps_ex(swdg_gpu* c, int nsteps, double t, double dt, int flag
                                                    c->flags + kDiagFlags, c->stream, false),
                                 "launch_diagnostics");
       for (int k = 0; k < 3; ++k) std::swap(c->W[k], c->A[k]);
+    };
+    int s0 = 0;
+    if (nsteps >= 2 && !c->no_graphs) {
+      // replay the two-step graph (re-captured when dt, the reductions flag or the
+      // buffer assignment changed); the kernels' time argument only feeds forcing,
+      // which this path excludes
+      if (c->snap_buf) {  // a pending snapshot copy reads W: let it land first
+        ck(cudaEventSynchronize(c->snap_done), "snapshot sync");
+        c->snap_buf = nullptr;
+      }
+      if (!c->graph_stream) {
+        ck(cudaStreamCreateWithFlags(&c->graph_stream, cudaStreamNonBlocking), "graph stream");
+        ck(cudaEventCreateWithFlags(&c->graph_in, cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&c->graph_out, cudaEventDisableTiming), "event");
+      }
+      bool stale = !c->graph || c->graph_dt != dt || c->graph_red != reductions;
+      if (!stale && c->graph_w0 != c->W[0]) {  // odd step count last time: realign
+        one_step(t);
+        s0 = 1;
+      }
+      if (stale) {
+        // one eager step first: first-launch work (shared-memory attributes,
+        // occupancy queries) stays out of the capture
+        one_step(t);
+        s0 = 1;
+        if (c->graph) cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+        cudaStream_t user = c->stream;
+        c->stream = c->graph_stream;
+        const int64_t l0 = c->launches;
+        const double* w0 = c->W[0];
+        ck(cudaStreamBeginCapture(c->graph_stream, cudaStreamCaptureModeThreadLocal), "capture");
+        try {
+          one_step(t + s0 * dt);
+          one_step(t + (s0 + 1) * dt);
+        } catch (...) {
+          cudaGraph_t g = nullptr;
+          cudaStreamEndCapture(c->graph_stream, &g);
+          if (g) cudaGraphDestroy(g);
+          c->stream = user;
+          throw;
+        }
+        cudaGraph_t g = nullptr;
+        ck(cudaStreamEndCapture(c->graph_stream, &g), "end capture");
+        c->stream = user;
+        ck(cudaGraphInstantiate(&c->graph, g, 0), "graph instantiate");
+        cudaGraphDestroy(g);
+        c->graph_launches = c->launches - l0;
+        c->launches = l0;
+        c->graph_dt = dt;
+        c->graph_red = reductions;
+        c->graph_w0 = w0;
+      }
+      ck(cudaEventRecord(c->graph_in, c->stream), "graph in");
+      ck(cudaStreamWaitEvent(c->graph_stream, c->graph_in, 0), "graph wait");
+      if (c->graph_w0 != c->W[0]) throw CudaError{cudaErrorUnknown, "graph buffer assignment"};
+      for (; s0 + 2 <= nsteps; s0 += 2) {
+        ck(cudaGraphLaunch(c->graph, c->graph_stream), "graph launch");
+        c->launches += c->graph_launches;
+      }
+      ck(cudaEventRecord(c->graph_out, c->graph_stream), "graph out");
+      ck(cudaStreamWaitEvent(c->stream, c->graph_out, 0), "graph join");
     }
+    for (int s = s0; s < nsteps; ++s) one_step(t + s * dt);
     read_flags(c);
     swdg_step_info r{};
     r.min_stage_h = std::numeric_limits<double>::infinity();

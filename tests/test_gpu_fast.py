@@ -270,3 +270,27 @@ def test_fast_viscous_step(sid, kx, deg):
         assert normwise(s2.arrays(), s1) <= 1e-9
         assert abs(gi.last_max_eps() - a.max_eps) <= 1e-13 * max(a.max_eps, 1e-300)
         s1 = [x.copy() for x in s2.arrays()]
+
+
+@pytest.mark.parametrize("N,visc", [(1, False), (3, False), (7, False), (7, True)])
+def test_run_steps_graph_matches_eager(N, visc, monkeypatch):
+    """run_steps replays a captured two-step CUDA graph (odd counts and a changed
+    dt re-align / re-capture); the result is bitwise the eager launches'."""
+    m = ref.build_mesh("wavy", N, 12, 10, periodic_x=True, periodic_y=True).bathymetry("smooth")
+    smin, smax = swdg.default_sigma_band(max(N, 2))
+    p = ref.params(g=9.81, visc=visc, epsilon0=0.1, sigma_min=smin, sigma_max=smax)
+    s = smooth_state(m, 0.1)
+    outs = []
+    for eager in (False, True):
+        if eager:
+            monkeypatch.setenv("SWDG_NO_GRAPHS", "1")
+        g = swdg.TimeIntegrator(m, cfg_from(p))
+        st = S(s)
+        g.upload(st)
+        dt = 0.2 * g.compute_dt_device(0.5)
+        for n, r in ((7, False), (4, True), (5, False), (2, False)):
+            assert g.run_steps(n, 0.0, dt * (1.0 if n != 4 else 0.5), reductions=r)
+        g.download(st)
+        outs.append(st.arrays())
+    for a, b in zip(*outs):
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
