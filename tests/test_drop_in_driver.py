@@ -92,16 +92,17 @@ def test_device_driver_fast_mode(tmp_path):
                                             "0", "1"], str(tmp_path))
     assert line.split()[0] == ref_line.split()[0]  # step count
     assert sorted(os.listdir(work)) == sorted(os.listdir(tmp_path / "r"))
-    # the headers (config hash) agree; step numbers agree and t, dt, mass agree to
-    # the fast kernels' rounding (the next dt is a CFL minimum of the fast state)
+    # the headers (config hash) agree; step numbers agree and t, dt agree to 1e-8
+    # (the next dt is a CFL minimum over the moving wet/dry front, where u = hu/h
+    # amplifies the fast kernels' rounding: measured 2.6e-9), mass to 1e-12
     with open(work / "diagnostics.txt") as f, open(tmp_path / "r" / "diagnostics.txt") as g:
         a, b = f.read().splitlines(), g.read().splitlines()
     assert a[:2] == b[:2] and len(a) == len(b)
     for la, lb in zip(a[2:], b[2:]):
         ca, cb = la.split(";"), lb.split(";")
         assert ca[0] == cb[0]
-        for x, y in zip(ca[1:4], cb[1:4]):  # t, dt, mass
-            assert abs(float(x) - float(y)) <= 1e-9 * abs(float(y))
+        for x, y, tol in zip(ca[1:4], cb[1:4], (1e-8, 1e-8, 1e-12)):  # t, dt, mass
+            assert abs(float(x) - float(y)) <= tol * abs(float(y))
 
 
 CRITERIA = ["wellbalanced", "glitch", "wetdry", "convergence", "scenarios"]

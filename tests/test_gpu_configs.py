@@ -101,8 +101,14 @@ def ref_stages(ri, m, p, wn, stages, dt):
     run_simulation's reject-and-halve does (driver.hpp:101-111): the CFL step
     ignores the viscous (parabolic) limit, which the rough field with eps0 = 0.1
     exceeds"""
+    halved = False
     for _ in range(30):
         try:
+            if halved:
+                # the largest accepted dt leaves some element mean at the edge of
+                # zero, where theta = mean / (mean - min) is ill-conditioned; a
+                # margin of 4 keeps the comparison about the kernels' arithmetic
+                dt *= 0.25
             outs, w_in = [], [a.copy() for a in wn]
             for k in stages:
                 want, nlim = ref_stage(ri, m, p, wn, w_in, k, 0.0, dt)
@@ -112,6 +118,7 @@ def ref_stages(ri, m, p, wn, stages, dt):
         except RuntimeError as e:  # limit_element: negative element mean (a reject)
             assert "negative element mean" in str(e)
             dt *= 0.5
+            halved = True
     raise AssertionError("no accepted step")
 
 
