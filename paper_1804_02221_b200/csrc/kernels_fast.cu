@@ -37,6 +37,7 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "fast_common.cuh"
 
@@ -537,11 +538,17 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
   uint32_t ph_node = 0;
   int buf = 0;
 
-  // padded in-element offset of node k of this line
-  auto pidx = [&](int k) { return xi ? k * PAD + li : li * PAD + k; };
-
   __shared__ int s_next;  // the next group, claimed by thread 0
   unsigned long long kmin = ~0ull;  // min height key of this thread's elements
+  // The group loop is instantiated per line direction (xi is warp-uniform): the
+  // metric selection (y_eta, x_eta) / -(y_xi, x_xi), the padded node addressing and
+  // the xi-only node phase become compile-time, instead of both loads plus a
+  // select per node value.  Every instantiation passes the same barriers in the
+  // same order.
+  auto group_loop = [&](auto xi_c) {
+  constexpr bool xi = decltype(xi_c)::value;
+  // padded in-element offset of node k of this line
+  auto pidx = [&](int k) { return xi ? k * PAD + li : li * PAD + k; };
   for (int grp = blockIdx.x; grp < ngroups; grp = s_next, buf = P::DB ? buf ^ 1 : 0) {
     const int e0 = M.e_lo + grp * P::E, ne = min(P::E, M.n_owned - e0);
     const bool active = line_ok && el < ne;
@@ -974,6 +981,11 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
       }
     }
   }
+  };
+  if (role < 2)
+    group_loop(std::true_type{});
+  else
+    group_loop(std::false_type{});
   cp_async_wait_all();
   if (hl_blockmin(N1, VISC)) {  // one atomic per CTA for the whole launch
     const unsigned long long bmin = block_min_key(kmin);

@@ -181,16 +181,21 @@ __global__ void k_limiter_entropy(Mesh M, Phys P, StageArgs A, const Flags* F,
 // positivity_dt_bounds (limiter.hpp:107-130) evaluated by every owned
 // element-face node from its own side (the reference evaluates the minus side
 // and, for interior faces, the plus side with the plus normal: the same set).
-
-// own: the element's state at the face node (staged by the caller)
 __device__ __forceinline__ double posdt_bound(const Mesh& M, const Phys& P, const CState& S,
-                                               long long idx, int4 ef, double hm, double hum,
-                                               double hvm) {
+                                               long long idx);
+
+__device__ __forceinline__ double posdt_bound(const Mesh& M, const Phys& P, const CState& S,
+                                               long long idx) {
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
   const int n1 = M.n1;
   const int t = (int)(idx % n1);
+  const int face = (int)((idx / n1) % 4);
+  const int e = (int)(idx / (4 * n1));
+  const int4 ef = M.ef[e * 4 + face];
   if (!(ef.y & EF_PRESENT)) return inf;
+  const long long n = (long long)e * M.np + face_node(n1, face, t);
   const double nx = M.fnx[idx], ny = M.fny[idx], a_scale = M.fa[idx];
+  const double hm = S.h[n], hum = S.hu[n], hvm = S.hv[n];
   double hp, hup, hvp;
   if (ef.y & EF_WALL) {
     const double mn = hum * nx + hvm * ny;
@@ -227,58 +232,29 @@ __device__ __forceinline__ double posdt_bound(const Mesh& M, const Phys& P, cons
 // the tile's face-node positivity bounds, whose own-side state was just read
 // (L1/L2 hits) and whose neighbour traces are mostly L2 hits (the tiles of all
 // CTAs advance together).  Partial sums are per CTA in a fixed order.
-constexpr int kTileNodes = 1024;  // nodes per tile: 4 per thread
-
+template <int T>
 __global__ void __launch_bounds__(kSumThreads) k_step_diag(Mesh M, Phys P, CState S,
-                                                           double* partial, Flags* F, int T) {
-  __shared__ double st[3][kTileNodes];  // the tile's h, hu, hv for the face pass
+                                                           double* partial, Flags* F) {
   const int np = M.np, n1 = M.n1;
   const int ntiles = (M.n_owned + T - 1) / T;
   const double order = 2.0 * M.degree + 1.0;
   NodeAcc acc;
   unsigned long long kpos = ~0ull;
-  constexpr int R = kTileNodes / kSumThreads;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int e0 = tile * T, ne = min(T, M.n_owned - e0);
     const int n0 = e0 * np, nn = ne * np;
-    // the R nodes of this thread: all 7 loads issued before any arithmetic
-    double h[R], hu[R], hv[R], jac[R], b[R], lxi[R], leta[R];
-#pragma unroll
-    for (int k = 0; k < R; ++k) {
-      const int r = threadIdx.x + k * kSumThreads;
-      if (r < nn) {
-        const int n = n0 + r;
-        h[k] = __ldg(S.h + n);
-        hu[k] = __ldg(S.hu + n);
-        hv[k] = __ldg(S.hv + n);
-        jac[k] = __ldg(M.jac + n);
-        b[k] = __ldg(M.b + n);
-        lxi[k] = __ldg(M.len_xi + n);
-        leta[k] = __ldg(M.len_eta + n);
-      }
+    for (int r = threadIdx.x; r < nn; r += blockDim.x) {
+      const int n = n0 + r;
+      node_terms(M, P, order, n, __ldg(S.h + n), __ldg(S.hu + n), __ldg(S.hv + n),
+                 __ldg(M.jac + n), __ldg(M.b + n), __ldg(M.len_xi + n), __ldg(M.len_eta + n),
+                 acc);
     }
-#pragma unroll
-    for (int k = 0; k < R; ++k) {
-      const int r = threadIdx.x + k * kSumThreads;
-      if (r < nn) {
-        node_terms(M, P, order, n0 + r, h[k], hu[k], hv[k], jac[k], b[k], lxi[k], leta[k], acc);
-        st[0][r] = h[k];
-        st[1][r] = hu[k];
-        st[2][r] = hv[k];
-      }
-    }
-    __syncthreads();
     const long long f0 = (long long)e0 * 4 * n1;
     const int nf = ne * 4 * n1;
-    for (int r = threadIdx.x; r < nf; r += kSumThreads) {
-      const int t = r % n1, face = (r / n1) % 4, el = r / (4 * n1);
-      const int4 ef = __ldg(M.ef + (e0 + el) * 4 + face);
-      const int q = el * np + face_node(n1, face, t);
-      const unsigned long long k = order_key(
-          posdt_bound(M, P, S, f0 + r, ef, st[0][q], st[1][q], st[2][q]));
+    for (int r = threadIdx.x; r < nf; r += blockDim.x) {
+      const unsigned long long k = order_key(posdt_bound(M, P, S, f0 + r));
       kpos = k < kpos ? k : kpos;
     }
-    __syncthreads();  // the next tile overwrites the staged state
   }
   block_sum2(acc.mass, acc.ent);
   if (threadIdx.x == 0) {
@@ -338,9 +314,14 @@ int step_sum_partials() { return kSumBlocks; }
 // reference's summation order (exact mode).
 int launch_diagnostics(const Mesh& M, const Phys& P, CState S, double* partial, double* out2,
                        Flags* F, cudaStream_t st, bool serial) {
-  // tiles of at most kTileNodes nodes (4 per thread)
-  const int T = kTileNodes / M.np;
-  k_step_diag<<<kSumBlocks, kSumThreads, 0, st>>>(M, P, S, partial, F, T);
+  // tiles of ~1024 nodes (4 per thread): T = 1024 / (N+1)^2 elements
+  const int T = M.np <= 16 ? 64 : M.np <= 64 ? 16 : M.np <= 128 ? 8 : 4;
+  switch (T) {
+    case 64: k_step_diag<64><<<kSumBlocks, kSumThreads, 0, st>>>(M, P, S, partial, F); break;
+    case 16: k_step_diag<16><<<kSumBlocks, kSumThreads, 0, st>>>(M, P, S, partial, F); break;
+    case 8: k_step_diag<8><<<kSumBlocks, kSumThreads, 0, st>>>(M, P, S, partial, F); break;
+    default: k_step_diag<4><<<kSumBlocks, kSumThreads, 0, st>>>(M, P, S, partial, F); break;
+  }
   k_step_final<<<1, 1024, 0, st>>>(partial, kSumBlocks, out2);
   if (serial) {  // exact mode: the reference's serial summation order
     k_serial_sums<<<1, 32, 0, st>>>(M, P, S, out2);
