@@ -127,8 +127,13 @@ def check_stage(N, viscous, kind, stages=(0,)):
     p = c5_params(N, viscous)
     gi, ri = c5_context(N, viscous)
     wn = c5_state(m, kind)
-    # the C5 workload's step (bench.py): dt = 0.1 compute_dt(cfl 0.5)
-    dt, outs = ref_stages(ri, m, p, wn, stages, 0.1 * ref.compute_dt(m, p, wn, 0.5))
+    # the C5 workload's step (bench.py): dt = 0.1 compute_dt(cfl 0.5).
+    # The rough field with eps0 = 0.1 is far beyond the viscous (parabolic) limit
+    # of that step: stage 2 then leaves element means near zero, where the
+    # limiter's theta = mean / (mean - min) turns ulp-level differences into 1e-8
+    # (measured at N = 7); a tenth of the step keeps it a test of the kernels
+    dt0 = 0.1 * ref.compute_dt(m, p, wn, 0.5) * (0.1 if viscous and kind != "smooth" else 1.0)
+    dt, outs = ref_stages(ri, m, p, wn, stages, dt0)
     errs = []
     for k, (w_in, want, nlim) in zip(stages, outs):
         got = gi.run_stage(k, swdg.State(*wn), swdg.State(*w_in), 0.0, dt)
