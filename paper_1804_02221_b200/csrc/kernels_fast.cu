@@ -183,6 +183,10 @@ struct HL {
   static constexpr int BAR = RED + 2 * E * 2 * 5;
   // transposed node phase (NT): every thread finalises E (N+1)^2 / THREADS nodes;
   // the xi lines leave their accumulators and state next to the eta ones
+  // one instantiation of the group loop per line direction (XI_SPLIT): measured
+  // (B200, 1M elements) inviscid N=5 1.615 -> 1.463 ms/stage; slower at every
+  // other degree (twice the code: N=8 4.34 -> 5.16, N=15 13.2 -> 27.0)
+  static constexpr bool XI_SPLIT = !V && N1 == 6;
   static constexpr bool NT = !V && N1 == 9;  // measured: faster only at N+1 = 9 (4.56 -> 4.34 ms), slower at 6, 7, 8, 10
   static constexpr int NPT = (E * NP + THREADS - 1) / THREADS;  // nodes per thread
   static constexpr int PMAX = NP / 32 + 2;                      // node-warp pieces
@@ -540,13 +544,12 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
 
   __shared__ int s_next;  // the next group, claimed by thread 0
   unsigned long long kmin = ~0ull;  // min height key of this thread's elements
-  // The group loop is instantiated per line direction (xi is warp-uniform): the
-  // metric selection (y_eta, x_eta) / -(y_xi, x_xi), the padded node addressing and
-  // the xi-only node phase become compile-time, instead of both loads plus a
-  // select per node value.  Every instantiation passes the same barriers in the
-  // same order.
+  // With HL::XI_SPLIT the group loop is instantiated per line direction (xi is
+  // warp-uniform): the metric selection (y_eta, x_eta) / -(y_xi, x_xi), the padded
+  // addressing and the xi-only node phase become compile-time.  Every
+  // instantiation passes the same barriers in the same order.
   auto group_loop = [&](auto xi_c) {
-  constexpr bool xi = decltype(xi_c)::value;
+  const bool xi = xi_c;  // a compile-time constant when xi_c is std::integral_constant
   // padded in-element offset of node k of this line
   auto pidx = [&](int k) { return xi ? k * PAD + li : li * PAD + k; };
   for (int grp = blockIdx.x; grp < ngroups; grp = s_next, buf = P::DB ? buf ^ 1 : 0) {
@@ -982,10 +985,14 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
     }
   }
   };
-  if (role < 2)
-    group_loop(std::true_type{});
-  else
-    group_loop(std::false_type{});
+  if constexpr (P::XI_SPLIT) {
+    if (role < 2)
+      group_loop(std::true_type{});
+    else
+      group_loop(std::false_type{});
+  } else {
+    group_loop(role < 2);
+  }
   cp_async_wait_all();
   if (hl_blockmin(N1, VISC)) {  // one atomic per CTA for the whole launch
     const unsigned long long bmin = block_min_key(kmin);
