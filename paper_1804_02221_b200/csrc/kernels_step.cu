@@ -90,14 +90,18 @@ __device__ __forceinline__ void node_terms(const Mesh& M, const Phys& P, double 
                                            double b, double lxi, double leta, NodeAcc& acc) {
   const int loc = n % M.np, i = loc / M.n1, j = loc - i * M.n1;
   const double wi = M.w[i], wj = M.w[j];
-  // total_mass: sum += h * J * w_i * w_j; total_entropy: e * J * w_i * w_j
-  acc.mass += h * jac * wi * wj;
-  acc.ent += entropy(h, hu, hv, b, P) * jac * wi * wj;
-  const unsigned long long kh = order_key(h);
-  acc.kmin = kh < acc.kmin ? kh : acc.kmin;
-  // compute_dt per node (timeloop.hpp:58-71), lengths precomputed with glibc hypot
+  // one phys::velocity per node serves both the entropy (physics.hpp:47-62) and
+  // compute_dt (timeloop.hpp:58-71): the same call in the reference, same bits
   double u, v;
   velocity(h, hu, hv, P.h_des, u, v);
+  const double kin = 0.5 * h * (u * u + v * v);
+  const double en = kin + 0.5 * P.g * h * h + P.g * h * b;
+  // total_mass: sum += h * J * w_i * w_j; total_entropy: e * J * w_i * w_j
+  acc.mass += h * jac * wi * wj;
+  acc.ent += en * jac * wi * wj;
+  const unsigned long long kh = order_key(h);
+  acc.kmin = kh < acc.kmin ? kh : acc.kmin;
+  // compute_dt per node, lengths precomputed with glibc hypot
   const double c = sqrt(P.g * smax(h, 0.0));
   double dt = __longlong_as_double(0x7ff0000000000000ll);
   const double lx = fabs(u) + c, ly = fabs(v) + c;
