@@ -590,35 +590,6 @@ __global__ void k_limit(Mesh M, Phys P, State S, Flags* F) {
   atomicMin(&F->min_h_key, order_key(mn));
 }
 
-// compute_dt (timeloop.hpp:53-75): per-node candidates, min via ordered keys;
-// the lengths 2J/hypot(.) come precomputed by the host with std::hypot.
-__global__ void k_dt(Mesh M, Phys P, CState S, Flags* F) {
-  unsigned long long kdt = ~0ull, klen = ~0ull;
-  const long long nn = (long long)M.n_owned * M.np;
-  const double order = 2.0 * M.degree + 1.0;
-  for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < nn;
-       n += (long long)gridDim.x * blockDim.x) {
-    double u, v;
-    velocity(S.h[n], S.hu[n], S.hv[n], P.h_des, u, v);
-    const double c = sqrt(P.g * smax(S.h[n], 0.0));
-    const double lxi = M.len_xi[n], leta = M.len_eta[n];
-    double dt = __longlong_as_double(0x7ff0000000000000ll);
-    const double lx = fabs(u) + c, ly = fabs(v) + c;
-    if (lx > 1e-14) dt = smin(dt, lxi / (order * lx));
-    if (ly > 1e-14) dt = smin(dt, leta / (order * ly));
-    const unsigned long long a = order_key(dt), b = order_key(smin(lxi, leta));
-    kdt = a < kdt ? a : kdt;
-    klen = b < klen ? b : klen;
-  }
-  // min is exact (order-independent): one atomic per block
-  kdt = block_min_key(kdt);
-  klen = block_min_key(klen);
-  if (threadIdx.x == 0) {
-    atomicMin(&F->dt_key, kdt);
-    atomicMin(&F->minlen_key, klen);
-  }
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -651,11 +622,5 @@ int launch_exact_limit(const Mesh& M, const Phys& P, State S, Flags* F, cudaStre
   return 1;
 }
 
-int launch_exact_dt(const Mesh& M, const Phys& P, CState S, Flags* F, cudaStream_t st) {
-  const long long nn = (long long)M.n_owned * M.np;
-  const long long blocks = (nn + 255) / 256;
-  k_dt<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, st>>>(M, P, S, F);
-  return 1;
-}
 
 }  // namespace swdg_dev

@@ -47,6 +47,56 @@ __device__ __forceinline__ void velocity(double h, double hu, double hv, double 
   }
 }
 
+// Fast-mode arithmetic (the step reductions of SWDG_MODE_FAST need not be
+// bitwise): a reciprocal from the MUFU seed and two Newton steps in explicit
+// round-to-nearest FMAs (within an ulp), and the square root from the
+// reciprocal square root, instead of the IEEE division / square-root sequences
+// this --fmad=false translation unit otherwise emits.
+__device__ __forceinline__ double rcp_fast(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = __fma_rn(-x, r, 1.0);
+  r = __fma_rn(r, e, r);
+  e = __fma_rn(-x, r, 1.0);
+  return __fma_rn(r, e, r);
+}
+
+__device__ __forceinline__ double sqrt_fast(double x) {  // x >= 0
+  if (!(x > 0.0)) return 0.0;
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  // two Newton steps on 1/sqrt, then s = x r with one correction
+  double h = __dmul_rn(0.5, x);
+  r = __dmul_rn(r, __fma_rn(-h, __dmul_rn(r, r), 1.5));
+  r = __dmul_rn(r, __fma_rn(-h, __dmul_rn(r, r), 1.5));
+  const double s = __dmul_rn(x, r);
+  return __fma_rn(__fma_rn(-s, s, x), __dmul_rn(0.5, r), s);
+}
+
+template <bool FAST>
+__device__ __forceinline__ void vel_t(double h, double hu, double hv, double h_des, double& u,
+                                      double& v) {
+  if constexpr (FAST) {
+    const double r = h >= h_des ? rcp_fast(h) : 0.0;
+    u = __dmul_rn(hu, r);
+    v = __dmul_rn(hv, r);
+  } else {
+    velocity(h, hu, hv, h_des, u, v);
+  }
+}
+
+template <bool FAST>
+__device__ __forceinline__ double div_t(double a, double b) {
+  if constexpr (FAST) return __dmul_rn(a, rcp_fast(b));
+  else return a / b;
+}
+
+template <bool FAST>
+__device__ __forceinline__ double sqrt_t(double x) {
+  if constexpr (FAST) return sqrt_fast(x);
+  else return sqrt(x);
+}
+
 // phys::entropy (physics.hpp:47-62): h(u^2+v^2)/2 + g h^2/2 + g h b
 __device__ __forceinline__ double entropy(double h, double hu, double hv, double b,
                                           const Phys& P) {
@@ -85,6 +135,7 @@ struct NodeAcc {
   unsigned long long kmin = ~0ull, kdt = ~0ull, klen = ~0ull;
 };
 
+template <bool FAST>
 __device__ __forceinline__ void node_terms(const Mesh& M, const Phys& P, double order, int n,
                                            double h, double hu, double hv, double jac,
                                            double b, double lxi, double leta, NodeAcc& acc) {
@@ -93,7 +144,7 @@ __device__ __forceinline__ void node_terms(const Mesh& M, const Phys& P, double 
   // one phys::velocity per node serves both the entropy (physics.hpp:47-62) and
   // compute_dt (timeloop.hpp:58-71): the same call in the reference, same bits
   double u, v;
-  velocity(h, hu, hv, P.h_des, u, v);
+  vel_t<FAST>(h, hu, hv, P.h_des, u, v);
   const double kin = 0.5 * h * (u * u + v * v);
   const double en = kin + 0.5 * P.g * h * h + P.g * h * b;
   // total_mass: sum += h * J * w_i * w_j; total_entropy: e * J * w_i * w_j
@@ -102,11 +153,11 @@ __device__ __forceinline__ void node_terms(const Mesh& M, const Phys& P, double 
   const unsigned long long kh = order_key(h);
   acc.kmin = kh < acc.kmin ? kh : acc.kmin;
   // compute_dt per node, lengths precomputed with glibc hypot
-  const double c = sqrt(P.g * smax(h, 0.0));
+  const double c = sqrt_t<FAST>(P.g * smax(h, 0.0));
   double dt = __longlong_as_double(0x7ff0000000000000ll);
   const double lx = fabs(u) + c, ly = fabs(v) + c;
-  if (lx > 1e-14) dt = smin(dt, lxi / (order * lx));
-  if (ly > 1e-14) dt = smin(dt, leta / (order * ly));
+  if (lx > 1e-14) dt = smin(dt, div_t<FAST>(lxi, order * lx));
+  if (ly > 1e-14) dt = smin(dt, div_t<FAST>(leta, order * ly));
   const unsigned long long a = order_key(dt), l = order_key(smin(lxi, leta));
   acc.kdt = a < acc.kdt ? a : acc.kdt;
   acc.klen = l < acc.klen ? l : acc.klen;
@@ -188,6 +239,7 @@ __global__ void k_limiter_entropy(Mesh M, Phys P, StageArgs A, const Flags* F,
 __device__ __forceinline__ double posdt_bound(const Mesh& M, const Phys& P, const CState& S,
                                                long long idx);
 
+template <bool FAST>
 __device__ __forceinline__ double posdt_bound(const Mesh& M, const Phys& P, const CState& S,
                                                long long idx) {
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
@@ -215,18 +267,18 @@ __device__ __forceinline__ double posdt_bound(const Mesh& M, const Phys& P, cons
     hvp = S.hv[nb];
   }
   double um, vm, up, vp;
-  velocity(hm, hum, hvm, P.h_des, um, vm);
-  velocity(hp, hup, hvp, P.h_des, up, vp);
+  vel_t<FAST>(hm, hum, hvm, P.h_des, um, vm);
+  vel_t<FAST>(hp, hup, hvp, P.h_des, up, vp);
   const double unm = nx * um + ny * vm, unp = nx * up + ny * vp;
   const double uavg = 0.5 * (unm + unp);
-  const double cavg = 0.5 * (sqrt(P.g * smax(hm, 0.0)) + sqrt(P.g * smax(hp, 0.0)));
+  const double cavg = 0.5 * (sqrt_t<FAST>(P.g * smax(hm, 0.0)) + sqrt_t<FAST>(P.g * smax(hp, 0.0)));
   const double a = fabs(uavg + cavg) + fabs(uavg - cavg);
   const double bb = fabs(uavg + cavg) - fabs(uavg - cavg);
   const double den1 = a + 2.0 * uavg;
-  double bound = den1 > 1e-300 ? M.w0 * a_scale / den1 : inf;
+  double bound = den1 > 1e-300 ? div_t<FAST>(M.w0 * a_scale, den1) : inf;
   const double jump = unp - unm;
   if (hm > 0.0 && bb * jump < 0.0)
-    bound = smin(bound, fabs(M.w0 * a_scale * P.g * hm / (cavg * bb * jump)));
+    bound = smin(bound, fabs(div_t<FAST>(M.w0 * a_scale * P.g * hm, cavg * bb * jump)));
   return bound;
 }
 
@@ -236,7 +288,7 @@ __device__ __forceinline__ double posdt_bound(const Mesh& M, const Phys& P, cons
 // the tile's face-node positivity bounds, whose own-side state was just read
 // (L1/L2 hits) and whose neighbour traces are mostly L2 hits (the tiles of all
 // CTAs advance together).  Partial sums are per CTA in a fixed order.
-template <int T>
+template <int T, bool FAST>
 __global__ void __launch_bounds__(kSumThreads) k_step_diag(Mesh M, Phys P, CState S,
                                                            double* partial, Flags* F) {
   const int np = M.np, n1 = M.n1;
@@ -249,14 +301,14 @@ __global__ void __launch_bounds__(kSumThreads) k_step_diag(Mesh M, Phys P, CStat
     const int n0 = e0 * np, nn = ne * np;
     for (int r = threadIdx.x; r < nn; r += blockDim.x) {
       const int n = n0 + r;
-      node_terms(M, P, order, n, __ldg(S.h + n), __ldg(S.hu + n), __ldg(S.hv + n),
+      node_terms<FAST>(M, P, order, n, __ldg(S.h + n), __ldg(S.hu + n), __ldg(S.hv + n),
                  __ldg(M.jac + n), __ldg(M.b + n), __ldg(M.len_xi + n), __ldg(M.len_eta + n),
                  acc);
     }
     const long long f0 = (long long)e0 * 4 * n1;
     const int nf = ne * 4 * n1;
     for (int r = threadIdx.x; r < nf; r += blockDim.x) {
-      const unsigned long long k = order_key(posdt_bound(M, P, S, f0 + r));
+      const unsigned long long k = order_key(posdt_bound<FAST>(M, P, S, f0 + r));
       kpos = k < kpos ? k : kpos;
     }
   }
@@ -274,6 +326,36 @@ __global__ void __launch_bounds__(kSumThreads) k_step_diag(Mesh M, Phys P, CStat
     if (kdt != ~0ull) atomicMin(&F->dt_key, kdt);
     if (klen != ~0ull) atomicMin(&F->minlen_key, klen);
     if (kp != ~0ull) atomicMin(&F->posdt_key, kp);
+  }
+}
+
+// compute_dt's two reductions (timeloop.hpp:57-74): the CFL candidate minimum and
+// the all-dry fallback length, with the same per-node arithmetic as the step
+// reductions (so the driver's first dt and the step reports' next dt agree
+// bitwise in both modes)
+template <bool FAST>
+__global__ void __launch_bounds__(kSumThreads) k_cfl_dt(Mesh M, Phys P, CState S, Flags* F) {
+  const int nn = M.n_owned * M.np;
+  const double order = 2.0 * M.degree + 1.0;
+  unsigned long long kdt = ~0ull, klen = ~0ull;
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < nn; n += gridDim.x * blockDim.x) {
+    const double h = __ldg(S.h + n), lxi = __ldg(M.len_xi + n), leta = __ldg(M.len_eta + n);
+    double u, v;
+    vel_t<FAST>(h, __ldg(S.hu + n), __ldg(S.hv + n), P.h_des, u, v);
+    const double c = sqrt_t<FAST>(P.g * smax(h, 0.0));
+    double dt = __longlong_as_double(0x7ff0000000000000ll);
+    const double lx = fabs(u) + c, ly = fabs(v) + c;
+    if (lx > 1e-14) dt = smin(dt, div_t<FAST>(lxi, order * lx));
+    if (ly > 1e-14) dt = smin(dt, div_t<FAST>(leta, order * ly));
+    const unsigned long long a = order_key(dt), l = order_key(smin(lxi, leta));
+    kdt = a < kdt ? a : kdt;
+    klen = l < klen ? l : klen;
+  }
+  kdt = block_min_key(kdt);
+  klen = block_min_key(klen);
+  if (threadIdx.x == 0) {
+    if (kdt != ~0ull) atomicMin(&F->dt_key, kdt);
+    if (klen != ~0ull) atomicMin(&F->minlen_key, klen);
   }
 }
 
@@ -320,18 +402,32 @@ int launch_diagnostics(const Mesh& M, const Phys& P, CState S, double* partial, 
                        Flags* F, cudaStream_t st, bool serial) {
   // tiles of ~1024 nodes (4 per thread): T = 1024 / (N+1)^2 elements
   const int T = M.np <= 16 ? 64 : M.np <= 64 ? 16 : M.np <= 128 ? 8 : 4;
+  // fast mode: fast reciprocals / square roots (the exact mode keeps the IEEE
+  // operations, bitwise the reference)
+#define SWDG_DIAG(t)                                                                 \
+  case t:                                                                            \
+    if (serial) k_step_diag<t, false><<<kSumBlocks, kSumThreads, 0, st>>>(M, P, S, partial, F); \
+    else k_step_diag<t, true><<<kSumBlocks, kSumThreads, 0, st>>>(M, P, S, partial, F);        \
+    break;
   switch (T) {
-    case 64: k_step_diag<64><<<kSumBlocks, kSumThreads, 0, st>>>(M, P, S, partial, F); break;
-    case 16: k_step_diag<16><<<kSumBlocks, kSumThreads, 0, st>>>(M, P, S, partial, F); break;
-    case 8: k_step_diag<8><<<kSumBlocks, kSumThreads, 0, st>>>(M, P, S, partial, F); break;
-    default: k_step_diag<4><<<kSumBlocks, kSumThreads, 0, st>>>(M, P, S, partial, F); break;
+    SWDG_DIAG(64)
+    SWDG_DIAG(16)
+    SWDG_DIAG(8)
+    default: SWDG_DIAG(4)
   }
+#undef SWDG_DIAG
   k_step_final<<<1, 1024, 0, st>>>(partial, kSumBlocks, out2);
   if (serial) {  // exact mode: the reference's serial summation order
     k_serial_sums<<<1, 32, 0, st>>>(M, P, S, out2);
     return 3;
   }
   return 2;
+}
+
+int launch_cfl_dt(const Mesh& M, const Phys& P, CState S, Flags* F, cudaStream_t st, bool fast) {
+  if (fast) k_cfl_dt<true><<<kSumBlocks, kSumThreads, 0, st>>>(M, P, S, F);
+  else k_cfl_dt<false><<<kSumBlocks, kSumThreads, 0, st>>>(M, P, S, F);
+  return 1;
 }
 
 int launch_limiter_entropy(const Mesh& M, const Phys& P, const StageArgs& A, const Flags* F,

@@ -920,8 +920,8 @@ int swdg_gpu_compute_dt(swdg_gpu* c, double cfl, double* dt) {
   return guarded(c, [&] {
     if (!(cfl > 0.0) || cfl > 1.0) throw InputError{"compute_dt: cfl must be in (0, 1]"};
     reset_flags(c);
-    c->launches += launched(launch_exact_dt(c->M, c->phys, cs(c->W), c->flags + kDiagFlags,
-                                            c->stream), "launch_exact_dt");
+    c->launches += launched(launch_cfl_dt(c->M, c->phys, cs(c->W), c->flags + kDiagFlags,
+                                          c->stream, c->fast), "launch_cfl_dt");
     read_flags(c);
     *dt = cfl_dt(c, cfl);
     return SWDG_OK;
@@ -1354,7 +1354,8 @@ int swdg_gpu_halo_unpack(swdg_gpu* c, int what, int k, const double* recv_buf) {
 int swdg_gpu_dt_candidates(swdg_gpu* c, double* dt_min, double* min_len) {
   return guarded(c, [&] {
     reset_flags(c);
-    c->launches += launched(launch_exact_dt(c->M, c->phys, cs(c->W), c->flags, c->stream), "launch_exact_dt");
+    c->launches += launched(launch_cfl_dt(c->M, c->phys, cs(c->W), c->flags, c->stream, c->fast),
+                            "launch_cfl_dt");
     read_flags(c);
     *dt_min = key_value(c->flags_h[0].dt_key);
     *min_len = key_value(c->flags_h[0].minlen_key);

@@ -35,7 +35,6 @@ int launch_exact_grad(const Mesh& M, const Phys& P, CState S, const double* eps,
                       double* fvv, double* gvu, double* gvv, cudaStream_t st);
 int launch_exact_rhs_stage(const Mesh& M, const Phys& P, const StageArgs& A, cudaStream_t st);
 int launch_exact_limit(const Mesh& M, const Phys& P, State S, Flags* F, cudaStream_t st);
-int launch_exact_dt(const Mesh& M, const Phys& P, CState S, Flags* F, cudaStream_t st);
 
 // fast mode: dispatch (kernels_common.cu) over the three degree-range objects of
 // kernels_fast.cu (SWDG_PART 0/1/2: N+1 in [2,7], [8,11], [12,16])
@@ -64,6 +63,8 @@ SWDG_FAST_PART_DECL(p2)
 // per-step reductions (kernels_step.cu, --fmad=false): mass/entropy partials
 // (step_sum_partials() pairs) for launch_diagnostics
 int step_sum_partials();
+// compute_dt's CFL candidates (fast: the fast arithmetic of the fast step reductions)
+int launch_cfl_dt(const Mesh& M, const Phys& P, CState S, Flags* F, cudaStream_t st, bool fast);
 // limited_entropy_check of the elements a stage limited (A.rhs holds its dW/dt)
 int launch_limiter_entropy(const Mesh& M, const Phys& P, const StageArgs& A, const Flags* F,
                            unsigned long long* key, cudaStream_t st);
