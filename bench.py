@@ -184,7 +184,7 @@ def memcpy_d2d_gbs(nbytes: int = 4 << 30, reps: int = 10) -> float:
 
 
 def measure_gpu(N: int, steps: int, warmup: int, viscous: bool, rank: int, world: int,
-                e2e_steps: int = 20):
+                e2e_steps: int = 50):
     import numpy as np
     import torch
     from paper_1804_02221_b200 import swdg
