@@ -23,6 +23,7 @@
 // bitwise repeatable.
 #include <cuda_runtime.h>
 
+#include "fast_math.cuh"
 #include "swdg_device.cuh"
 #include "swdg_launch.h"
 
@@ -48,38 +49,15 @@ __device__ __forceinline__ void velocity(double h, double hu, double hv, double 
 }
 
 // Fast-mode arithmetic (the step reductions of SWDG_MODE_FAST need not be
-// bitwise): a reciprocal from the MUFU seed and two Newton steps in explicit
-// round-to-nearest FMAs (within an ulp), and the square root from the
-// reciprocal square root, instead of the IEEE division / square-root sequences
-// this --fmad=false translation unit otherwise emits.
-__device__ __forceinline__ double rcp_fast(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = __fma_rn(-x, r, 1.0);
-  r = __fma_rn(r, e, r);
-  e = __fma_rn(-x, r, 1.0);
-  return __fma_rn(r, e, r);
-}
-
-__device__ __forceinline__ double sqrt_fast(double x) {  // x >= 0
-  if (!(x > 0.0)) return 0.0;
-  double r;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  // two Newton steps on 1/sqrt, then s = x r with one correction
-  double h = __dmul_rn(0.5, x);
-  r = __dmul_rn(r, __fma_rn(-h, __dmul_rn(r, r), 1.5));
-  r = __dmul_rn(r, __fma_rn(-h, __dmul_rn(r, r), 1.5));
-  const double s = __dmul_rn(x, r);
-  return __fma_rn(__fma_rn(-s, s, x), __dmul_rn(0.5, r), s);
-}
-
+// bitwise): fast_math.cuh's reciprocal and square root (MUFU seeds and Newton
+// steps in explicit round-to-nearest FMAs, within an ulp) and the stage
+// kernels' velocity, instead of the IEEE division / square-root sequences this
+// --fmad=false translation unit otherwise emits.
 template <bool FAST>
 __device__ __forceinline__ void vel_t(double h, double hu, double hv, double h_des, double& u,
                                       double& v) {
   if constexpr (FAST) {
-    const double r = h >= h_des ? rcp_fast(h) : 0.0;
-    u = __dmul_rn(hu, r);
-    v = __dmul_rn(hv, r);
+    vel(h, hu, hv, h_des, u, v);
   } else {
     velocity(h, hu, hv, h_des, u, v);
   }
@@ -87,13 +65,13 @@ __device__ __forceinline__ void vel_t(double h, double hu, double hv, double h_d
 
 template <bool FAST>
 __device__ __forceinline__ double div_t(double a, double b) {
-  if constexpr (FAST) return __dmul_rn(a, rcp_fast(b));
+  if constexpr (FAST) return __dmul_rn(a, frcp(b));
   else return a / b;
 }
 
 template <bool FAST>
 __device__ __forceinline__ double sqrt_t(double x) {
-  if constexpr (FAST) return sqrt_fast(x);
+  if constexpr (FAST) return fsqrt0(x);
   else return sqrt(x);
 }
 
