@@ -194,10 +194,7 @@ struct HL {
   static constexpr int STT = ACCX + (NT ? 3 * GPAD : 0);        // [3][GPAD] state
   static constexpr int NRED = STT + (NT ? 3 * GPAD : 0);        // [E][PMAX][5]
   static constexpr int ELM = NRED + (NT ? E * PMAX * 5 : 0);    // [E][4]
-  // stage-3 step reductions (the DIAG instantiation, inviscid): per xi-line
-  // thread (part, element, line) its nodes' (mass, entropy) of the final state
-  static constexpr int DSL = ELM + (NT ? E * 4 : 0);            // [2][E][N1][2]
-  static constexpr int TOTAL = DSL + (V ? 0 : 2 * E * N1 * 2);
+  static constexpr int TOTAL = ELM + (NT ? E * 4 : 0);
   static constexpr size_t bytes = TOTAL * sizeof(double);
 };
 
@@ -512,13 +509,7 @@ __host__ __device__ constexpr bool hl_blockmin(int n1, bool visc) {
   return SWDG_HL_BLOCKMIN >= 0 ? SWDG_HL_BLOCKMIN != 0 : visc;
 }
 
-// DIAG (inviscid, stage 3 of a step whose reductions are requested): the write-out
-// also accumulates the per-element mass and entropy of the final state
-// (field.hpp:39-61) into A.diag_elem and the compute_dt candidates
-// (timeloop.hpp:58-71) into A.diag_flags, with fast_math.cuh's arithmetic (the
-// same bits as the fast k_cfl_dt); kernels_step.cu then only sums the element
-// pairs and runs the face-only positivity pass.
-template <int N1, bool FORCE, bool VISC, bool DIAG = false>
+template <int N1, bool FORCE, bool VISC>
 __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC))
     k_stage_hl(Mesh M, Phys Ph, StageArgs A, Flags* F) {
   using P = HL<N1, VISC>;
@@ -553,27 +544,6 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
 
   __shared__ int s_next;  // the next group, claimed by thread 0
   unsigned long long kmin = ~0ull;  // min height key of this thread's elements
-  // DIAG: CFL candidate keys of this thread's nodes; the previous group whose
-  // element (mass, entropy) slots await their fixed-order sum
-  unsigned long long kdt = ~0ull, klen = ~0ull;
-  int diag_e0 = -1, diag_ne = 0;
-  const double order = 2.0 * M.degree + 1.0;
-  auto diag_flush = [&]() {  // after a barrier: one thread per element
-    if constexpr (DIAG) {
-      if (diag_e0 >= 0 && tid < diag_ne) {
-        const double* d = sm + P::DSL;
-        double ms = 0.0, en = 0.0;
-        for (int pp = 0; pp < 2; ++pp)
-          for (int l = 0; l < N1; ++l) {
-            const double* q = d + (((pp * P::E + tid) * N1) + l) * 2;
-            ms += q[0];
-            en += q[1];
-          }
-        A.diag_elem[2 * (diag_e0 + tid)] = ms;
-        A.diag_elem[2 * (diag_e0 + tid) + 1] = en;
-      }
-    }
-  };
   // With HL::XI_SPLIT the group loop is instantiated per line direction (xi is
   // warp-uniform): the metric selection (y_eta, x_eta) / -(y_xi, x_xi), the padded
   // addressing and the xi-only node phase become compile-time.  Every
@@ -588,7 +558,6 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
     const int e = e0 + el;
     cp_async_wait_all();
     __syncthreads();  // line(g) and connectivity(g) resident for every thread
-    diag_flush();     // the previous group's element sums (slots rewritten later)
     if (tid == 0) {
       fence_proxy_async();
       hl_issue_node<N1, VISC>(sm, M, A, grp, bar_node);
@@ -982,7 +951,6 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
       }
       if (lim && !Ph.limiter && mmin < 0.0 && lead) atomicExch(&F->abort, 1);
       if (lim) {
-        double dms = 0.0, den = 0.0;  // DIAG: this thread's nodes' mass, entropy
 #pragma unroll
         for (int s = 0; s < S; ++s) {
           if (s >= nk) continue;
@@ -1000,33 +968,6 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
           A.out.h[n] = sh;
           A.out.hu[n] = shu;
           A.out.hv[n] = shv;
-          if constexpr (DIAG) {
-            // total_mass / total_entropy terms (field.hpp:39-61) and the CFL
-            // candidates (timeloop.hpp:58-71) of the final state
-            const double* Nd = sm + P::NODE + (int)(((long long)e0 * NP) & 1) + el * NP;
-            const double wq = O::w(k0 + s) * O::w(li) * Nd[P::N_JAC * P::GNP + (k0 + s) * N1 + li];
-            double u, v;
-            vel(sh, shu, shv, h_des, u, v);
-            const double bn = __ldg(M.b + n);
-            const double kin = 0.5 * sh * (u * u + v * v);
-            const double ent = kin + 0.5 * g * sh * sh + g * sh * bn;
-            dms += wq * sh;
-            den += wq * ent;
-            const double lxi = __ldg(M.len_xi + n), leta = __ldg(M.len_eta + n);
-            const double c = fsqrt0(g * smax(sh, 0.0));
-            double dtc = __longlong_as_double(0x7ff0000000000000ll);
-            const double lx = fabs(u) + c, ly = fabs(v) + c;
-            if (lx > 1e-14) dtc = smin(dtc, __dmul_rn(lxi, frcp(__dmul_rn(order, lx))));
-            if (ly > 1e-14) dtc = smin(dtc, __dmul_rn(leta, frcp(__dmul_rn(order, ly))));
-            const unsigned long long a = order_key(dtc), l = order_key(smin(lxi, leta));
-            kdt = a < kdt ? a : kdt;
-            klen = l < klen ? l : klen;
-          }
-        }
-        if constexpr (DIAG) {
-          double* q = sm + P::DSL + (((part * P::E + el) * N1) + li) * 2;
-          q[0] = dms;
-          q[1] = den;
         }
         if (lead) {
           // the limited heights are a monotone map of the unlimited ones: the
@@ -1042,10 +983,6 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
         }
       }
     }
-    if constexpr (DIAG) {
-      diag_e0 = e0;
-      diag_ne = ne;
-    }
   }
   };
   if constexpr (P::XI_SPLIT) {
@@ -1060,16 +997,6 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
   if (hl_blockmin(N1, VISC)) {  // one atomic per CTA for the whole launch
     const unsigned long long bmin = block_min_key(kmin);
     if (tid == 0 && bmin != ~0ull) atomicMin(&F->min_h_key, bmin);
-  }
-  if constexpr (DIAG) {
-    __syncthreads();  // the last group's slots
-    diag_flush();
-    const unsigned long long bd = block_min_key(kdt);
-    const unsigned long long bl = block_min_key(klen);
-    if (tid == 0) {
-      if (bd != ~0ull) atomicMin(&A.diag_flags->dt_key, bd);
-      if (bl != ~0ull) atomicMin(&A.diag_flags->minlen_key, bl);
-    }
   }
 }
 
@@ -1790,19 +1717,10 @@ template <int N1, bool FORCE, bool VISC>
 static void launch_half(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
                         cudaStream_t st) {
   using PL = HL<N1, VISC>;
-  const int groups = (M.n_owned - M.e_lo + PL::E - 1) / PL::E;
-  if constexpr (!FORCE && !VISC) {
-    if (A.diag_elem) {  // stage 3 with the step reductions fused
-      static int cache_d[kMaxDevices] = {};
-      auto kd = k_stage_hl<N1, false, false, true>;
-      const int gd = grid_for(kd, PL::THREADS, PL::bytes, groups, cache_d, A.reserve_sms);
-      kd<<<gd, PL::THREADS, PL::bytes, st>>>(M, P, A, F);
-      return;
-    }
-  }
   static int cache[kMaxDevices] = {};
   auto kern = k_stage_hl<N1, FORCE, VISC>;
-  const int grid = grid_for(kern, PL::THREADS, PL::bytes, groups, cache, A.reserve_sms);
+  const int grid = grid_for(kern, PL::THREADS, PL::bytes, (M.n_owned - M.e_lo + PL::E - 1) / PL::E,
+                            cache, A.reserve_sms);
   kern<<<grid, PL::THREADS, PL::bytes, st>>>(M, P, A, F);
 }
 

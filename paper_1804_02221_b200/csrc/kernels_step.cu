@@ -307,36 +307,6 @@ __global__ void __launch_bounds__(kSumThreads) k_step_diag(Mesh M, Phys P, CStat
   }
 }
 
-// The half of the step reductions the fused stage-3 kernel leaves: the per-element
-// (mass, entropy) pairs summed over a static chunking (fixed order), and the
-// positivity bounds over the face nodes (fast arithmetic: fused only in fast mode)
-__global__ void __launch_bounds__(kSumThreads) k_diag_finish(Mesh M, Phys P, CState S,
-                                                             const double* elem, double* partial,
-                                                             Flags* F) {
-  double ms = 0.0, en = 0.0;
-  const int K = M.n_owned;
-  const int chunk = (K + gridDim.x - 1) / gridDim.x;
-  const int lo = blockIdx.x * chunk, hi = min(K, lo + chunk);
-  for (int e = lo + threadIdx.x; e < hi; e += blockDim.x) {
-    ms += elem[2 * e];
-    en += elem[2 * e + 1];
-  }
-  block_sum2(ms, en);
-  if (threadIdx.x == 0) {
-    partial[2 * blockIdx.x] = ms;
-    partial[2 * blockIdx.x + 1] = en;
-  }
-  unsigned long long kpos = ~0ull;
-  const long long nf = (long long)K * 4 * M.n1;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < nf;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const unsigned long long k = order_key(posdt_bound<true>(M, P, S, idx));
-    kpos = k < kpos ? k : kpos;
-  }
-  kpos = block_min_key(kpos);
-  if (threadIdx.x == 0 && kpos != ~0ull) atomicMin(&F->posdt_key, kpos);
-}
-
 // compute_dt's two reductions (timeloop.hpp:57-74): the CFL candidate minimum and
 // the all-dry fallback length, with the same per-node arithmetic as the step
 // reductions (so the driver's first dt and the step reports' next dt agree
@@ -429,13 +399,6 @@ int launch_diagnostics(const Mesh& M, const Phys& P, CState S, double* partial, 
     k_serial_sums<<<1, 32, 0, st>>>(M, P, S, out2);
     return 3;
   }
-  return 2;
-}
-
-int launch_diag_finish(const Mesh& M, const Phys& P, CState S, const double* diag_elem,
-                       double* partial, double* out2, Flags* F, cudaStream_t st) {
-  k_diag_finish<<<kSumBlocks, kSumThreads, 0, st>>>(M, P, S, diag_elem, partial, F);
-  k_step_final<<<1, 1024, 0, st>>>(partial, kSumBlocks, out2);
   return 2;
 }
 

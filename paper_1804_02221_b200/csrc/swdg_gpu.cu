@@ -89,12 +89,7 @@ struct swdg_gpu {
   double *partial = nullptr, *sums = nullptr;
   int int_lo = 0, int_hi = 0;   // interior element range (halo overlap), empty by default
   int reserve_sms = 0;          // SMs the next stage launch leaves free
-  // the step reductions fused into stage 3 (fast inviscid half-line kernel):
-  // per-element (mass, entropy) pairs, [K][2]; fuse_stage3 set for that launch
-  double* diag_elem = nullptr;
-  bool fuse_stage3 = false;
   bool no_graphs = std::getenv("SWDG_NO_GRAPHS") != nullptr;  // A/B: eager launches
-  bool no_fuse = std::getenv("SWDG_NO_FUSED_DIAG") != nullptr;  // A/B: separate reductions
   int* gctr = nullptr;          // device group counter of the persistent stage kernels
   // device report: Flags[4] (one per stage + one for the step reductions) and the
   // mass/entropy sums, contiguous so one copy (one host sync) reads a whole step
@@ -325,10 +320,6 @@ void stage_main(swdg_gpu* c, CState in, double* const* out, int k, double t, dou
   }
   const Mesh& M = range ? *range : c->M;
   a.reserve_sms = c->reserve_sms;
-  if (c->fuse_stage3 && k == 2 && out && c->fast) {
-    a.diag_elem = c->diag_elem;
-    a.diag_flags = c->flags + kDiagFlags;
-  }
   if (out) fence_snapshot(c, out);
   if (c->fast) {
     ck(cudaMemsetAsync(c->gctr, 0, sizeof(int), c->stream), "group counter");
@@ -960,30 +951,6 @@ static int fold_flags(swdg_gpu* c, swdg_step_info& r, int& code) {
   return 3;
 }
 
-// The step reductions of a step's stage-3 output (buffer A): fused into the stage-3
-// kernel where the fast kernels support it (then only the element-pair sum and the
-// face-only positivity pass remain), else the full pass.  `fused` says which way
-// stage 3 was launched.
-void queue_step_reductions(swdg_gpu* c, bool fused) {
-  if (fused)
-    c->launches += launched(launch_diag_finish(c->M, c->phys, cs(c->A), c->diag_elem, c->partial,
-                                               c->sums, c->flags + kDiagFlags, c->stream),
-                            "launch_diag_finish");
-  else
-    c->launches += launched(launch_diagnostics(c->M, c->phys, cs(c->A), c->partial, c->sums,
-                                               c->flags + kDiagFlags, c->stream, !c->fast),
-                            "launch_diagnostics");
-}
-
-// fast mode: fuse the step reductions into stage 3 when the kernel supports it
-bool begin_fused_step(swdg_gpu* c, bool reductions) {
-  const bool f = reductions && c->fast && !c->no_fuse &&
-                 fast_stage_fuses_diag(c->M, c->params.visc_enabled != 0, c->forcing != nullptr);
-  if (f && !c->diag_elem) c->diag_elem = c->dalloc<double>(2 * (size_t)c->M.K);
-  c->fuse_stage3 = f;
-  return f;
-}
-
 // One SSPRK3 step of the device state (try_step timeloop.hpp:156-170).  With
 // `diag`, the step reductions of the stage-3 output (the next state if the step
 // is accepted) are queued behind the stages, so the device-resident driver reads
@@ -999,16 +966,15 @@ static int try_step_impl(swdg_gpu* c, double t, double dt, swdg_step_info& r, bo
   reset_flags(c);
   if (c->fast && !c->forcing) {
     // device-resident: three stages back to back, one flag read per step
-    const bool fused = begin_fused_step(c, diag);
     for (int k = 0; k < 3; ++k) {
       stage(c, in, outs[k], k, t, dt, viscous, nullptr, c->flags + k);
       in = cs(outs[k]);
     }
-    c->fuse_stage3 = false;
-    if (diag) queue_step_reductions(c, fused);
+    if (diag)
+      c->launches += launched(launch_diagnostics(c->M, c->phys, cs(c->A), c->partial, c->sums,
+                                                 c->flags + kDiagFlags, c->stream, !c->fast),
+                              "launch_diagnostics");
     read_flags(c);
-    // the minimum height of the new state is stage 3's minimum after limiting
-    if (fused) c->flags_h[kDiagFlags].min_h_key = c->flags_h[2].min_h_key;
     r.accepted = fold_flags(c, r, code) == 3 && code == SWDG_OK;
   } else {
     for (int k = 0; k < 3; ++k) {
@@ -1081,15 +1047,16 @@ int swdg_gpu_run_steps_ex(swdg_gpu* c, int nsteps, double t, double dt, int flag
     double* const* outs[3] = {c->A, c->B, c->A};
     auto one_step = [&](double ts) {
       CState in = cs(c->W);
-      const bool fused = begin_fused_step(c, reductions);
       for (int k = 0; k < 3; ++k) {
         stage(c, in, outs[k], k, ts, dt, viscous, nullptr, c->flags + k);
         in = cs(outs[k]);
       }
-      c->fuse_stage3 = false;
       // the per-step StepDiagnostics reductions and the next CFL candidate of the
       // new state, as the driver needs them every step (driver.hpp:92, 117-127)
-      if (reductions) queue_step_reductions(c, fused);
+      if (reductions)
+        c->launches += launched(launch_diagnostics(c->M, c->phys, cs(c->A), c->partial, c->sums,
+                                                   c->flags + kDiagFlags, c->stream, false),
+                                "launch_diagnostics");
       for (int k = 0; k < 3; ++k) std::swap(c->W[k], c->A[k]);
     };
     int s0 = 0;

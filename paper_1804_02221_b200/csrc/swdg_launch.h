@@ -28,23 +28,7 @@ struct StageArgs {
   // SMs the persistent stage kernels leave free (0: use all): a partition's
   // interior launch runs while NCCL moves the halo, whose kernels need SMs
   int reserve_sms;
-  // stage 3 with the step reductions fused (inviscid half-line kernel): per
-  // element (mass, entropy) of the output, [K][2], and the CFL candidates into
-  // diag_flags; nullptr: not fused
-  double* diag_elem;
-  Flags* diag_flags;
 };
-
-// whether launch_fast_stage fuses the step reductions at this configuration:
-// the inviscid half-line kernel (N+1 >= 5) except its transposed-node-phase
-// degree (N+1 = 9, HL::NT), without forcing
-inline bool fast_stage_fuses_diag(const Mesh& M, bool viscous, bool forcing) {
-  return M.n1 >= 5 && M.n1 != 9 && !viscous && !forcing;
-}
-// the rest of the fused step reductions: the element pairs summed in a fixed
-// order (sums into out2) and the face-only positivity pass into F
-int launch_diag_finish(const Mesh& M, const Phys& P, CState S, const double* diag_elem,
-                       double* partial, double* out2, Flags* F, cudaStream_t st);
 
 // exact mode (kernels_exact.cu)
 int launch_exact_indicator(const Mesh& M, CState S, double* r, cudaStream_t st);
