@@ -376,7 +376,7 @@ __device__ __forceinline__ void hl_node_phase_t(double* sm, const Mesh& M, const
           (sm[P::ACC + 2 * GP + pq] + sm[P::ACCX + 2 * GP + pq] + hg2 * Nd[P::N_SY * P::GNP + r]) *
           ij;
       if (FORCE) {
-        if (A.fh) rh += A.fh[n];
+        rh += A.fh[n];
         rhu += A.fhu[n];
         rhv += A.fhv[n];
       }
@@ -842,7 +842,7 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
         double rhu = (acc[1 * P::GPAD + qp] + r1[s] + hg2 * sxv) * ij;
         double rhv = (acc[2 * P::GPAD + qp] + r2[s] + hg2 * syv) * ij;
         if (FORCE) {
-          if (A.fh) rh += A.fh[n];
+          rh += A.fh[n];
           rhu += A.fhu[n];
           rhv += A.fhv[n];
         }
@@ -1163,7 +1163,7 @@ __global__ void __launch_bounds__(128) k_stage_elem(Mesh M, Phys Ph, StageArgs A
       double rhu = (r1[q] + hg2 * sxa[q]) * ij;
       double rhv = (r2[q] + hg2 * sya[q]) * ij;
       if (FORCE) {
-        if (A.fh) rh += A.fh[n];
+        rh += A.fh[n];
         rhu += A.fhu[n];
         rhv += A.fhv[n];
       }
@@ -1555,7 +1555,7 @@ __global__ void __launch_bounds__(NodePlan<N1, VISC>::THREADS, 16 / NodePlan<N1,
       double rhu = (r1 + hg2 * sb[P::F_SX * P::GNS + ln]) * ij;
       double rhv = (r2 + hg2 * sb[P::F_SY * P::GNS + ln]) * ij;
       if (FORCE && active) {
-        if (A.fh) rh += A.fh[n];
+        rh += A.fh[n];
         rhu += A.fhu[n];
         rhv += A.fhv[n];
       }
@@ -1729,52 +1729,29 @@ static void launch_half(const Mesh& M, const Phys& P, const StageArgs& A, Flags*
 // 0.197 / 0.552 ms/stage), node-per-thread at N+1 = 4 (0.853 vs full-line 0.926 vs
 // half-line 1.65), half-line above; viscous node-per-thread at N+1 = 3 (1.013 vs 1.224),
 // half-line above (N+1 = 4: 1.585 vs node 1.798).
-// viscous stages through the split path (k_visc_lhs + the inviscid stage kernel
-// with the viscous term as a forcing) at N+1 >= this; SWDG_VISC_SPLIT=0/1 forces
-// it off/on (A/B)
-#ifndef SWDG_VISC_SPLIT_MIN
-#define SWDG_VISC_SPLIT_MIN 17
-#endif
-static bool visc_split(int n1) {
-  const char* s = getenv("SWDG_VISC_SPLIT");  // read per launch: tests toggle it
-  return s ? atoi(s) != 0 : n1 >= SWDG_VISC_SPLIT_MIN;
-}
-
 template <int N1>
 static void launch_n(const Mesh& M, const Phys& P, const StageArgs& A, Flags* F,
                      cudaStream_t st) {
   if constexpr (N1 >= 3) {
     if (A.fvu) {
-      if (A.vsu && visc_split(N1)) {
-        // viscous_lhs / J into the split buffers (plus the host forcing, if any),
-        // then the inviscid stage kernel adds them like a forcing
-        launch_visc_lhs_n<N1>(M, A.fvu, A.gvu, A.fvv, A.gvv, A.fhu, A.fhv, A.vsu, A.vsv, st);
-        StageArgs B = A;
-        B.fvu = B.fvv = B.gvu = B.gvv = nullptr;
-        B.fhu = A.vsu;
-        B.fhv = A.vsv;
-        launch_n<N1>(M, P, B, F, st);
-        return;
-      }
       if constexpr (N1 <= SWDG_VISC_NODE_MAX) {
-        if (A.fhu) launch_node<N1, true, true>(M, P, A, F, st);
+        if (A.fh) launch_node<N1, true, true>(M, P, A, F, st);
         else launch_node<N1, false, true>(M, P, A, F, st);
       } else {
-        if (A.fhu) launch_half<N1, true, true>(M, P, A, F, st);
+        if (A.fh) launch_half<N1, true, true>(M, P, A, F, st);
         else launch_half<N1, false, true>(M, P, A, F, st);
       }
       return;
     }
   }
-  // FORCE: a forcing (A.fh may be null: the split viscous term has no mass part)
   if constexpr (N1 <= 3) {
-    if (A.fhu) launch_elem<N1, true>(M, P, A, F, st);
+    if (A.fh) launch_elem<N1, true>(M, P, A, F, st);
     else launch_elem<N1, false>(M, P, A, F, st);
   } else if constexpr (N1 == 4) {
-    if (A.fhu) launch_node<N1, true, false>(M, P, A, F, st);
+    if (A.fh) launch_node<N1, true, false>(M, P, A, F, st);
     else launch_node<N1, false, false>(M, P, A, F, st);
   } else {
-    if (A.fhu) launch_half<N1, true, false>(M, P, A, F, st);
+    if (A.fh) launch_half<N1, true, false>(M, P, A, F, st);
     else launch_half<N1, false, false>(M, P, A, F, st);
   }
 }

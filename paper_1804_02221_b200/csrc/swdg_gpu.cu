@@ -84,7 +84,6 @@ struct swdg_gpu {
   double* R[3] = {};       // rhs output
   double *eps = nullptr, *r_ind = nullptr;
   double *fvu = nullptr, *fvv = nullptr, *gvu = nullptr, *gvv = nullptr;
-  double *vsu = nullptr, *vsv = nullptr;
   double *fh = nullptr, *fhu = nullptr, *fhv = nullptr;
   double *partial = nullptr, *sums = nullptr;
   int int_lo = 0, int_hi = 0;   // interior element range (halo overlap), empty by default
@@ -310,8 +309,6 @@ void stage_main(swdg_gpu* c, CState in, double* const* out, int k, double t, dou
     a.fvv = c->fvv;
     a.gvu = c->gvu;
     a.gvv = c->gvv;
-    a.vsu = c->vsu;
-    a.vsv = c->vsv;
   }
   if (stage_forcing(c, a.t)) {
     a.fh = c->fh;
@@ -470,13 +467,11 @@ void allocate(swdg_gpu* c, int K, int n_owned, int N, const std::vector<int4>& e
   if (c->params.visc_enabled) {
     // padded stride like the state buffers: 16-byte aligned bases and slack for
     // the node kernel's bulk copies (one double before, one after a group)
-    double* vb = c->dalloc<double>(6 * nnp);
+    double* vb = c->dalloc<double>(4 * nnp);
     c->fvu = vb;
     c->fvv = vb + nnp;
     c->gvu = vb + 2 * nnp;
     c->gvv = vb + 3 * nnp;
-    c->vsu = vb + 4 * nnp;  // the split viscous path's per-node terms
-    c->vsv = vb + 5 * nnp;
   }
   c->partial = c->dalloc<double>(2 * (size_t)std::max(K, step_sum_partials()));
   c->rep = c->dalloc<Report>(1);

@@ -20,7 +20,6 @@ struct StageArgs {
   const double* eps;                        // per element viscosity
   const double *fvu, *fvv, *gvu, *gvv;      // viscous flux pairs (nullptr: inviscid)
   const double *fh, *fhu, *fhv;             // nodal forcing (nullptr: none)
-  double *vsu, *vsv;  // scratch of the split viscous path (viscous_lhs / J per node)
   // persistent stage kernels claim element groups from this counter (zeroed
   // before each launch) so the CTAs sweep the mesh as one wavefront and the
   // neighbour face traces they gather are still in L2 when reused

@@ -344,114 +344,3 @@ void launch_visc_lines_n(const Mesh& M, const Phys& P, CState S, double* eps, do
   const int grid = (M.n_owned + PL::E - 1) / PL::E;
   k_visc_lines<N1><<<grid, PL::THREADS, PL::bytes, st>>>(M, P, S, eps, fvu, fvv, gvu, gvv, F);
 }
-
-// ===========================================================================
-// Split viscous stage (the path chosen per degree in launch_n, VISC_SPLIT):
-// viscous_lhs (viscosity.hpp:175-247) as its own node-per-thread kernel, divided
-// by J, so the stage kernel that follows is the inviscid one with this term
-// added to dW/dt like a forcing (assemble_rhs dg_rhs.hpp:295-302: res -= visc,
-// then x(-1/J): dW/dt gains +visc / J).  Per node: the contravariant viscous
-// fluxes of the element (shared memory), the strong-form D divergence along both
-// directions, and the interface penalty J_surf (phi+ - phi-) / (2 w0) with the
-// minus side's normal (the reference's face loop, :226-246), walls 0 - phi-.
-// Costs 80 B/node (4 flux pairs + 4 metrics in, 2 terms out) but frees the stage
-// kernel of the 4 flux-pair line fields, 4 trace slots and the divergence.
-template <int N1>
-struct VLH {
-  static constexpr int NP = N1 * N1;
-  static constexpr int E = (256 / NP) > 1 ? 256 / NP : 1;
-  static constexpr int THREADS = E * NP;
-};
-
-template <int N1>
-__global__ void __launch_bounds__(VLH<N1>::THREADS)
-    k_visc_lhs(Mesh M, const double* __restrict__ fvu, const double* __restrict__ gvu,
-               const double* __restrict__ fvv, const double* __restrict__ gvv,
-               const double* fhu_in, const double* fhv_in, double* out_u, double* out_v) {
-  using P = VLH<N1>;
-  constexpr int NP = P::NP, N = N1 - 1;
-  __shared__ double s[4][P::THREADS];  // ftu, ftv, gtu, gtv
-  const int tid = threadIdx.x, el = tid / NP, loc = tid - el * NP;
-  const int i = loc / N1, j = loc - i * N1;
-  const int e = M.e_lo + blockIdx.x * P::E + el;
-  const bool active = e < M.n_owned;
-  const long long n = (long long)(active ? e : M.e_lo) * NP + loc;
-  const double fu = __ldg(fvu + n), gu = __ldg(gvu + n), fv = __ldg(fvv + n), gv = __ldg(gvv + n);
-  {
-    const double ye = __ldg(M.ye + n), xe = __ldg(M.xe + n);
-    const double yx = __ldg(M.yx + n), xx = __ldg(M.xx + n);
-    s[0][tid] = ye * fu - xe * gu;
-    s[1][tid] = ye * fv - xe * gv;
-    s[2][tid] = -yx * fu + xx * gu;
-    s[3][tid] = -yx * fv + xx * gv;
-  }
-  double di[N1], dj[N1];
-#pragma unroll
-  for (int m = 0; m < N1; ++m) {
-    di[m] = __ldg(M.D + i * N1 + m);
-    dj[m] = __ldg(M.D + j * N1 + m);
-  }
-  __syncthreads();
-  if (!active) return;
-  const int b = el * NP;
-  double su = 0.0, sv = 0.0;
-#pragma unroll
-  for (int m = 0; m < N1; ++m) {
-    su += di[m] * s[0][b + m * N1 + j] + dj[m] * s[2][b + i * N1 + m];
-    sv += di[m] * s[1][b + m * N1 + j] + dj[m] * s[3][b + i * N1 + m];
-  }
-  int faces[2], ts[2];
-  const int nfc = node_faces(N1, i, j, faces, ts);
-  const double iw0 = 1.0 / M.w0;
-  for (int q = 0; q < nfc; ++q) {
-    const int f = faces[q], t = ts[q];
-    const int4 ef = __ldg(M.ef + (long long)e * 4 + f);
-    if (!(ef.y & EF_PRESENT)) continue;
-    double du, dv, js;
-    if (ef.y & EF_MINUS) {
-      const long long fi = ((long long)e * 4 + f) * N1 + t;
-      const double nx = __ldg(M.fnx + fi), ny = __ldg(M.fny + fi);
-      js = __ldg(M.fjs + fi);
-      const double pmu = nx * fu + ny * gu, pmv = nx * fv + ny * gv;
-      if (ef.y & EF_WALL) {
-        du = 0.0 - pmu;
-        dv = 0.0 - pmv;
-      } else {
-        const int nf = ef.y & EF_NBR_FACE_MASK;
-        const int tp = (ef.y & EF_REVERSED) ? N - t : t;
-        const long long nb = (long long)ef.x * NP + face_node(N1, nf, tp);
-        const double ppu = nx * __ldg(fvu + nb) + ny * __ldg(gvu + nb);
-        const double ppv = nx * __ldg(fvv + nb) + ny * __ldg(gvv + nb);
-        du = 0.5 * (ppu - pmu);
-        dv = 0.5 * (ppv - pmv);
-      }
-    } else {  // plus side: the minus element's normal at the partner node
-      const int nf = ef.y & EF_NBR_FACE_MASK;
-      const int tp = (ef.y & EF_REVERSED) ? N - t : t;
-      const long long fi = ((long long)ef.x * 4 + nf) * N1 + tp;
-      const double nx = __ldg(M.fnx + fi), ny = __ldg(M.fny + fi);
-      js = __ldg(M.fjs + fi);
-      const long long nb = (long long)ef.x * NP + face_node(N1, nf, tp);
-      const double pmu = nx * __ldg(fvu + nb) + ny * __ldg(gvu + nb);
-      const double pmv = nx * __ldg(fvv + nb) + ny * __ldg(gvv + nb);
-      du = 0.5 * ((nx * fu + ny * gu) - pmu);
-      dv = 0.5 * ((nx * fv + ny * gv) - pmv);
-    }
-    su += js * du * iw0;
-    sv += js * dv * iw0;
-  }
-  const double ij = frcp(__ldg(M.jac + n));
-  out_u[n] = su * ij + (fhu_in ? fhu_in[n] : 0.0);
-  out_v[n] = sv * ij + (fhv_in ? fhv_in[n] : 0.0);
-}
-
-template <int N1>
-void launch_visc_lhs_n(const Mesh& M, const double* fvu, const double* gvu, const double* fvv,
-                       const double* gvv, const double* fhu, const double* fhv, double* ou,
-                       double* ov, cudaStream_t st) {
-  using P = VLH<N1>;
-  const int ne = M.n_owned - M.e_lo;
-  if (ne <= 0) return;
-  k_visc_lhs<N1><<<(ne + P::E - 1) / P::E, P::THREADS, 0, st>>>(M, fvu, gvu, fvv, gvv, fhu, fhv,
-                                                                 ou, ov);
-}
