@@ -294,62 +294,3 @@ def test_run_steps_graph_matches_eager(N, visc, monkeypatch):
         outs.append(st.arrays())
     for a, b in zip(*outs):
         assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
-
-
-<<<<<<< HEAD
-@pytest.mark.parametrize("N", [2, 3, 4, 7, 9, 12, 15])
-def test_viscous_split_path(N, monkeypatch):
-    """The split viscous stage (k_visc_lhs, viscous_lhs / J as a forcing of the
-    inviscid stage kernel) and the fused one (the viscous half-line / node kernel)
-    against the reference's viscous evaluate_rhs: one stage within 1e-12 normwise,
-    smooth and rough states, on a mesh large enough for many groups per CTA."""
-    m = ref.build_mesh("wavy", N, 24, 20, periodic_x=True, periodic_y=True).bathymetry("smooth")
-    smin, smax = swdg.default_sigma_band(N)
-    p = ref.params(g=9.81, visc=True, epsilon0=0.1, sigma_min=smin, sigma_max=smax)
-    ri = ref.Integrator(m, p)
-    for kind in ("smooth", "rough"):
-        if kind == "smooth":
-            s = smooth_state(m, 0.1)
-        else:
-            s = ref.bench_rough_state(N, m.n_elem)
-        dt = 0.01 * ref.compute_dt(m, p, s, 0.5)
-        r = ri.evaluate_rhs(s, 0.0)
-        want = [a + dt * b for a, b in zip(s, r)]
-        ref.limit_all(m, p, want)
-        for split in ("1", "0"):
-            monkeypatch.setenv("SWDG_VISC_SPLIT", split)
-            g = swdg.TimeIntegrator(m, cfg_from(p))
-            got = g.run_stage(0, S(s), None, 0.0, dt)
-            assert normwise(got.arrays(), want) <= 1e-12, (kind, split)
-=======
-@pytest.mark.parametrize("N", [4, 7, 8, 12])
-def test_fused_step_reductions_match_separate(N, monkeypatch):
-    """The step reductions fused into the stage-3 half-line kernel (mass, entropy,
-    CFL candidates in the write-out; then the element-pair sum and the face-only
-    positivity pass) against the separate pass: the next dt, min h and the
-    positivity bound bitwise, mass and entropy to 1e-13; the state bitwise."""
-    m = ref.build_mesh("wavy", N, 9, 8, periodic_x=True, periodic_y=True).bathymetry("smooth")
-    p = ref.params(g=9.81)
-    s = random_state(m.n_nodes, np.random.default_rng(N), h=(0.5, 1.5), vel=0.5, dry_prob=0.05)
-    reps, states = [], []
-    for separate in (False, True):
-        if separate:
-            monkeypatch.setenv("SWDG_NO_FUSED_DIAG", "1")
-        g = swdg.TimeIntegrator(m, cfg_from(p))
-        st = S(s)
-        g.upload(st)
-        dt = 0.2 * g.compute_dt_device(0.5)
-        r = g.step_device(0.0, dt, 0.5)
-        assert r.info.accepted
-        g.download(st)
-        reps.append(r)
-        states.append(st.arrays())
-    a, b = reps
-    assert a.next_dt == b.next_dt
-    assert a.diag.min_h == b.diag.min_h
-    assert a.diag.positivity_dt == b.diag.positivity_dt
-    assert abs(a.diag.mass - b.diag.mass) <= 1e-13 * abs(b.diag.mass)
-    assert abs(a.diag.entropy - b.diag.entropy) <= 1e-13 * abs(b.diag.entropy)
-    for x, y in zip(*states):
-        assert np.array_equal(x.view(np.uint64), y.view(np.uint64))
->>>>>>> parent of 0ee0e31 (Split viscous stage: viscous_lhs / J per node (k_visc_lhs) added by the inviscid stage kernel like a forcing; per-degree switch (SWDG_VISC_SPLIT for A/B), test against the reference)
