@@ -21,7 +21,7 @@ ROOT = os.path.dirname(PKG)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-          "-diag-suppress=177",
+          "-diag-suppress=177", *os.environ.get("SWDG_NVCC_FLAGS", "").split(),
           "-I" + CSRC, "-I" + os.path.join(ROOT, "include")]
 
 # object name -> (source, extra flags).  kernels_fast.cu is compiled once per
