@@ -215,35 +215,6 @@ __device__ __forceinline__ void pair_flux(double ha, double ua, double va, doubl
 template <int N1>
 using HArr = double[HL<N1>::H];
 
-// Pair order inside a half: with SWDG_HL_ILP the unordered pairs run in
-// round-robin rounds (the circle method: every round is a perfect matching of the
-// half's nodes), so consecutive pairs update disjoint accumulators and their
-// dependency chains interleave; otherwise row by row.
-#ifndef SWDG_HL_ILP
-#define SWDG_HL_ILP 1
-#endif
-// pair p of the round-robin schedule of nk nodes: first the corner diagonal,
-// then the rounds; {-1, -1} past the end (dummy partner of an odd nk)
-struct Pair {
-  int a = 0, b = 0;
-};
-__host__ __device__ constexpr Pair rr_pair(int nk, int corner, int p) {
-  if (p == 0) return {corner, corner};
-  p -= 1;
-  const int m = nk + (nk & 1);  // even player count (m - 1 = dummy when nk is odd)
-  const int per = m / 2, r = p / per, k = p % per;
-  int a = 0, b = 0;
-  if (k == 0) {
-    a = r;
-    b = m - 1;
-  } else {
-    a = (r + k) % (m - 1);
-    b = (r - k + (m - 1)) % (m - 1);
-  }
-  if (a >= nk || b >= nk) return {-1, -1};
-  return a < b ? Pair{a, b} : Pair{b, a};
-}
-
 template <int N1, int PART>
 __device__ __forceinline__ void hl_intra(const HArr<N1>& h, const HArr<N1>& u,
                                          const HArr<N1>& v, const HArr<N1>& hu,
@@ -253,33 +224,21 @@ __device__ __forceinline__ void hl_intra(const HArr<N1>& h, const HArr<N1>& u,
   using O = Ops<N1>;
   constexpr int H = HL<N1>::H, NK = PART ? N1 - H : H, OFF = PART ? H : 0;
   constexpr int CORNER = PART ? NK - 1 : 0;  // node 0 (X) / node N (Y): Dtilde(i,i) != 0
-  auto one = [&](int a, int b) {
-    double F0, T1, T2;
-    pair_flux(h[a], u[a], v[a], hu[a], hv[a], Am[a], Bm[a], h[b], u[b], v[b], hu[b], hv[b],
-              Am[b], Bm[b], g2, F0, T1, T2);
-    r0[a] += O::D4(OFF + a, OFF + b) * F0;
-    r1[a] += O::D8(OFF + a, OFF + b) * T1;
-    r2[a] += O::D8(OFF + a, OFF + b) * T2;
-    if (a != b) {
-      r0[b] += O::D4(OFF + b, OFF + a) * F0;
-      r1[b] += O::D8(OFF + b, OFF + a) * T1;
-      r2[b] += O::D8(OFF + b, OFF + a) * T2;
-    }
-  };
-  if constexpr (SWDG_HL_ILP) {
-    constexpr int M = NK + (NK & 1), NP_ = 1 + (M - 1) * (M / 2);
 #pragma unroll
-    for (int p = 0; p < NP_; ++p) {
-      const Pair q = rr_pair(NK, CORNER, p);
-      if (q.a >= 0) one(q.a, q.b);
-    }
-  } else {
+  for (int a = 0; a < NK; ++a) {
 #pragma unroll
-    for (int a = 0; a < NK; ++a) {
-#pragma unroll
-      for (int b = a; b < NK; ++b) {
-        if (a == b && a != CORNER) continue;
-        one(a, b);
+    for (int b = a; b < NK; ++b) {
+      if (a == b && a != CORNER) continue;
+      double F0, T1, T2;
+      pair_flux(h[a], u[a], v[a], hu[a], hv[a], Am[a], Bm[a], h[b], u[b], v[b], hu[b], hv[b],
+                Am[b], Bm[b], g2, F0, T1, T2);
+      r0[a] += O::D4(OFF + a, OFF + b) * F0;
+      r1[a] += O::D8(OFF + a, OFF + b) * T1;
+      r2[a] += O::D8(OFF + a, OFF + b) * T2;
+      if (a != b) {
+        r0[b] += O::D4(OFF + b, OFF + a) * F0;
+        r1[b] += O::D8(OFF + b, OFF + a) * T1;
+        r2[b] += O::D8(OFF + b, OFF + a) * T2;
       }
     }
   }
@@ -682,8 +641,7 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
         const double Bb = xi ? Lb[P::F_XE * P::GPAD + q] : -Lb[P::F_XX * P::GPAD + q];
         double ub, vb;
         vel(hb, hub, hvb, h_des, ub, vb);
-        // the streamed node's sums in two interleaved chains (SWDG_HL_ILP)
-        double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0}, c2[2] = {0.0, 0.0};
+        double c0 = 0.0, c1 = 0.0, c2 = 0.0;
 #pragma unroll
         for (int a = 0; a < H; ++a) {
           double F0, T1, T2;
@@ -692,14 +650,13 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
           r0[a] += O::D4(a, H + s) * F0;
           r1[a] += O::D8(a, H + s) * T1;
           r2[a] += O::D8(a, H + s) * T2;
-          const int ch = SWDG_HL_ILP ? (a & 1) : 0;
-          c0[ch] += O::D4(H + s, a) * F0;
-          c1[ch] += O::D8(H + s, a) * T1;
-          c2[ch] += O::D8(H + s, a) * T2;
+          c0 += O::D4(H + s, a) * F0;
+          c1 += O::D8(H + s, a) * T1;
+          c2 += O::D8(H + s, a) * T2;
         }
-        xch(3 * s + 0) = c0[0] + c0[1];
-        xch(3 * s + 1) = c1[0] + c1[1];
-        xch(3 * s + 2) = c2[0] + c2[1];
+        xch(3 * s + 0) = c0;
+        xch(3 * s + 1) = c1;
+        xch(3 * s + 2) = c2;
       }
     } else {
 #pragma unroll
@@ -711,7 +668,7 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
         const double Ba = xi ? Lb[P::F_XE * P::GPAD + q] : -Lb[P::F_XX * P::GPAD + q];
         double ua, va;
         vel(ha, hua, hva, h_des, ua, va);
-        double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0}, c2[2] = {0.0, 0.0};
+        double c0 = 0.0, c1 = 0.0, c2 = 0.0;
 #pragma unroll
         for (int s = NB0; s < N1 - H; ++s) {
           double F0, T1, T2;
@@ -720,14 +677,13 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
           r0[s] += O::D4(H + s, a) * F0;
           r1[s] += O::D8(H + s, a) * T1;
           r2[s] += O::D8(H + s, a) * T2;
-          const int ch = SWDG_HL_ILP ? ((s - NB0) & 1) : 0;
-          c0[ch] += O::D4(a, H + s) * F0;
-          c1[ch] += O::D8(a, H + s) * T1;
-          c2[ch] += O::D8(a, H + s) * T2;
+          c0 += O::D4(a, H + s) * F0;
+          c1 += O::D8(a, H + s) * T1;
+          c2 += O::D8(a, H + s) * T2;
         }
-        xch(3 * NB0 + 3 * a + 0) = c0[0] + c0[1];
-        xch(3 * NB0 + 3 * a + 1) = c1[0] + c1[1];
-        xch(3 * NB0 + 3 * a + 2) = c2[0] + c2[1];
+        xch(3 * NB0 + 3 * a + 0) = c0;
+        xch(3 * NB0 + 3 * a + 1) = c1;
+        xch(3 * NB0 + 3 * a + 2) = c2;
       }
     }
     // ---- viscous divergence along the line, own endpoint flux pairs kept for the
