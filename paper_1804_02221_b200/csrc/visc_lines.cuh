@@ -53,8 +53,17 @@ struct VLP {
   static constexpr size_t bytes = TOTAL * sizeof(double);
 };
 
+// resident CTAs the register allocation is compiled for (0: no bound)
+#ifndef VL_MINB_LO
+#define VL_MINB_LO 0  // N+1 <= 8
+#endif
+#ifndef VL_MINB_HI
+#define VL_MINB_HI 0  // N+1 >= 9
+#endif
+__host__ __device__ constexpr int vl_min_blocks(int n1) { return n1 <= 8 ? VL_MINB_LO : VL_MINB_HI; }
+
 template <int N1>
-__global__ void __launch_bounds__(VLP<N1>::THREADS)
+__global__ void __launch_bounds__(VLP<N1>::THREADS, vl_min_blocks(N1))
     k_visc_lines(Mesh M, Phys Ph, CState S, double* eps_out, double* fvu, double* fvv,
                  double* gvu, double* gvv, Flags* F) {
   using P = VLP<N1>;
