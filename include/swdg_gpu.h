@@ -343,6 +343,11 @@ int swdg_gpu_stage_info(swdg_gpu* ctx, int stage, swdg_step_info* info);
  * unpack (part 0 = all, like stage_run).  Exact mode runs everything in part 2. */
 int swdg_gpu_set_interior(swdg_gpu* ctx, int32_t lo, int32_t hi);
 int swdg_gpu_stage_run_part(swdg_gpu* ctx, int stage, double t, double dt, int part);
+/* The viscous pre-pass of a stage in the same two parts: part 1 (the interior:
+ * its BR1 face corrections need no ghost state) while the state exchange is in
+ * flight, part 2 after the unpack; then the flux-pair exchange overlaps the
+ * interior stage (stage_run_part 1).  Exact mode runs it whole in part 2. */
+int swdg_gpu_stage_visc_part(swdg_gpu* ctx, int stage, double t, double dt, int part);
 
 #ifdef __cplusplus
 }

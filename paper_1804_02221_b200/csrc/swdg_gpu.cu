@@ -276,9 +276,9 @@ bool stage_forcing(swdg_gpu* c, double ts) {
 // Viscous pre-pass of a stage input: eps, BR1 gradients and the flux pairs into
 // c->fvu.. (fast: one device kernel, max eps into F; exact: indicator on the
 // device, ramp on the host).  Returns the host-side max eps (exact mode).
-double stage_visc(swdg_gpu* c, CState in, Flags* F) {
+double stage_visc(swdg_gpu* c, CState in, Flags* F, const Mesh* range = nullptr) {
   if (c->fast) {
-    c->launches += launched(launch_fast_visc_pre(c->M, c->phys, in, c->eps, c->fvu, c->fvv, c->gvu,
+    c->launches += launched(launch_fast_visc_pre(range ? *range : c->M, c->phys, in, c->eps, c->fvu, c->fvv, c->gvu,
                                         c->gvv, F, c->stream), "launch_fast_visc_pre");
     return 0.0;
   }
@@ -1388,6 +1388,39 @@ int swdg_gpu_stage_run(swdg_gpu* c, int k, double t, double dt) {
     if (k < 0 || k > 2) throw InputError{"stage_run: bad stage"};
     stage_main(c, cs(stage_input(c, k)), stage_output(c, k), k, t, dt,
                c->params.visc_enabled != 0, nullptr, c->flags + k);
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_stage_visc_part(swdg_gpu* c, int k, double t, double dt, int part) {
+  (void)t;
+  (void)dt;
+  return guarded(c, [&] {
+    if (k < 0 || k > 2) throw InputError{"stage_visc_part: bad stage"};
+    if (part < 0 || part > 2) throw InputError{"stage_visc_part: bad part"};
+    if (!c->params.visc_enabled) return SWDG_OK;
+    const CState in = cs(stage_input(c, k));
+    if (part == 0 || !c->fast || c->int_hi <= c->int_lo) {
+      // exact mode (host ramp over all elements) and partitions without an
+      // interior: everything after the exchange
+      if (part != 1) c->split_max_eps = std::max(c->split_max_eps, stage_visc(c, in, c->flags + k));
+      return SWDG_OK;
+    }
+    Mesh r = c->M;
+    if (part == 1) {
+      r.e_lo = c->int_lo;
+      r.n_owned = c->int_hi;
+      c->reserve_sms = kHaloReserveSms;
+      stage_visc(c, in, c->flags + k, &r);
+      c->reserve_sms = 0;
+    } else {
+      r.e_lo = 0;
+      r.n_owned = c->int_lo;
+      stage_visc(c, in, c->flags + k, &r);
+      r.e_lo = c->int_hi;
+      r.n_owned = c->M.n_owned;
+      stage_visc(c, in, c->flags + k, &r);
+    }
     return SWDG_OK;
   });
 }

@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(VLP<N1>::THREADS, vl_min_blocks(N1))
   const int ls = xi ? tid : tid - P::LS;  // line slot within the direction
   const bool line_ok = ls < LPD;
   const int el = line_ok ? ls / N1 : 0, li = line_ok ? ls - (ls / N1) * N1 : 0;
-  const int e0 = blockIdx.x * P::E, ne = min(P::E, M.n_owned - e0);
+  const int e0 = M.e_lo + blockIdx.x * P::E, ne = min(P::E, M.n_owned - e0);
   const bool active = line_ok && el < ne;
   const int e = e0 + el;
   const double h_des = Ph.h_des, iw0 = 1.0 / M.w0;
@@ -350,6 +350,7 @@ void launch_visc_lines_n(const Mesh& M, const Phys& P, CState S, double* eps, do
                          (int)PL::bytes);
     attr[dev] = true;
   }
-  const int grid = (M.n_owned + PL::E - 1) / PL::E;
+  if (M.n_owned <= M.e_lo) return;
+  const int grid = (M.n_owned - M.e_lo + PL::E - 1) / PL::E;
   k_visc_lines<N1><<<grid, PL::THREADS, PL::bytes, st>>>(M, P, S, eps, fvu, fvv, gvu, gvv, F);
 }

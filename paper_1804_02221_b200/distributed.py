@@ -143,9 +143,23 @@ INTERIOR, BOUNDARY = 1, 2
 
 
 def _overlap(b: Backend) -> bool:
-    """inviscid partitions with an interior run the stage in two parts, the
-    interior one while the state halo is in flight"""
-    return not b.visc and getattr(b, "has_interior", False)
+    """partitions with an interior run each stage in two parts, the interior one
+    while a halo is in flight: inviscid, the stage kernel during the state
+    exchange; viscous, the pre-kernel during the state exchange and the stage
+    kernel during the flux-pair exchange"""
+    return getattr(b, "has_interior", False)
+
+
+def _stage_overlapped(b: Backend, ex, k: int, t: float, dt: float):
+    h = ex.start(0, k)
+    if b.visc:
+        b.stage_visc_part(k, t, dt, INTERIOR)
+        ex.finish(h)
+        b.stage_visc_part(k, t, dt, BOUNDARY)
+        h = ex.start(1, k)
+    b.stage_run_part(k, t, dt, INTERIOR)
+    ex.finish(h)
+    b.stage_run_part(k, t, dt, BOUNDARY)
 
 
 def try_step_distributed(b: Backend, ex, t: float, dt: float) -> bool:
@@ -153,10 +167,7 @@ def try_step_distributed(b: Backend, ex, t: float, dt: float) -> bool:
     b.step_begin()
     for k in range(3):
         if _overlap(b) and hasattr(ex, "start"):
-            h = ex.start(0, k)
-            b.stage_run_part(k, t, dt, INTERIOR)
-            ex.finish(h)
-            b.stage_run_part(k, t, dt, BOUNDARY)
+            _stage_overlapped(b, ex, k, t, dt)
             continue
         ex.exchange(0, k)
         if b.visc:
@@ -183,10 +194,7 @@ def run_steps_distributed(b: Backend, ex, nsteps: int, t: float, dt: float) -> b
         ts = t + s * dt
         for k in range(3):
             if _overlap(b) and hasattr(ex, "start"):
-                h = ex.start(0, k)
-                b.stage_run_part(k, ts, dt, INTERIOR)
-                ex.finish(h)
-                b.stage_run_part(k, ts, dt, BOUNDARY)
+                _stage_overlapped(b, ex, k, ts, dt)
                 continue
             ex.exchange(0, k)
             if b.visc:
@@ -206,10 +214,20 @@ def try_step_loopback(bs, ex: LoopbackExchanger, t: float, dt: float) -> bool:
     for b in bs:
         b.step_begin()
     for k in range(3):
-        if all(_overlap(b) for b in bs):  # interior before the exchange, like NCCL ranks
-            for b in bs:
-                b.stage_run_part(k, t, dt, INTERIOR)
-            ex.exchange_all(0, k)
+        if all(_overlap(b) for b in bs):  # interior before each exchange, like NCCL ranks
+            if bs[0].visc:
+                for b in bs:
+                    b.stage_visc_part(k, t, dt, INTERIOR)
+                ex.exchange_all(0, k)
+                for b in bs:
+                    b.stage_visc_part(k, t, dt, BOUNDARY)
+                for b in bs:
+                    b.stage_run_part(k, t, dt, INTERIOR)
+                ex.exchange_all(1, k)
+            else:
+                for b in bs:
+                    b.stage_run_part(k, t, dt, INTERIOR)
+                ex.exchange_all(0, k)
             for b in bs:
                 b.stage_run_part(k, t, dt, BOUNDARY)
             continue
@@ -329,6 +347,8 @@ class GpuPartition(Backend):
                            ("swdg_gpu_stage_visc", [vp, C.c_int, C.c_double, C.c_double]),
                            ("swdg_gpu_stage_run", [vp, C.c_int, C.c_double, C.c_double]),
                            ("swdg_gpu_set_interior", [vp, C.c_int32, C.c_int32]),
+                           ("swdg_gpu_stage_visc_part", [vp, C.c_int, C.c_double, C.c_double,
+                                                         C.c_int]),
                            ("swdg_gpu_stage_run_part", [vp, C.c_int, C.c_double, C.c_double,
                                                         C.c_int]),
                            ("swdg_gpu_step_flags", [vp, i32p, i32p]),
@@ -400,6 +420,9 @@ class GpuPartition(Backend):
 
     def stage_run_part(self, k, t, dt, part):
         self._chk(self.L.swdg_gpu_stage_run_part(self.integ._h, k, t, dt, part))
+
+    def stage_visc_part(self, k, t, dt, part):
+        self._chk(self.L.swdg_gpu_stage_visc_part(self.integ._h, k, t, dt, part))
 
     def step_flags(self):
         r, a = C.c_int32(), C.c_int32()
