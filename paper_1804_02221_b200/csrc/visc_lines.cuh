@@ -53,17 +53,8 @@ struct VLP {
   static constexpr size_t bytes = TOTAL * sizeof(double);
 };
 
-// resident CTAs the register allocation is compiled for (0: no bound)
-#ifndef VL_MINB_LO
-#define VL_MINB_LO 0  // N+1 <= 8
-#endif
-#ifndef VL_MINB_HI
-#define VL_MINB_HI 0  // N+1 >= 9
-#endif
-__host__ __device__ constexpr int vl_min_blocks(int n1) { return n1 <= 8 ? VL_MINB_LO : VL_MINB_HI; }
-
 template <int N1>
-__global__ void __launch_bounds__(VLP<N1>::THREADS, vl_min_blocks(N1))
+__global__ void __launch_bounds__(VLP<N1>::THREADS)
     k_visc_lines(Mesh M, Phys Ph, CState S, double* eps_out, double* fvu, double* fvv,
                  double* gvu, double* gvv, Flags* F) {
   using P = VLP<N1>;
@@ -75,7 +66,7 @@ __global__ void __launch_bounds__(VLP<N1>::THREADS, vl_min_blocks(N1))
   const int ls = xi ? tid : tid - P::LS;  // line slot within the direction
   const bool line_ok = ls < LPD;
   const int el = line_ok ? ls / N1 : 0, li = line_ok ? ls - (ls / N1) * N1 : 0;
-  const int e0 = M.e_lo + blockIdx.x * P::E, ne = min(P::E, M.n_owned - e0);
+  const int e0 = blockIdx.x * P::E, ne = min(P::E, M.n_owned - e0);
   const bool active = line_ok && el < ne;
   const int e = e0 + el;
   const double h_des = Ph.h_des, iw0 = 1.0 / M.w0;
@@ -350,7 +341,6 @@ void launch_visc_lines_n(const Mesh& M, const Phys& P, CState S, double* eps, do
                          (int)PL::bytes);
     attr[dev] = true;
   }
-  if (M.n_owned <= M.e_lo) return;
-  const int grid = (M.n_owned - M.e_lo + PL::E - 1) / PL::E;
+  const int grid = (M.n_owned + PL::E - 1) / PL::E;
   k_visc_lines<N1><<<grid, PL::THREADS, PL::bytes, st>>>(M, P, S, eps, fvu, fvv, gvu, gvv, F);
 }
