@@ -20,6 +20,8 @@ def main():
     ap.add_argument("--viscous", action="store_true")
     ap.add_argument("--exact", action="store_true")
     ap.add_argument("--time", type=int, default=0, help="time this many extra steps")
+    ap.add_argument("--diag", action="store_true",
+                    help="also run the step reductions (run_steps with reductions, step_device)")
     a = ap.parse_args()
     N = a.degree
     visc = swdg.ViscosityConfig(False)
@@ -36,7 +38,9 @@ def main():
     st = swdg.State(h, 0.3 * h, -0.2 * h)
     integ.upload(st)
     dt = 0.1 * integ.compute_dt_device(0.5)
-    integ.run_steps(a.steps, 0.0, dt)
+    integ.run_steps(a.steps, 0.0, dt, reductions=a.diag)
+    if a.diag:
+        integ.step_device(a.steps * dt, dt, 0.5)
     integ.synchronize()
     if a.time:
         import time
