@@ -278,6 +278,7 @@ bool stage_forcing(swdg_gpu* c, double ts) {
 // device, ramp on the host).  Returns the host-side max eps (exact mode).
 double stage_visc(swdg_gpu* c, CState in, Flags* F, const Mesh* range = nullptr) {
   if (c->fast) {
+    if (range && range->n_owned <= range->e_lo) return 0.0;  // empty boundary slab
     c->launches += launched(launch_fast_visc_pre(range ? *range : c->M, c->phys, in, c->eps, c->fvu, c->fvv, c->gvu,
                                         c->gvv, F, c->stream), "launch_fast_visc_pre");
     return 0.0;
