@@ -37,9 +37,11 @@ struct VLP {
   static constexpr int THREADS = 2 * LS;
   static constexpr int PAD = N1 | 1, EPAD = N1 * PAD, GPAD = E * EPAD;
   static constexpr int PMAX = (LPD + 31) / 32 + 1;
-  // shared fields [E][N1][PAD]: state and metrics, the first modal pass, and the
-  // four BR1 partials of each direction
-  enum { H, U, V, YE, XE, YX, XX, TMP, XU1, XU2, XV1, XV2, EU1, EU2, EV1, EV2, kF };
+  // shared fields [E][N1][PAD]: state, the first modal pass, and the four BR1
+  // partials of each direction.  The metrics are read from global memory by the
+  // line threads (each is used by one direction only): 12 instead of 16 fields
+  // per node, so more CTAs share an SM
+  enum { H, U, V, TMP, XU1, XU2, XV1, XV2, EU1, EU2, EV1, EV2, kF };
   // asynchronous (LDGSTS) staging, measured (viscous ms/stage, pre-kernel +
   // stage): N=10 14.94 -> 13.67, N=12 22.44 -> 20.80; slower at N+1 = 8 (6.24
   // synchronous vs 6.32-6.37) and N+1 = 5 (2.57 -> 2.80)
@@ -66,7 +68,7 @@ __global__ void __launch_bounds__(VLP<N1>::THREADS)
   const int ls = xi ? tid : tid - P::LS;  // line slot within the direction
   const bool line_ok = ls < LPD;
   const int el = line_ok ? ls / N1 : 0, li = line_ok ? ls - (ls / N1) * N1 : 0;
-  const int e0 = blockIdx.x * P::E, ne = min(P::E, M.n_owned - e0);
+  const int e0 = M.e_lo + blockIdx.x * P::E, ne = min(P::E, M.n_owned - e0);
   const bool active = line_ok && el < ne;
   const int e = e0 + el;
   const double h_des = Ph.h_des, iw0 = 1.0 / M.w0;
@@ -92,10 +94,6 @@ __global__ void __launch_bounds__(VLP<N1>::THREADS)
       cp_async8(d + P::H * GP, S.h + n);
       cp_async8(d + P::XU1 * GP, S.hu + n);
       cp_async8(d + P::XU2 * GP, S.hv + n);
-      cp_async8(d + P::YE * GP, M.ye + n);
-      cp_async8(d + P::XE * GP, M.xe + n);
-      cp_async8(d + P::YX * GP, M.yx + n);
-      cp_async8(d + P::XX * GP, M.xx + n);
     }
     cp_async_commit();
   }
@@ -116,6 +114,20 @@ __global__ void __launch_bounds__(VLP<N1>::THREADS)
         nhu[end] = __ldg(S.hu + nb);
         nhv[end] = __ldg(S.hv + nb);
       }
+    }
+  }
+  // this line's metrics, straight from global memory (in flight with the staging):
+  // node k of the line is (k, li) on xi lines, (li, k) on eta lines
+  double A[N1], B[N1];
+  {
+    const double* ga = xi ? M.ye : M.yx;
+    const double* gb = xi ? M.xe : M.xx;
+    const long long g0 = (long long)(active ? e : e0) * NP + (xi ? li : li * N1);
+    const int gs = xi ? N1 : 1;
+#pragma unroll
+    for (int k = 0; k < N1; ++k) {
+      A[k] = __ldg(ga + g0 + k * gs);
+      B[k] = __ldg(gb + g0 + k * gs);
     }
   }
   if constexpr (P::kAsync) {
@@ -142,10 +154,6 @@ __global__ void __launch_bounds__(VLP<N1>::THREADS)
       d[P::H * GP] = h;
       d[P::U * GP] = u;
       d[P::V * GP] = v;
-      d[P::YE * GP] = M.ye[n];
-      d[P::XE * GP] = M.xe[n];
-      d[P::YX * GP] = M.yx[n];
-      d[P::XX * GP] = M.xx[n];
     }
   }
   __syncthreads();
@@ -153,14 +161,6 @@ __global__ void __launch_bounds__(VLP<N1>::THREADS)
   // ---- line phase: node k of this line at off0 + k*st
   const int off0 = el * P::EPAD + (xi ? li : li * PAD), st = xi ? PAD : 1;
   if (active) {
-    double A[N1], B[N1];
-    const int fa = (xi ? P::YE : P::YX) * GP, fb = (xi ? P::XE : P::XX) * GP;
-#pragma unroll
-    for (int k = 0; k < N1; ++k) {
-      const int q = off0 + k * st;
-      A[k] = sm[fa + q];
-      B[k] = sm[fb + q];
-    }
     if (xi) {  // first modal pass along i: tmp(a, j) = sum_k Vinv(a, k) h(k, j)
       double hh[N1];
 #pragma unroll
@@ -341,6 +341,7 @@ void launch_visc_lines_n(const Mesh& M, const Phys& P, CState S, double* eps, do
                          (int)PL::bytes);
     attr[dev] = true;
   }
-  const int grid = (M.n_owned + PL::E - 1) / PL::E;
+  if (M.n_owned <= M.e_lo) return;
+  const int grid = (M.n_owned - M.e_lo + PL::E - 1) / PL::E;
   k_visc_lines<N1><<<grid, PL::THREADS, PL::bytes, st>>>(M, P, S, eps, fvu, fvv, gvu, gvv, F);
 }
