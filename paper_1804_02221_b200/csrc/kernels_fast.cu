@@ -79,6 +79,12 @@
 #define SWDG_HL_MB7 4
 #endif
 
+// viscous stages from this N+1 on: the eta lines apply the source and -1/J to
+// their half before the hand-over (HL::PRE)
+#ifndef SWDG_HL_PRE_VMIN
+#define SWDG_HL_PRE_VMIN 16  // measured: viscous N=15 44.4 -> 40.1 ms/stage; N+1 = 13..15 1-4% slower
+#endif
+
 namespace swdg_dev {
 
 namespace {
@@ -104,6 +110,7 @@ __device__ __forceinline__ int next_group(int* ctr, int grp) {
 template <int N1, bool V = false>
 struct HL {
   static constexpr bool kVisc = V;
+  static constexpr bool NT_ = !V && N1 == 9;  // transposed node phase (see NT)
   static constexpr int NP = N1 * N1, LE = 2 * N1;
   static constexpr int H = (N1 + 1) / 2, NB = N1 - H;
   static constexpr int work_x(int b0) { return H * (H - 1) / 2 + H * b0; }
@@ -175,7 +182,10 @@ struct HL {
   static constexpr int NBUF = DB ? 2 : 1;
   static constexpr int LINE = 0;
   static constexpr int ACC = LINE + NBUF * LBUF;
-  static constexpr int XCH = ACC + 3 * GPAD;
+  // eta-line hand-over: 3 accumulators, plus -1/J (PRE: the eta lines apply the
+  // source and -1/J to their half before handing over)
+  static constexpr bool PRE = !NT_ && V && N1 >= SWDG_HL_PRE_VMIN;
+  static constexpr int XCH = ACC + (PRE ? 4 : 3) * GPAD;
   static constexpr int NODE = XCH + LP * XS;
   static constexpr int TR = NODE + kNodeFields * GNP;  // [kTr][E][4][N1]
   static constexpr int EFO = TR + E * 4 * N1 * kTr;     // int4 [NBUF][E][4]
@@ -187,7 +197,7 @@ struct HL {
   // (B200, 1M elements) inviscid N=5 1.615 -> 1.463 ms/stage; slower at every
   // other degree (twice the code: N=8 4.34 -> 5.16, N=15 13.2 -> 27.0)
   static constexpr bool XI_SPLIT = !V && N1 == 6;
-  static constexpr bool NT = !V && N1 == 9;  // measured: faster only at N+1 = 9 (4.56 -> 4.34 ms), slower at 6, 7, 8, 10
+  static constexpr bool NT = NT_;  // measured: faster only at N+1 = 9 (4.56 -> 4.34 ms), slower at 6, 7, 8, 10
   static constexpr int NPT = (E * NP + THREADS - 1) / THREADS;  // nodes per thread
   static constexpr int PMAX = NP / 32 + 2;                      // node-warp pieces
   static constexpr int ACCX = BAR + 2;                          // [3][GPAD] xi accumulators
@@ -797,7 +807,30 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
     }
     // eta-line threads hand their accumulators to the xi-line owners (NT: the
     // xi lines also leave theirs and the state, for the transposed node phase)
-    if (active && (!xi || P::NT)) {
+    if constexpr (P::PRE) {
+      // the eta lines finish their half of each node before handing it over:
+      // split source (dg_rhs.hpp:154-183) and the -1/J scaling, so the xi-line
+      // node phase (the longer one) is one FMA per component
+      if (active && !xi) {
+        mbar_wait(bar_node, ph_node);
+        double* acc = sm + P::ACC + el * P::EPAD;
+        const double* Nd = sm + P::NODE + (int)(((long long)e0 * NP) & 1) + el * NP;
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+          if (s < nk) {
+            const int q = li * N1 + k0 + s, qp = pidx(k0 + s);
+            const double ij = -1.0 / Nd[P::N_JAC * P::GNP + q], hg2 = 0.5 * g * h[s];
+            const long long n = (long long)e * NP + q;
+            const double sxv = P::kSxGlobal ? __ldg(M.sx + n) : Nd[P::N_SX * P::GNP + q];
+            const double syv = P::kSxGlobal ? __ldg(M.sy + n) : Nd[P::N_SY * P::GNP + q];
+            acc[0 * P::GPAD + qp] = r0[s] * ij;
+            acc[1 * P::GPAD + qp] = (r1[s] + hg2 * sxv) * ij;
+            acc[2 * P::GPAD + qp] = (r2[s] + hg2 * syv) * ij;
+            acc[3 * P::GPAD + qp] = ij;
+          }
+      }
+    }
+    if (active && (P::NT || (!P::PRE && !xi))) {
       double* acc = sm + (xi ? P::ACCX : P::ACC) + el * P::EPAD;
 #pragma unroll
       for (int s = 0; s < S; ++s)
@@ -835,12 +868,20 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
         const int k = k0 + s, q = k * N1 + li, qp = k * PAD + li;
         const long long n = (long long)e * NP + q;
         const double jac = Nd[P::N_JAC * P::GNP + q];
-        const double ij = -1.0 / jac, hg2 = 0.5 * g * h[s];
-        double rh = (acc[0 * P::GPAD + qp] + r0[s]) * ij;
-        const double sxv = P::kSxGlobal ? __ldg(M.sx + n) : Nd[P::N_SX * P::GNP + q];
-        const double syv = P::kSxGlobal ? __ldg(M.sy + n) : Nd[P::N_SY * P::GNP + q];
-        double rhu = (acc[1 * P::GPAD + qp] + r1[s] + hg2 * sxv) * ij;
-        double rhv = (acc[2 * P::GPAD + qp] + r2[s] + hg2 * syv) * ij;
+        double rh, rhu, rhv;
+        if constexpr (P::PRE) {
+          const double ij = acc[3 * P::GPAD + qp];  // -1/J from the eta line
+          rh = __fma_rn(r0[s], ij, acc[0 * P::GPAD + qp]);
+          rhu = __fma_rn(r1[s], ij, acc[1 * P::GPAD + qp]);
+          rhv = __fma_rn(r2[s], ij, acc[2 * P::GPAD + qp]);
+        } else {
+          const double ij = -1.0 / jac, hg2 = 0.5 * g * h[s];
+          const double sxv = P::kSxGlobal ? __ldg(M.sx + n) : Nd[P::N_SX * P::GNP + q];
+          const double syv = P::kSxGlobal ? __ldg(M.sy + n) : Nd[P::N_SY * P::GNP + q];
+          rh = (acc[0 * P::GPAD + qp] + r0[s]) * ij;
+          rhu = (acc[1 * P::GPAD + qp] + r1[s] + hg2 * sxv) * ij;
+          rhv = (acc[2 * P::GPAD + qp] + r2[s] + hg2 * syv) * ij;
+        }
         if (FORCE) {
           rh += A.fh[n];
           rhu += A.fhu[n];
