@@ -143,3 +143,37 @@ def test_distributed_dt_matches():
 
     dt = compute_dt_distributed(bs[0], MinEx(bs), 0.5, m.degree, cfg.phys)
     assert dt == ref.compute_dt(m, p, st, 0.5)
+
+
+def test_visc_interior_pass_touches_only_its_range():
+    """The interior viscous pre-pass (run during the state exchange) computes eps and
+    the flux pairs of the interior range only; the halo-adjacent elements keep their
+    previous values until the boundary pass (a pre-kernel that ignored the range would
+    redo, and for the boundary elements miscompute, the whole partition)."""
+    sid, kx, deg, P = "wetdry_dambreak", 12, 3, 2
+    m, st = ref.scenario_mesh(sid, kx, kx, deg)
+    p, _ = scenario_params(sid, deg)
+    lm = part.local_mesh(m, P, 0)
+    b = GpuPartition(lm, cfg_from(p, swdg.MODE_FAST))
+    lo, hi = part.interior_range(lm.faces, lm.n_owned)
+    lo, hi = (lo + 1) & ~1, hi & ~1  # swdg_gpu_set_interior's even bounds
+    assert hi - lo >= 2 and (lo > 0 or hi < lm.n_owned)
+    n = lm.n_elem * lm.n1 * lm.n1
+    lake = [np.full(n, 2.0), np.zeros(n), np.zeros(n)]  # no modal energy: eps = 0
+    rough = random_state(n, np.random.default_rng(5))
+    b.upload(lake)
+    b.step_begin()
+    b.stage_visc(0, 0.0, 1e-4)
+    assert not b.integ.last_eps()[: lm.n_owned].any()
+    b.upload(rough)
+    b.step_begin()
+    b.stage_visc_part(0, 0.0, 1e-4, 1)  # interior only
+    e1 = b.integ.last_eps()[: lm.n_owned]
+    outside = np.r_[0:lo, hi:lm.n_owned]
+    assert e1[lo:hi].any()
+    assert not e1[outside].any()
+    b.stage_visc_part(0, 0.0, 1e-4, 2)  # the rest
+    e2 = b.integ.last_eps()[: lm.n_owned]
+    b.step_begin()
+    b.stage_visc(0, 0.0, 1e-4)  # everything at once
+    assert beq([e2], [b.integ.last_eps()[: lm.n_owned]])
