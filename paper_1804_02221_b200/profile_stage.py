@@ -46,11 +46,14 @@ def main():
         import time
         reps = a.time
         t0 = time.perf_counter()
-        integ.run_steps(reps, 0.0, dt)  # ends with a flag read (host sync)
+        # ends with a flag read (host sync); with --diag every step also runs the
+        # per-step reductions
+        integ.run_steps(reps, 0.0, dt, reductions=a.diag)
         el = time.perf_counter() - t0
         dofs = 3 * integ.mesh.n_nodes
-        print(f"N={N} kx={a.kx} visc={a.viscous} stage_ms={el / reps / 3 * 1e3:.3f} "
-              f"dof_per_s={dofs * reps * 3 / el:.4e} accepted={integ.last_info().accepted}")
+        print(f"N={N} kx={a.kx} visc={a.viscous} diag={a.diag} stage_ms={el / reps / 3 * 1e3:.3f} "
+              f"step_ms={el / reps * 1e3:.3f} dof_per_s={dofs * reps * 3 / el:.4e} "
+              f"accepted={integ.last_info().accepted}")
     else:
         print("ok", integ.last_info().accepted, integ.launch_count())
 
