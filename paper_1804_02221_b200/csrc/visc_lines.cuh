@@ -42,11 +42,16 @@ struct VLP {
   // line threads (each is used by one direction only): 12 instead of 16 fields
   // per node, so more CTAs share an SM
   enum { H, U, V, TMP, XU1, XU2, XV1, XV2, EU1, EU2, EV1, EV2, kF };
-  // asynchronous (LDGSTS) staging, measured (viscous ms/stage, pre-kernel +
-  // stage): N=10 14.94 -> 13.67, N=12 22.44 -> 20.80; slower at N+1 = 8 (6.24
-  // synchronous vs 6.32-6.37) and N+1 = 5 (2.57 -> 2.80)
+  // asynchronous (LDGSTS) staging of the state from N+1 = 4 on (measured with the
+  // metrics out of shared memory: viscous N=3..6 1-4% faster than synchronous
+  // staging, neutral at 7, 8, profiles/r02_ab_visc_pre_staging.txt; with the
+  // metrics staged too it had measured slower at N+1 <= 8); N+1 = 3 stages
+  // synchronously with every node's loads issued first (N=2 0.957 -> 0.931)
+#ifndef VL_SYNC_BATCH
+#define VL_SYNC_BATCH 1
+#endif
 #ifndef VL_ASYNC_MIN
-#define VL_ASYNC_MIN 9
+#define VL_ASYNC_MIN 4
 #endif
   static constexpr bool kAsync = N1 >= VL_ASYNC_MIN;
   static constexpr int RED = kF * GPAD;             // [E][PMAX][4] shell-energy pieces
@@ -142,8 +147,32 @@ __global__ void __launch_bounds__(VLP<N1>::THREADS)
       d[P::U * GP] = u;
       d[P::V * GP] = v;
     }
+  } else if constexpr (VL_SYNC_BATCH) {
+    // stage the group's state (+ velocities), one thread per node: every node's
+    // loads issued before the first velocity (one memory round trip per CTA)
+    double th[R], thu[R], thv[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int r = tid + k * P::THREADS;
+      const long long n = base + (r < ne * NP ? r : 0);
+      th[k] = __ldg(S.h + n);
+      thu[k] = __ldg(S.hu + n);
+      thv[k] = __ldg(S.hv + n);
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int r = tid + k * P::THREADS;
+      if (r >= ne * NP) break;
+      const int el2 = r / NP, q = r - el2 * NP, i = q / N1, j = q - i * N1;
+      double* d = sm + el2 * P::EPAD + i * PAD + j;
+      double u, v;
+      vel(th[k], thu[k], thv[k], h_des, u, v);
+      d[P::H * GP] = th[k];
+      d[P::U * GP] = u;
+      d[P::V * GP] = v;
+    }
   } else {
-    // stage the group's state (+ velocities) and metrics, one thread per node
+    // stage the group's state (+ velocities), one thread per node
     for (int r = tid; r < ne * NP; r += P::THREADS) {
       const int el2 = r / NP, q = r - el2 * NP, i = q / N1, j = q - i * N1;
       double* d = sm + el2 * P::EPAD + i * PAD + j;
