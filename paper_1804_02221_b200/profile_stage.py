@@ -16,6 +16,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--degree", type=int, default=7)
     ap.add_argument("--kx", type=int, default=200)
+    ap.add_argument("--ky", type=int, default=0, help="elements in y (default: kx)")
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--viscous", action="store_true")
     ap.add_argument("--exact", action="store_true")
@@ -30,7 +31,7 @@ def main():
         visc = swdg.ViscosityConfig(True, 0.1, smin, smax)
     cfg = swdg.RunConfig(phys=swdg.PhysicsParams(9.81), visc=visc,
                          mode=swdg.MODE_EXACT if a.exact else swdg.MODE_FAST)
-    spec = swdg.structured_spec("wavy", N, a.kx, a.kx, periodic_x=True, periodic_y=True,
+    spec = swdg.structured_spec("wavy", N, a.kx, a.ky or a.kx, periodic_x=True, periodic_y=True,
                                 bathy="smooth")
     integ = swdg.TimeIntegrator.structured(spec, cfg)
     x, y = integ.geometry("x"), integ.geometry("y")
