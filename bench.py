@@ -272,14 +272,15 @@ def measure_gpu(N: int, steps: int, warmup: int, viscous: bool, rank: int, world
 
 
 def measure_gpu_distributed(N: int, steps: int, warmup: int, viscous: bool, rank: int,
-                            world: int, e2e_steps: int = 2):
+                            world: int, e2e_steps: int = 2, halo: str = "nccl"):
     """Strong scaling over `world` ranks (one GPU each) of the same 1M-element mesh:
     rank r owns a band of element rows, generates its owned + ghost geometry on its
-    device, and exchanges face-trace halos with NCCL between stages."""
+    device, and exchanges face-trace halos between stages: NCCL point-to-point, or
+    (halo="ipc") direct peer-memory stores through CUDA IPC."""
     import numpy as np
     import torch
     from paper_1804_02221_b200 import swdg
-    from paper_1804_02221_b200.distributed import (GpuPartition, TorchExchanger,
+    from paper_1804_02221_b200.distributed import (GpuPartition, IpcExchanger, TorchExchanger,
                                                    compute_dt_distributed, run_steps_distributed,
                                                    try_step_distributed)
 
@@ -296,7 +297,7 @@ def measure_gpu_distributed(N: int, steps: int, warmup: int, viscous: bool, rank
         hbuf.numpy()[:] = val
     st = swdg.State(*(hb.numpy() for hb in host))
     integ.upload(st)
-    ex = TorchExchanger(b, "cuda")
+    ex = IpcExchanger(b) if halo == "ipc" else TorchExchanger(b, "cuda")
     dt = 0.1 * compute_dt_distributed(b, ex, 0.5, N, cfg.phys)
     run_steps_distributed(b, ex, warmup, 0.0, dt)
     torch.distributed.barrier()
@@ -422,6 +423,8 @@ def main():
                     help="skip the N=1..15 sweep (single GPU)")
     ap.add_argument("--distributed", action="store_true",
                     help="use the partitioned (NCCL halo) path even on one GPU")
+    ap.add_argument("--halo", default="nccl", choices=["nccl", "ipc"],
+                    help="partitioned path: halo exchange by NCCL or by CUDA IPC peer stores")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -480,8 +483,10 @@ def main():
                 os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29531", RANK="0",
                                   WORLD_SIZE="1")
             torch.distributed.init_process_group("nccl")
-        r = measure_gpu_distributed(N, args.steps, args.warmup, args.viscous, rank, world)
-        config.update(parallelism=f"element partition over {world} GPU(s), NCCL halos",
+        r = measure_gpu_distributed(N, args.steps, args.warmup, args.viscous, rank, world,
+                                    halo=args.halo)
+        config.update(parallelism=f"element partition over {world} GPU(s), "
+                                  f"{'CUDA IPC peer-memory' if args.halo == 'ipc' else 'NCCL'} halos",
                       scaling="strong: the same 1M-element mesh for every N")
     else:
         r = measure_gpu(N, args.steps, args.warmup, args.viscous, rank, world)
@@ -538,7 +543,7 @@ def main():
         "gpu_launches": r["launches"],
         "e2e": {"value": (1 if distributed else world) * 3 * r["dofs"] / r["e2e_s"], "unit": UNIT,
                 "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"],
-                "path": ("per rank: swdg_gpu_upload_state + split-step C ABI with NCCL halos + "
+                "path": ("per rank: swdg_gpu_upload_state + split-step C ABI with halo exchanges + "
                          "download (pinned)") if distributed else
                         (f"driver.run_simulation_device, {r['e2e_steps']} steps: state uploaded "
                          "from pinned memory once, per step one swdg_gpu_step_device (3 stages + "

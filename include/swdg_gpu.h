@@ -305,6 +305,23 @@ int swdg_gpu_halo_setup(swdg_gpu* ctx, int64_t n_send, const int32_t* send_idx, 
                         const int32_t* recv_idx);
 int swdg_gpu_halo_pack(swdg_gpu* ctx, int what, int stage, double* send_buf);
 int swdg_gpu_halo_unpack(swdg_gpu* ctx, int what, int stage, const double* recv_buf);
+/* Direct peer-memory halo exchange (no NCCL): every rank owns a mailbox in
+ * device memory exported through CUDA IPC (ipc_alloc: zeroed, 64-byte
+ * cudaIpcMemHandle_t out) and maps its peers' (ipc_open; NVLink / NVSwitch
+ * between GPUs, plain device memory between processes sharing one GPU).
+ * halo_push packs send entries [first, first+count) of `what` (as halo_pack)
+ * straight into `dst` (a peer's mailbox slot) and then stores `seq` to `flag`
+ * (the peer's flag for this rank) with a system-scope release.  halo_wait
+ * queues a device-side wait until each of the n flags (this rank's mailbox)
+ * reaches seq -- no host synchronisation; after timeout_s it gives up and
+ * halo_status reports it (synchronises the stream; clears the report). */
+int swdg_gpu_ipc_alloc(swdg_gpu* ctx, int64_t bytes, void** dptr, void* handle);
+int swdg_gpu_ipc_open(swdg_gpu* ctx, const void* handle, void** dptr);
+int swdg_gpu_halo_push(swdg_gpu* ctx, int what, int stage, int64_t first, int64_t count,
+                       double* dst, uint64_t* flag, uint64_t seq);
+int swdg_gpu_halo_wait(swdg_gpu* ctx, const uint64_t* flags, int32_t n, uint64_t seq,
+                       double timeout_s);
+int swdg_gpu_halo_status(swdg_gpu* ctx, int32_t* timed_out);
 int swdg_gpu_dt_candidates(swdg_gpu* ctx, double* dt_min, double* min_len);
 int swdg_gpu_step_begin(swdg_gpu* ctx);
 int swdg_gpu_stage_visc(swdg_gpu* ctx, int stage, double t, double dt);

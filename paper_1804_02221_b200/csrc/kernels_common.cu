@@ -45,7 +45,71 @@ __global__ void k_halo_unpack(const int* idx, long long n, int nf, double* f0, d
   if (nf > 3) f3[k] = buf[i * nf + 3];
 }
 
+// direct peer-memory exchange: pack straight into the receiving rank's mailbox
+// (a CUDA IPC mapping: NVLink / NVSwitch stores between GPUs), then raise the
+// receiver's sequence flag with a system-scope release once every block of the
+// pack has finished (stream order + the fences)
+__global__ void k_halo_push(const int* idx, long long n, int nf, const double* f0,
+                            const double* f1, const double* f2, const double* f3, double* dst) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) {
+    const long long k = idx[i];
+    dst[i * nf + 0] = f0[k];
+    dst[i * nf + 1] = f1[k];
+    dst[i * nf + 2] = f2[k];
+    if (nf > 3) dst[i * nf + 3] = f3[k];
+  }
+  __threadfence_system();
+}
+
+__global__ void k_flag_release(unsigned long long* flag, unsigned long long seq) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(seq) : "memory");
+}
+
+// the receiver: one lane per peer polls its flag (system-scope acquire) until the
+// peer's data of exchange `seq` has landed; a peer that never arrives sets *err
+// after timeout_ns instead of hanging the stream
+__global__ void k_flags_wait(const unsigned long long* flags, int n, unsigned long long seq,
+                             unsigned long long timeout_ns, int* err) {
+  const int i = threadIdx.x;
+  if (i < n) {
+    unsigned long long t0, t, v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (true) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + i) : "memory");
+      if (v >= seq) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > timeout_ns) {
+        atomicExch(err, 1);
+        break;
+      }
+      __nanosleep(256);
+    }
+  }
+  __syncthreads();
+}
+
 }  // namespace
+
+int launch_halo_push(const int* idx, long long n, int nf, const double* const* f, double* dst,
+                     unsigned long long* flag, unsigned long long seq, cudaStream_t st) {
+  int launches = 0;
+  if (n > 0) {
+    k_halo_push<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(idx, n, nf, f[0], f[1], f[2],
+                                                            nf > 3 ? f[3] : f[0], dst);
+    ++launches;
+  }
+  k_flag_release<<<1, 1, 0, st>>>(flag, seq);
+  return launches + 1;
+}
+
+int launch_flags_wait(const unsigned long long* flags, int n, unsigned long long seq,
+                      unsigned long long timeout_ns, int* err, cudaStream_t st) {
+  if (n <= 0) return 0;
+  k_flags_wait<<<1, ((n + 31) / 32) * 32, 0, st>>>(flags, n, seq, timeout_ns, err);
+  return 1;
+}
 
 int launch_halo_pack(const int* idx, long long n, int nf, const double* const* f, double* buf,
                      cudaStream_t st) {

@@ -76,6 +76,8 @@ struct swdg_gpu {
   bool fast = false;   // fused fast stage kernel in use
 
   std::vector<void*> allocations;
+  std::vector<void*> ipc_opened;  // peer mailboxes mapped by swdg_gpu_ipc_open
+  int* ipc_err = nullptr;         // set by a flag wait that timed out
   double* geo = nullptr;   // 8 nodal + 4 face arrays
   double* xy = nullptr;    // device x,y (structured meshes)
   double* W[3] = {};       // current state
@@ -138,6 +140,7 @@ struct swdg_gpu {
     return static_cast<T*>(p);
   }
   ~swdg_gpu() {
+    for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     for (void* p : allocations) cudaFree(p);
     if (rep_h) cudaFreeHost(rep_h);
     if (copy_stream) cudaStreamDestroy(copy_stream);
@@ -1346,6 +1349,84 @@ int swdg_gpu_halo_unpack(swdg_gpu* c, int what, int k, const double* recv_buf) {
     }
     c->launches += launched(launch_halo_unpack(c->recv_idx, c->n_recv, what ? 4 : 3, f, recv_buf,
                                       c->stream), "launch_halo_unpack");
+    return SWDG_OK;
+  });
+}
+
+// ---- direct peer-memory halo exchange (CUDA IPC) --------------------------
+
+int swdg_gpu_ipc_alloc(swdg_gpu* c, int64_t bytes, void** dptr, void* handle) {
+  return guarded(c, [&] {
+    if (bytes <= 0 || !dptr || !handle) throw InputError{"ipc_alloc: bad arguments"};
+    char* p = c->dalloc<char>((size_t)bytes);
+    ck(cudaMemset(p, 0, (size_t)bytes), "ipc_alloc memset");
+    cudaIpcMemHandle_t h;
+    ck(cudaIpcGetMemHandle(&h, p), "cudaIpcGetMemHandle");
+    std::memcpy(handle, &h, sizeof h);
+    *dptr = p;
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_ipc_open(swdg_gpu* c, const void* handle, void** dptr) {
+  return guarded(c, [&] {
+    if (!handle || !dptr) throw InputError{"ipc_open: bad arguments"};
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    void* p = nullptr;
+    ck(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    c->ipc_opened.push_back(p);
+    *dptr = p;
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_halo_push(swdg_gpu* c, int what, int k, int64_t first, int64_t count, double* dst,
+                       uint64_t* flag, uint64_t seq) {
+  return guarded(c, [&] {
+    if (k < 0 || k > 2 || what < 0 || what > 1) throw InputError{"halo_push: bad stage/what"};
+    if (what == 1 && !c->fvu) throw InputError{"halo_push: viscosity is off"};
+    if (first < 0 || count < 0 || first + count > c->n_send) throw InputError{"halo_push: bad range"};
+    if (!flag || (count > 0 && !dst)) throw InputError{"halo_push: null destination"};
+    double* const* in = stage_input(c, k);
+    const double* f[4] = {in[0], in[1], in[2], nullptr};
+    if (what == 1) {
+      f[0] = c->fvu;
+      f[1] = c->fvv;
+      f[2] = c->gvu;
+      f[3] = c->gvv;
+    }
+    c->launches += launched(launch_halo_push(c->send_idx + first, count, what ? 4 : 3, f, dst,
+                                             reinterpret_cast<unsigned long long*>(flag), seq,
+                                             c->stream), "launch_halo_push");
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_halo_wait(swdg_gpu* c, const uint64_t* flags, int32_t n, uint64_t seq,
+                       double timeout_s) {
+  return guarded(c, [&] {
+    if (n < 0 || (n > 0 && !flags)) throw InputError{"halo_wait: bad arguments"};
+    if (!c->ipc_err) {
+      c->ipc_err = c->dalloc<int>(1);
+      ck(cudaMemset(c->ipc_err, 0, sizeof(int)), "ipc_err");
+    }
+    const unsigned long long tns = (unsigned long long)(std::max(timeout_s, 1e-3) * 1e9);
+    c->launches += launched(launch_flags_wait(reinterpret_cast<const unsigned long long*>(flags), n,
+                                              seq, tns, c->ipc_err, c->stream), "launch_flags_wait");
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_halo_status(swdg_gpu* c, int32_t* timed_out) {
+  return guarded(c, [&] {
+    int v = 0;
+    if (c->ipc_err) {
+      ck(cudaStreamSynchronize(c->stream), "halo_status sync");
+      ck(cudaMemcpy(&v, c->ipc_err, sizeof(int), cudaMemcpyDeviceToHost), "halo_status");
+      if (v) ck(cudaMemset(c->ipc_err, 0, sizeof(int)), "halo_status reset");
+    }
+    *timed_out = v;
     return SWDG_OK;
   });
 }

@@ -73,6 +73,10 @@ int launch_limiter_entropy(const Mesh& M, const Phys& P, const StageArgs& A, con
 extern int g_grid_cap;
 
 // mode-independent (kernels_common.cu)
+int launch_halo_push(const int* idx, long long n, int nf, const double* const* f, double* dst,
+                     unsigned long long* flag, unsigned long long seq, cudaStream_t st);
+int launch_flags_wait(const unsigned long long* flags, int n, unsigned long long seq,
+                      unsigned long long timeout_ns, int* err, cudaStream_t st);
 int launch_halo_pack(const int* idx, long long n, int nf, const double* const* f, double* buf,
                      cudaStream_t st);
 int launch_halo_unpack(const int* idx, long long n, int nf, double* const* f, const double* buf,

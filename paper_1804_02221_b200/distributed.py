@@ -11,7 +11,8 @@ GPU, face-trace halos exchanged between stages, one flag reduction per step.
 
 The stepping logic is backend-agnostic: `GpuPartition` drives the sm_100a kernels
 through the split-step C ABI; tests drive the same loop with the CPU oracle.  The
-exchanger is torch.distributed (NCCL between GPUs, gloo on CPU) or an in-process
+exchanger is torch.distributed point-to-point (NCCL between GPUs, gloo on CPU),
+direct peer-memory stores through CUDA IPC (`IpcExchanger`), or an in-process
 loopback for several partitions in one process.
 """
 from __future__ import annotations
@@ -111,6 +112,89 @@ class TorchExchanger:
         t = torch.tensor(vals, dtype=torch.float64, device=self.send.device)
         out = [torch.empty_like(t) for _ in range(torch.distributed.get_world_size())]
         torch.distributed.all_gather(out, t)
+        return [o.tolist() for o in out]
+
+
+class IpcExchanger:
+    """Halo exchange through peer memory, no NCCL: every rank exports a mailbox
+    (two receive slots -- exchanges alternate between them -- and one sequence
+    flag per peer) by CUDA IPC and maps its peers'.  `start` queues, per peer, one
+    kernel that packs this rank's send entries straight into the peer's slot (NVLink
+    / NVSwitch stores between GPUs) and then raises this rank's flag there;
+    `finish` queues a device-side wait on this rank's own flags and the unpack from
+    its slot.  Both are stream-ordered with the stage kernels: no host
+    synchronisation and no separate communication stream per exchange, and the
+    interior stage kernel queued between them overlaps the transfer.  Slot reuse is
+    safe without acknowledgements: a rank writes slot s&1 of exchange s only after
+    its wait for exchange s-1 saw the peer's flag, which the peer raised after
+    unpacking exchange s-2 (its own stream order).  torch.distributed (any backend,
+    CPU tensors) carries the setup and the per-step reductions.  Ranks may share a
+    GPU (the mapping is then plain device memory of the other process)."""
+
+    def __init__(self, backend: "GpuPartition", timeout_s: float = 30.0):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.b = backend
+        self.timeout_s = timeout_s
+        plan = backend.plan
+        self.peers = list(plan.peers)
+        self.soff, ns = _offsets(plan, "send_idx")
+        self.roff, nr = _offsets(plan, "recv_idx")
+        self.slot = max(nr, 1) * 4  # doubles per receive slot
+        nflag = max(len(self.peers), 1)
+        self.base, handle = backend.ipc_alloc((2 * self.slot + nflag) * 8)
+        self.flags = self.base + 2 * self.slot * 8
+        me = dist.get_rank()
+        info = dict(handle=handle, slot=self.slot,
+                    at={p: (self.roff[p][0], self.roff[p][1], j) for j, p in enumerate(self.peers)})
+        allinfo = [None] * dist.get_world_size()
+        dist.all_gather_object(allinfo, info)
+        self.dst, self.flag_at = {}, {}
+        for p in self.peers:
+            o, n, j = allinfo[p]["at"][me]
+            assert n == self.soff[p][1], "halo plans disagree between ranks"
+            base = backend.ipc_open(allinfo[p]["handle"])
+            self.dst[p] = (base, allinfo[p]["slot"], o)
+            self.flag_at[p] = base + (2 * allinfo[p]["slot"] + j) * 8
+        self.seq = 0
+
+    def start(self, what: int, k: int):
+        self.seq += 1
+        s, nf = self.seq & 1, (4 if what else 3)
+        for p in self.peers:
+            base, slot, o = self.dst[p]
+            first, n = self.soff[p]
+            self.b.push(what, k, first, n, base + (s * slot + o * nf) * 8, self.flag_at[p],
+                        self.seq)
+        return what, k, self.seq
+
+    def finish(self, handle):
+        what, k, seq = handle
+        self.b.wait_flags(self.flags, len(self.peers), seq, self.timeout_s)
+        self.b.unpack_at(what, k, self.base + (seq & 1) * self.slot * 8)
+
+    def exchange(self, what: int, k: int):
+        self.finish(self.start(what, k))
+
+    def _check(self):
+        if self.b.halo_timed_out():
+            raise RuntimeError("peer-memory halo exchange timed out (a peer never raised its flag)")
+
+    def all_max(self, vals):
+        self._check()
+        t = self.torch.tensor(vals, dtype=self.torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return t.tolist()
+
+    def all_min(self, vals):
+        return [-v for v in self.all_max([-v for v in vals])]
+
+    def all_gather(self, vals):
+        self._check()
+        t = self.torch.tensor(vals, dtype=self.torch.float64)
+        out = [self.torch.empty_like(t) for _ in range(self.dist.get_world_size())]
+        self.dist.all_gather(out, t)
         return [o.tolist() for o in out]
 
 
@@ -354,7 +438,15 @@ class GpuPartition(Backend):
                            ("swdg_gpu_step_flags", [vp, i32p, i32p]),
                            ("swdg_gpu_step_commit", [vp, C.c_int, C.POINTER(swdg.StepInfoC)]),
                            ("swdg_gpu_dt_candidates", [vp, C.POINTER(C.c_double),
-                                                       C.POINTER(C.c_double)])):
+                                                       C.POINTER(C.c_double)]),
+                           ("swdg_gpu_ipc_alloc", [vp, C.c_int64, C.POINTER(C.c_void_p),
+                                                   C.c_void_p]),
+                           ("swdg_gpu_ipc_open", [vp, C.c_void_p, C.POINTER(C.c_void_p)]),
+                           ("swdg_gpu_halo_push", [vp, C.c_int, C.c_int, C.c_int64, C.c_int64,
+                                                   C.c_void_p, C.c_void_p, C.c_uint64]),
+                           ("swdg_gpu_halo_wait", [vp, C.c_void_p, C.c_int32, C.c_uint64,
+                                                   C.c_double]),
+                           ("swdg_gpu_halo_status", [vp, i32p])):
             f = getattr(L, name)
             f.restype = C.c_int
             f.argtypes = args
@@ -411,6 +503,32 @@ class GpuPartition(Backend):
 
     def unpack(self, what, k, buf):
         self._chk(self.L.swdg_gpu_halo_unpack(self.integ._h, what, k, C.c_void_p(buf.data_ptr())))
+
+    def unpack_at(self, what, k, ptr: int):
+        self._chk(self.L.swdg_gpu_halo_unpack(self.integ._h, what, k, C.c_void_p(ptr)))
+
+    # direct peer-memory exchange (IpcExchanger)
+    def ipc_alloc(self, nbytes: int):
+        p, h = C.c_void_p(), (C.c_char * 64)()
+        self._chk(self.L.swdg_gpu_ipc_alloc(self.integ._h, nbytes, C.byref(p), h))
+        return p.value, bytes(h)
+
+    def ipc_open(self, handle: bytes) -> int:
+        p, h = C.c_void_p(), (C.c_char * 64).from_buffer_copy(handle)
+        self._chk(self.L.swdg_gpu_ipc_open(self.integ._h, h, C.byref(p)))
+        return p.value
+
+    def push(self, what, k, first, count, dst: int, flag: int, seq: int):
+        self._chk(self.L.swdg_gpu_halo_push(self.integ._h, what, k, first, count,
+                                            C.c_void_p(dst), C.c_void_p(flag), seq))
+
+    def wait_flags(self, flags: int, n: int, seq: int, timeout_s: float):
+        self._chk(self.L.swdg_gpu_halo_wait(self.integ._h, C.c_void_p(flags), n, seq, timeout_s))
+
+    def halo_timed_out(self) -> bool:
+        v = C.c_int32()
+        self._chk(self.L.swdg_gpu_halo_status(self.integ._h, C.byref(v)))
+        return bool(v.value)
 
     def stage_visc(self, k, t, dt):
         self._chk(self.L.swdg_gpu_stage_visc(self.integ._h, k, t, dt))

@@ -1,0 +1,96 @@
+"""Two processes exchanging halos through peer memory (IpcExchanger: CUDA IPC
+mailboxes, device-side flags, no NCCL) reproduce the single-GPU run.  Both ranks
+share cuda:0 (one B200 per gpurun box): the same kernels, handles and flags as
+between GPUs, the stores landing in the other process's device memory instead of
+crossing NVLink.  Exact mode bitwise (hence the reference); fast mode bitwise
+against the single-GPU fast run, as for the in-process partitions."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from oracle import ref
+from tests.conftest import gpu_available
+from tests.helpers import beq, scenario_params
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device"),
+              pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")]
+
+
+def _cfg(p, mode):
+    from paper_1804_02221_b200 import swdg
+    return swdg.RunConfig(phys=swdg.PhysicsParams(p.g, p.h_tol, p.h_des, p.h_ref),
+                          visc=swdg.ViscosityConfig(bool(p.visc_enabled), p.epsilon0,
+                                                    p.sigma_min, p.sigma_max),
+                          limiter_enabled=bool(p.limiter_enabled), mode=mode)
+
+
+def _worker(rank, world, port_no, scen, mode, steps, path):
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port_no}", rank=rank,
+                            world_size=world)
+    from paper_1804_02221_b200 import partition as part
+    from paper_1804_02221_b200.distributed import (GpuPartition, IpcExchanger,
+                                                   step_report_distributed,
+                                                   try_step_distributed)
+    sid, k, N, visc = scen
+    m, st = ref.scenario_mesh(sid, k, k, N)
+    p, c = scenario_params(sid, N, **({} if visc else {"visc_enabled": 0.0}))
+    lm = part.local_mesh(m, world, rank)
+    b = GpuPartition(lm, _cfg(p, mode), device=0)
+    b.upload(part.scatter_state(st, lm))
+    ex = IpcExchanger(b, timeout_s=20.0)
+    dt = ref.compute_dt(m, p, st, c["cfl"])
+    acc, reps = [], []
+    for s in range(steps):
+        acc.append(try_step_distributed(b, ex, s * dt, dt))
+        reps.append(step_report_distributed(b, ex) if acc[-1] else None)
+    np_ = lm.n1 * lm.n1
+    mine = np.stack([w[: lm.n_owned * np_] for w in b.download()])
+    out = [None] * world
+    dist.all_gather_object(out, (lm.global_ids[: lm.n_owned].tolist(), mine, acc, reps,
+                                 b.has_interior, ex.seq))
+    if rank == 0:
+        np.save(path, np.array(out, dtype=object), allow_pickle=True)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("scen", [("wetdry_dambreak", 12, 3, True),
+                                  ("oscillating_lake", 16, 4, False)])
+def test_two_processes_peer_memory_halo(tmp_path, mode, scen):
+    import torch.multiprocessing as mp
+    from paper_1804_02221_b200 import swdg
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port_no = s.getsockname()[1]
+    path = os.path.join(tmp_path, "res.npy")
+    steps = 4
+    mp.spawn(_worker, args=(2, port_no, scen, mode, steps, path), nprocs=2, join=True)
+    res = np.load(path, allow_pickle=True)
+    sid, k, N, visc = scen
+    m, st = ref.scenario_mesh(sid, k, k, N)
+    p, c = scenario_params(sid, N, **({} if visc else {"visc_enabled": 0.0}))
+    single = swdg.TimeIntegrator(m, _cfg(p, mode))
+    dt = ref.compute_dt(m, p, st, c["cfl"])
+    want = swdg.State(*[a.copy() for a in st])
+    acc_ref = [single.try_step(want, s * dt, dt) for s in range(steps)]
+    np_ = m.n1 * m.n1
+    got = [np.zeros(m.n_nodes) for _ in range(3)]
+    for gids, mine, acc, reps, has_interior, seq in res:
+        assert acc == acc_ref
+        assert has_interior  # the overlapped schedule (interior during the exchange) ran
+        # state exchange per stage (+ flux pairs when viscous) + one per step report
+        assert seq == steps * 3 * (2 if visc else 1) + sum(acc)
+        sel = (np.array(gids)[:, None] * np_ + np.arange(np_)).ravel()
+        for j in range(3):
+            got[j][sel] = mine[j]
+    assert beq(got, want.arrays())
+    d = single.diagnostics(want)
+    last = res[0][3][-1]
+    assert last["min_h"] == d.min_h
+    assert abs(last["mass"] - d.mass) <= 1e-13 * abs(d.mass)
