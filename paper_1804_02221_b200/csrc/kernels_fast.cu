@@ -85,6 +85,10 @@
 #define SWDG_HL_PRE_VMIN 16  // measured: viscous N=15 44.4 -> 40.1 ms/stage; N+1 = 13..15 1-4% slower
 #endif
 
+#ifndef SWDG_HL_XROLL
+#define SWDG_HL_XROLL 0  // > 0: roll the streamed-node loops from this N+1 on (A/B)
+#endif
+
 namespace swdg_dev {
 
 namespace {
@@ -505,6 +509,17 @@ __device__ __forceinline__ void hl_node_phase_t(double* sm, const Mesh& M, const
 // faster at N+1 = 10); above, a 168-register cap spills (N+1 = 11, 13..16)
 // The viscous variant keeps 3 at N+1 = 6, 7 (measured: N=5 3.566 vs 3.721, N=6
 // 5.180 vs 5.547 ms/stage with 4) and takes 4 at N+1 = 5 (2.777 -> 2.559).
+// streamed-node loops rolled (1) or unrolled (0) per configuration, measured
+// (ms/stage, 1M elements, profiles/r02_ab_hl_roll.txt): inviscid N+1 = 6 1.461 ->
+// 1.444, 7 2.365 -> 2.111, 10 4.440 -> 4.351; viscous N+1 = 8 6.02 -> 5.89,
+// 9 8.51 -> 7.79, 10 11.56 -> 10.87, 14 25.2 -> 24.6, 15 33.2 -> 31.2, 16 39.8 ->
+// 38.9; slower or neutral elsewhere (inviscid N+1 = 9: 4.36 -> 4.53, 12: 7.47 ->
+// 7.84, 16: 13.6 -> 14.1).  SWDG_HL_XROLL > 0 rolls every N+1 >= it (A/B builds).
+__host__ __device__ constexpr bool hl_roll(int n1, bool visc) {
+  return SWDG_HL_XROLL > 0 ? n1 >= SWDG_HL_XROLL
+         : visc ? (n1 >= 8 && n1 <= 10) || n1 >= 14 : (n1 == 6 || n1 == 7 || n1 == 10);
+}
+
 __host__ __device__ constexpr int hl_min_blocks(int n1, bool visc) {
   return n1 == 5 ? SWDG_HL_MB5 : (n1 == 6 && !visc) ? SWDG_HL_MB6
          : (n1 == 7 && !visc) ? SWDG_HL_MB7 : n1 <= 10 ? 3 : 1;
@@ -641,8 +656,13 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
     // exchange slots are slot-major ([XS][LP]): consecutive lanes, consecutive words
     double* xch_base = sm + P::XCH + line;
     auto xch = [&](int slot) -> double& { return xch_base[slot * P::LP]; };
+    // the streamed-node loops stay rolled where that measured faster (hl_roll: less
+    // code for the instruction cache, fewer live registers; the inner loops over the
+    // register-held half stay unrolled, the operator entries become warp-uniform
+    // constant loads)
+    constexpr int XU = hl_roll(N1, VISC) ? 1 : 32;
     if (part == 0) {
-#pragma unroll
+#pragma unroll(XU)
       for (int s = 0; s < NB0; ++s) {
         const int q = pidx(H + s);
         const double hb = Lb[P::F_H * P::GPAD + q], hub = Lb[P::F_HU * P::GPAD + q],
@@ -669,7 +689,7 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
         xch(3 * s + 2) = c2;
       }
     } else {
-#pragma unroll
+#pragma unroll(XU)
       for (int a = 0; a < H; ++a) {
         const int q = pidx(a);
         const double ha = Lb[P::F_H * P::GPAD + q], hua = Lb[P::F_HU * P::GPAD + q],
