@@ -114,7 +114,6 @@ __device__ __forceinline__ int next_group(int* ctr, int grp) {
 template <int N1, bool V = false>
 struct HL {
   static constexpr bool kVisc = V;
-  static constexpr bool NT_ = !V && N1 == 9;  // transposed node phase (see NT)
   static constexpr int NP = N1 * N1, LE = 2 * N1;
   static constexpr int H = (N1 + 1) / 2, NB = N1 - H;
   static constexpr int work_x(int b0) { return H * (H - 1) / 2 + H * b0; }
@@ -188,27 +187,18 @@ struct HL {
   static constexpr int ACC = LINE + NBUF * LBUF;
   // eta-line hand-over: 3 accumulators, plus -1/J (PRE: the eta lines apply the
   // source and -1/J to their half before handing over)
-  static constexpr bool PRE = !NT_ && V && N1 >= SWDG_HL_PRE_VMIN;
+  static constexpr bool PRE = V && N1 >= SWDG_HL_PRE_VMIN;
   static constexpr int XCH = ACC + (PRE ? 4 : 3) * GPAD;
   static constexpr int NODE = XCH + LP * XS;
   static constexpr int TR = NODE + kNodeFields * GNP;  // [kTr][E][4][N1]
   static constexpr int EFO = TR + E * 4 * N1 * kTr;     // int4 [NBUF][E][4]
   static constexpr int RED = EFO + 2 * E * 4 * 2;      // [2 parts][E][2 pieces][5]
   static constexpr int BAR = RED + 2 * E * 2 * 5;
-  // transposed node phase (NT): every thread finalises E (N+1)^2 / THREADS nodes;
-  // the xi lines leave their accumulators and state next to the eta ones
   // one instantiation of the group loop per line direction (XI_SPLIT): measured
   // (B200, 1M elements) inviscid N=5 1.615 -> 1.463 ms/stage; slower at every
   // other degree (twice the code: N=8 4.34 -> 5.16, N=15 13.2 -> 27.0)
   static constexpr bool XI_SPLIT = !V && N1 == 6;
-  static constexpr bool NT = NT_;  // measured: faster only at N+1 = 9 (4.56 -> 4.34 ms), slower at 6, 7, 8, 10
-  static constexpr int NPT = (E * NP + THREADS - 1) / THREADS;  // nodes per thread
-  static constexpr int PMAX = NP / 32 + 2;                      // node-warp pieces
-  static constexpr int ACCX = BAR + 2;                          // [3][GPAD] xi accumulators
-  static constexpr int STT = ACCX + (NT ? 3 * GPAD : 0);        // [3][GPAD] state
-  static constexpr int NRED = STT + (NT ? 3 * GPAD : 0);        // [E][PMAX][5]
-  static constexpr int ELM = NRED + (NT ? E * PMAX * 5 : 0);    // [E][4]
-  static constexpr int TOTAL = ELM + (NT ? E * 4 : 0);
+  static constexpr int TOTAL = BAR + 2;
   static constexpr size_t bytes = TOTAL * sizeof(double);
 };
 
@@ -354,152 +344,18 @@ __device__ __forceinline__ void hl_visc_div(const double* Lb, int li, bool xi,
   }
 }
 
-// Transposed node phase of the half-line kernel (HL::NT): thread per node over
-// the group (coalesced, every warp busy), -1/J, source, SSPRK3 update, element
-// means by a segmented warp-shuffle reduction in node order, one summary thread
-// per element (reject, theta, min h), then the limiter and the stores.
-template <int N1, bool FORCE, bool VISC>
-__device__ __forceinline__ void hl_node_phase_t(double* sm, const Mesh& M, const Phys& Ph,
-                                                const StageArgs& A, Flags* F, int e0, int ne,
-                                                int tid) {
-  using P = HL<N1, VISC>;
-  using O = Ops<N1>;
-  constexpr int NP = N1 * N1, NPT = P::NPT, GP = P::GPAD;
-  const double g = Ph.g;
-  const int lane = tid & 31;
-  const int shift = (int)(((long long)e0 * NP) & 1);
-  const double* Nd = sm + P::NODE + shift;
-  double sh[NPT], shu[NPT], shv[NPT];
-#pragma unroll
-  for (int m = 0; m < NPT; ++m) {
-    const int r = tid + m * P::THREADS;
-    const bool ok = r < ne * NP;
-    const int el = ok ? r / NP : 0, loc = r - el * NP, i = loc / N1, j = loc - i * N1;
-    const int pq = el * P::EPAD + i * P::PAD + j;
-    double pv[5] = {0.0, 0.0, 0.0, 0.0, 1.0e300};
-    sh[m] = shu[m] = shv[m] = 0.0;
-    if (ok) {
-      const long long n = (long long)e0 * NP + r;
-      const double jac = Nd[P::N_JAC * P::GNP + r];
-      const double h = sm[P::STT + pq], hu = sm[P::STT + GP + pq], hv = sm[P::STT + 2 * GP + pq];
-      const double ij = -1.0 / jac, hg2 = 0.5 * g * h;
-      double rh = (sm[P::ACC + pq] + sm[P::ACCX + pq]) * ij;
-      double rhu =
-          (sm[P::ACC + GP + pq] + sm[P::ACCX + GP + pq] + hg2 * Nd[P::N_SX * P::GNP + r]) * ij;
-      double rhv =
-          (sm[P::ACC + 2 * GP + pq] + sm[P::ACCX + 2 * GP + pq] + hg2 * Nd[P::N_SY * P::GNP + r]) *
-          ij;
-      if (FORCE) {
-        rh += A.fh[n];
-        rhu += A.fhu[n];
-        rhv += A.fhv[n];
-      }
-      if (A.rhs.h) {
-        A.rhs.h[n] = rh;
-        A.rhs.hu[n] = rhu;
-        A.rhs.hv[n] = rhv;
-      }
-      double a0 = h + A.dt * rh, a1 = hu + A.dt * rhu, a2 = hv + A.dt * rhv;
-      if (A.stage > 0 && A.update) {
-        a0 = A.ca * Nd[P::N_WH * P::GNP + r] + A.cb * a0;
-        a1 = A.ca * Nd[P::N_WHU * P::GNP + r] + A.cb * a1;
-        a2 = A.ca * Nd[P::N_WHV * P::GNP + r] + A.cb * a2;
-      }
-      sh[m] = a0;
-      shu[m] = a1;
-      shv[m] = a2;
-      const double wq = O::w(i) * O::w(j) * jac;
-      pv[0] = wq;
-      pv[1] = wq * a0;
-      pv[2] = wq * a1;
-      pv[3] = wq * a2;
-      pv[4] = a0;
-    }
-    // segmented reduction over this pass's lanes of the same element
-    const int seg = ok ? el : -1 - lane;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int seg2 = __shfl_down_sync(0xffffffffu, seg, o);
-      double t[5];
-#pragma unroll
-      for (int c = 0; c < 5; ++c) t[c] = __shfl_down_sync(0xffffffffu, pv[c], o);
-      if (lane + o < 32 && seg2 == seg) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) pv[c] += t[c];
-        pv[4] = smin(pv[4], t[4]);
-      }
-    }
-    if (ok && (lane == 0 || loc == 0)) {
-      const int nw = (m * P::THREADS + tid) >> 5, w0 = (el * NP) >> 5;
-      double* rr = sm + P::NRED + (el * P::PMAX + nw - w0) * 5;
-#pragma unroll
-      for (int c = 0; c < 5; ++c) rr[c] = pv[c];
-    }
-  }
-  __syncthreads();
-  // one thread per element: the summary (limit_element, limiter.hpp:43-84;
-  // reject, timeloop.hpp:205-209)
-  if (tid < ne && A.update) {
-    const int el = tid, w0 = (el * NP) >> 5, npc = ((el * NP + NP - 1) >> 5) - w0 + 1;
-    double area = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, mmin = 1.0e300;
-    for (int pc = 0; pc < npc; ++pc) {
-      const double* rr = sm + P::NRED + (el * P::PMAX + pc) * 5;
-      area += rr[0];
-      b0 += rr[1];
-      b1 += rr[2];
-      b2 += rr[3];
-      mmin = smin(mmin, rr[4]);
-    }
-    const double inv = 1.0 / area;
-    const double avg0 = inv * b0, avg1 = inv * b1, avg2 = inv * b2;
-    double theta = 1.0;
-    bool ok = true;
-    if (avg0 < 0.0) {
-      atomicExch(&F->reject, 1);
-      if (!Ph.limiter) atomicExch(&F->abort, 1);
-      ok = false;
-    }
-    if (ok && Ph.limiter && mmin < 0.0) {
-      const double denom = avg0 - mmin;
-      theta = denom < 1e-14 ? 1.0 : smin(1.0, avg0 / denom);
-    }
-    if (ok && !Ph.limiter && mmin < 0.0) atomicExch(&F->abort, 1);
-    if (ok) {
-      const double mlim = theta < 1.0 ? smax(theta * (mmin - avg0) + avg0, 0.0) : mmin;
-      atomicMin(&F->min_h_key, order_key(mlim));
-      if (theta < 1.0) atomicAdd(&F->n_limited, 1);
-    }
-    double* em = sm + P::ELM + el * 4;
-    em[0] = avg0;
-    em[1] = avg1;
-    em[2] = avg2;
-    em[3] = ok ? theta : -1.0;
-  }
-  __syncthreads();
-  if (!A.update) return;
-#pragma unroll
-  for (int m = 0; m < NPT; ++m) {
-    const int r = tid + m * P::THREADS;
-    if (r >= ne * NP) continue;
-    const int el = r / NP;
-    const double* em = sm + P::ELM + el * 4;
-    const double theta = em[3];
-    if (theta < 0.0) continue;  // rejected element: nothing written
-    double a0 = sh[m], a1 = shu[m], a2 = shv[m];
-    if (theta < 1.0) {
-      a0 = smax(theta * (a0 - em[0]) + em[0], 0.0);
-      a1 = theta * (a1 - em[1]) + em[1];
-      a2 = theta * (a2 - em[2]) + em[2];
-    }
-    if (Ph.limiter && a0 < Ph.h_tol) {
-      a1 = 0.0;
-      a2 = 0.0;
-    }
-    const long long n = (long long)e0 * NP + r;
-    A.out.h[n] = a0;
-    A.out.hu[n] = a1;
-    A.out.hv[n] = a2;
-  }
+// streamed-node loops rolled (1) or unrolled (0) per configuration, measured
+// (ms/stage, 1M elements, profiles/r02_ab_hl_roll.txt): inviscid N+1 = 6 1.461 ->
+// 1.444, 7 2.365 -> 2.111, 10 4.440 -> 4.351; viscous N+1 = 8 6.02 -> 5.89,
+// 9 8.51 -> 7.79, 10 11.56 -> 10.87, 14 25.2 -> 24.6, 15 33.2 -> 31.2, 16 39.8 ->
+// 38.9; slower or neutral elsewhere (inviscid N+1 = 12: 7.47 -> 7.84, 16: 13.6 ->
+// 14.1).  At N+1 = 9 the rolled loops replaced the transposed node phase (a
+// thread-per-node node phase over the group, with the xi lines' accumulators and
+// state handed over through shared memory), which had been the faster choice
+// there unrolled: 4.37 -> 4.06 ms/stage.  SWDG_HL_XROLL > 0 rolls every N+1 >= it.
+__host__ __device__ constexpr bool hl_roll(int n1, bool visc) {
+  return SWDG_HL_XROLL > 0 ? n1 >= SWDG_HL_XROLL
+         : visc ? (n1 >= 8 && n1 <= 10) || n1 >= 14 : (n1 == 6 || n1 == 7 || n1 == 9 || n1 == 10);
 }
 
 // resident CTAs the register allocation must allow: 4 (<= 128 registers) for
@@ -509,17 +365,6 @@ __device__ __forceinline__ void hl_node_phase_t(double* sm, const Mesh& M, const
 // faster at N+1 = 10); above, a 168-register cap spills (N+1 = 11, 13..16)
 // The viscous variant keeps 3 at N+1 = 6, 7 (measured: N=5 3.566 vs 3.721, N=6
 // 5.180 vs 5.547 ms/stage with 4) and takes 4 at N+1 = 5 (2.777 -> 2.559).
-// streamed-node loops rolled (1) or unrolled (0) per configuration, measured
-// (ms/stage, 1M elements, profiles/r02_ab_hl_roll.txt): inviscid N+1 = 6 1.461 ->
-// 1.444, 7 2.365 -> 2.111, 10 4.440 -> 4.351; viscous N+1 = 8 6.02 -> 5.89,
-// 9 8.51 -> 7.79, 10 11.56 -> 10.87, 14 25.2 -> 24.6, 15 33.2 -> 31.2, 16 39.8 ->
-// 38.9; slower or neutral elsewhere (inviscid N+1 = 9: 4.36 -> 4.53, 12: 7.47 ->
-// 7.84, 16: 13.6 -> 14.1).  SWDG_HL_XROLL > 0 rolls every N+1 >= it (A/B builds).
-__host__ __device__ constexpr bool hl_roll(int n1, bool visc) {
-  return SWDG_HL_XROLL > 0 ? n1 >= SWDG_HL_XROLL
-         : visc ? (n1 >= 8 && n1 <= 10) || n1 >= 14 : (n1 == 6 || n1 == 7 || n1 == 10);
-}
-
 __host__ __device__ constexpr int hl_min_blocks(int n1, bool visc) {
   return n1 == 5 ? SWDG_HL_MB5 : (n1 == 6 && !visc) ? SWDG_HL_MB6
          : (n1 == 7 && !visc) ? SWDG_HL_MB7 : n1 <= 10 ? 3 : 1;
@@ -825,8 +670,7 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
         r2[0] += c * f2;
       }
     }
-    // eta-line threads hand their accumulators to the xi-line owners (NT: the
-    // xi lines also leave theirs and the state, for the transposed node phase)
+    // eta-line threads hand their accumulators to the xi-line owners
     if constexpr (P::PRE) {
       // the eta lines finish their half of each node before handing it over:
       // split source (dg_rhs.hpp:154-183) and the -1/J scaling, so the xi-line
@@ -850,8 +694,8 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
           }
       }
     }
-    if (active && (P::NT || (!P::PRE && !xi))) {
-      double* acc = sm + (xi ? P::ACCX : P::ACC) + el * P::EPAD;
+    if (active && !P::PRE && !xi) {
+      double* acc = sm + P::ACC + el * P::EPAD;
 #pragma unroll
       for (int s = 0; s < S; ++s)
         if (s < nk) {
@@ -859,21 +703,11 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
           acc[0 * P::GPAD + q] = r0[s];
           acc[1 * P::GPAD + q] = r1[s];
           acc[2 * P::GPAD + q] = r2[s];
-          if (P::NT && xi) {
-            double* stt = sm + P::STT + el * P::EPAD;
-            stt[0 * P::GPAD + q] = h[s];
-            stt[1 * P::GPAD + q] = hu[s];
-            stt[2 * P::GPAD + q] = hv[s];
-          }
         }
     }
     __syncthreads();
     mbar_wait(bar_node, ph_node);
     ph_node ^= 1;
-    if constexpr (P::NT) {
-      hl_node_phase_t<N1, FORCE, VISC>(sm, M, Ph, A, F, e0, ne, tid);
-      continue;
-    }
 
     // ---- node phase on the xi-line threads: nodes (k, li), k in the own half
     double pv[5] = {0.0, 0.0, 0.0, 0.0, 1.0e300};  // element partials of this thread
