@@ -280,9 +280,9 @@ def measure_gpu_distributed(N: int, steps: int, warmup: int, viscous: bool, rank
     import numpy as np
     import torch
     from paper_1804_02221_b200 import swdg
-    from paper_1804_02221_b200.distributed import (GpuPartition, IpcExchanger, TorchExchanger,
-                                                   compute_dt_distributed, run_steps_distributed,
-                                                   try_step_distributed)
+    from paper_1804_02221_b200.distributed import (GpuPartition, GraphStepper, IpcExchanger,
+                                                   TorchExchanger, compute_dt_distributed,
+                                                   run_steps_distributed, try_step_distributed)
 
     spec = spec_for(N)
     cfg = run_config(N, viscous)
@@ -299,19 +299,35 @@ def measure_gpu_distributed(N: int, steps: int, warmup: int, viscous: bool, rank
     integ.upload(st)
     ex = IpcExchanger(b) if halo == "ipc" else TorchExchanger(b, "cuda")
     dt = 0.1 * compute_dt_distributed(b, ex, 0.5, N, cfg.phys)
-    run_steps_distributed(b, ex, warmup, 0.0, dt)
+    if halo == "ipc":  # the steps replay a captured graph (GraphStepper)
+        stepper = GraphStepper(b, ex, 0.0, dt)
+        stepper.begin()
+        stepper.run(warmup)
+        if not stepper.accepted():
+            raise RuntimeError("a warm-up step was rejected")
+    else:
+        run_steps_distributed(b, ex, warmup, 0.0, dt)
     torch.distributed.barrier()
     torch.cuda.synchronize()
     l0 = integ.launch_count()
+    r0 = stepper.replays if halo == "ipc" else 0
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev) as clk:
         ev0.record(stream)
-        ok = run_steps_distributed(b, ex, steps, warmup * dt, dt)
-        ev1.record(stream)
-        torch.cuda.synchronize()
+        if halo == "ipc":
+            stepper.run(steps)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            ok = stepper.accepted()
+        else:
+            ok = run_steps_distributed(b, ex, steps, warmup * dt, dt)
+            ev1.record(stream)
+            torch.cuda.synchronize()
     if not ok:
         raise RuntimeError("a step was rejected during the timed run (invalid measurement)")
     launches = integ.launch_count() - l0
+    if halo == "ipc":  # kernels replayed from the graph are not API calls: count them
+        launches += (stepper.replays - r0) * stepper.replay_launches
     t = torch.tensor([ev0.elapsed_time(ev1)], device="cuda", dtype=torch.float64)
     torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms = float(t.item())

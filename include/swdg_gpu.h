@@ -310,17 +310,21 @@ int swdg_gpu_halo_unpack(swdg_gpu* ctx, int what, int stage, const double* recv_
  * cudaIpcMemHandle_t out) and maps its peers' (ipc_open; NVLink / NVSwitch
  * between GPUs, plain device memory between processes sharing one GPU).
  * halo_push packs send entries [first, first+count) of `what` (as halo_pack)
- * straight into `dst` (a peer's mailbox slot) and then stores `seq` to `flag`
- * (the peer's flag for this rank) with a system-scope release.  halo_wait
- * queues a device-side wait until each of the n flags (this rank's mailbox)
- * reaches seq -- no host synchronisation; after timeout_s it gives up and
- * halo_status reports it (synchronises the stream; clears the report). */
+ * straight into `dst` (a peer's mailbox slot) and then stores the sequence
+ * number to `flag` (the peer's flag for this rank) with a system-scope release.
+ * halo_wait queues a device-side wait until each of the n flags (this rank's
+ * mailbox) reaches the sequence number -- no host synchronisation; after
+ * timeout_s it gives up and halo_status reports it (synchronises the stream;
+ * clears the report).  The sequence number is `seq`, or `*seq_base + seq` with a
+ * device-resident base (seq_base non-NULL): a captured CUDA graph then carries
+ * offsets and seq_advance (queued at the end of each replay) moves the base. */
 int swdg_gpu_ipc_alloc(swdg_gpu* ctx, int64_t bytes, void** dptr, void* handle);
 int swdg_gpu_ipc_open(swdg_gpu* ctx, const void* handle, void** dptr);
 int swdg_gpu_halo_push(swdg_gpu* ctx, int what, int stage, int64_t first, int64_t count,
-                       double* dst, uint64_t* flag, uint64_t seq);
-int swdg_gpu_halo_wait(swdg_gpu* ctx, const uint64_t* flags, int32_t n, uint64_t seq,
-                       double timeout_s);
+                       double* dst, uint64_t* flag, const uint64_t* seq_base, uint64_t seq);
+int swdg_gpu_halo_wait(swdg_gpu* ctx, const uint64_t* flags, int32_t n, const uint64_t* seq_base,
+                       uint64_t seq, double timeout_s);
+int swdg_gpu_seq_advance(swdg_gpu* ctx, uint64_t* seq_base, uint64_t by);
 int swdg_gpu_halo_status(swdg_gpu* ctx, int32_t* timed_out);
 int swdg_gpu_dt_candidates(swdg_gpu* ctx, double* dt_min, double* min_len);
 int swdg_gpu_step_begin(swdg_gpu* ctx);

@@ -62,17 +62,26 @@ __global__ void k_halo_push(const int* idx, long long n, int nf, const double* f
   __threadfence_system();
 }
 
-__global__ void k_flag_release(unsigned long long* flag, unsigned long long seq) {
+// sequence numbers are `seq`, or `*base + seq` when the caller keeps the base on
+// the device (graph replays: the captured kernels carry offsets, a kernel at the
+// end of each replay advances the base)
+__global__ void k_flag_release(unsigned long long* flag, const unsigned long long* base,
+                               unsigned long long seq) {
   __threadfence_system();
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(seq) : "memory");
+  const unsigned long long v = (base ? *base : 0ull) + seq;
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(v) : "memory");
 }
+
+__global__ void k_seq_advance(unsigned long long* base, unsigned long long by) { *base += by; }
 
 // the receiver: one lane per peer polls its flag (system-scope acquire) until the
 // peer's data of exchange `seq` has landed; a peer that never arrives sets *err
 // after timeout_ns instead of hanging the stream
-__global__ void k_flags_wait(const unsigned long long* flags, int n, unsigned long long seq,
+__global__ void k_flags_wait(const unsigned long long* flags, int n,
+                             const unsigned long long* base, unsigned long long seq,
                              unsigned long long timeout_ns, int* err) {
   const int i = threadIdx.x;
+  if (base) seq += *base;
   if (i < n) {
     unsigned long long t0, t, v;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -93,21 +102,28 @@ __global__ void k_flags_wait(const unsigned long long* flags, int n, unsigned lo
 }  // namespace
 
 int launch_halo_push(const int* idx, long long n, int nf, const double* const* f, double* dst,
-                     unsigned long long* flag, unsigned long long seq, cudaStream_t st) {
+                     unsigned long long* flag, const unsigned long long* base,
+                     unsigned long long seq, cudaStream_t st) {
   int launches = 0;
   if (n > 0) {
     k_halo_push<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(idx, n, nf, f[0], f[1], f[2],
                                                             nf > 3 ? f[3] : f[0], dst);
     ++launches;
   }
-  k_flag_release<<<1, 1, 0, st>>>(flag, seq);
+  k_flag_release<<<1, 1, 0, st>>>(flag, base, seq);
   return launches + 1;
 }
 
-int launch_flags_wait(const unsigned long long* flags, int n, unsigned long long seq,
-                      unsigned long long timeout_ns, int* err, cudaStream_t st) {
+int launch_seq_advance(unsigned long long* base, unsigned long long by, cudaStream_t st) {
+  k_seq_advance<<<1, 1, 0, st>>>(base, by);
+  return 1;
+}
+
+int launch_flags_wait(const unsigned long long* flags, int n, const unsigned long long* base,
+                      unsigned long long seq, unsigned long long timeout_ns, int* err,
+                      cudaStream_t st) {
   if (n <= 0) return 0;
-  k_flags_wait<<<1, ((n + 31) / 32) * 32, 0, st>>>(flags, n, seq, timeout_ns, err);
+  k_flags_wait<<<1, ((n + 31) / 32) * 32, 0, st>>>(flags, n, base, seq, timeout_ns, err);
   return 1;
 }
 

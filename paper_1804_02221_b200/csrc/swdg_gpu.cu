@@ -1382,7 +1382,7 @@ int swdg_gpu_ipc_open(swdg_gpu* c, const void* handle, void** dptr) {
 }
 
 int swdg_gpu_halo_push(swdg_gpu* c, int what, int k, int64_t first, int64_t count, double* dst,
-                       uint64_t* flag, uint64_t seq) {
+                       uint64_t* flag, const uint64_t* seq_base, uint64_t seq) {
   return guarded(c, [&] {
     if (k < 0 || k > 2 || what < 0 || what > 1) throw InputError{"halo_push: bad stage/what"};
     if (what == 1 && !c->fvu) throw InputError{"halo_push: viscosity is off"};
@@ -1397,14 +1397,15 @@ int swdg_gpu_halo_push(swdg_gpu* c, int what, int k, int64_t first, int64_t coun
       f[3] = c->gvv;
     }
     c->launches += launched(launch_halo_push(c->send_idx + first, count, what ? 4 : 3, f, dst,
-                                             reinterpret_cast<unsigned long long*>(flag), seq,
-                                             c->stream), "launch_halo_push");
+                                             reinterpret_cast<unsigned long long*>(flag),
+                                             reinterpret_cast<const unsigned long long*>(seq_base),
+                                             seq, c->stream), "launch_halo_push");
     return SWDG_OK;
   });
 }
 
-int swdg_gpu_halo_wait(swdg_gpu* c, const uint64_t* flags, int32_t n, uint64_t seq,
-                       double timeout_s) {
+int swdg_gpu_halo_wait(swdg_gpu* c, const uint64_t* flags, int32_t n, const uint64_t* seq_base,
+                       uint64_t seq, double timeout_s) {
   return guarded(c, [&] {
     if (n < 0 || (n > 0 && !flags)) throw InputError{"halo_wait: bad arguments"};
     if (!c->ipc_err) {
@@ -1413,7 +1414,17 @@ int swdg_gpu_halo_wait(swdg_gpu* c, const uint64_t* flags, int32_t n, uint64_t s
     }
     const unsigned long long tns = (unsigned long long)(std::max(timeout_s, 1e-3) * 1e9);
     c->launches += launched(launch_flags_wait(reinterpret_cast<const unsigned long long*>(flags), n,
+                                              reinterpret_cast<const unsigned long long*>(seq_base),
                                               seq, tns, c->ipc_err, c->stream), "launch_flags_wait");
+    return SWDG_OK;
+  });
+}
+
+int swdg_gpu_seq_advance(swdg_gpu* c, uint64_t* seq_base, uint64_t by) {
+  return guarded(c, [&] {
+    if (!seq_base) throw InputError{"seq_advance: null base"};
+    c->launches += launched(launch_seq_advance(reinterpret_cast<unsigned long long*>(seq_base), by,
+                                               c->stream), "launch_seq_advance");
     return SWDG_OK;
   });
 }

@@ -74,9 +74,12 @@ extern int g_grid_cap;
 
 // mode-independent (kernels_common.cu)
 int launch_halo_push(const int* idx, long long n, int nf, const double* const* f, double* dst,
-                     unsigned long long* flag, unsigned long long seq, cudaStream_t st);
-int launch_flags_wait(const unsigned long long* flags, int n, unsigned long long seq,
-                      unsigned long long timeout_ns, int* err, cudaStream_t st);
+                     unsigned long long* flag, const unsigned long long* base,
+                     unsigned long long seq, cudaStream_t st);
+int launch_flags_wait(const unsigned long long* flags, int n, const unsigned long long* base,
+                      unsigned long long seq, unsigned long long timeout_ns, int* err,
+                      cudaStream_t st);
+int launch_seq_advance(unsigned long long* base, unsigned long long by, cudaStream_t st);
 int launch_halo_pack(const int* idx, long long n, int nf, const double* const* f, double* buf,
                      cudaStream_t st);
 int launch_halo_unpack(const int* idx, long long n, int nf, double* const* f, const double* buf,

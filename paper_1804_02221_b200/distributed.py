@@ -143,8 +143,13 @@ class IpcExchanger:
         self.roff, nr = _offsets(plan, "recv_idx")
         self.slot = max(nr, 1) * 4  # doubles per receive slot
         nflag = max(len(self.peers), 1)
-        self.base, handle = backend.ipc_alloc((2 * self.slot + nflag) * 8)
+        # mailbox: 2 receive slots, the peers' flags, and this rank's device-resident
+        # sequence base (graph replays; local use only)
+        self.base, handle = backend.ipc_alloc((2 * self.slot + nflag + 1) * 8)
         self.flags = self.base + 2 * self.slot * 8
+        self.seq_base = self.flags + nflag * 8
+        self.dev_base = 0   # host mirror of *seq_base
+        self.capturing = None  # exchange count inside a capture
         me = dist.get_rank()
         info = dict(handle=handle, slot=self.slot,
                     at={p: (self.roff[p][0], self.roff[p][1], j) for j, p in enumerate(self.peers)})
@@ -160,19 +165,51 @@ class IpcExchanger:
         self.seq = 0
 
     def start(self, what: int, k: int):
-        self.seq += 1
-        s, nf = self.seq & 1, (4 if what else 3)
+        if self.capturing is None:  # eager: absolute sequence numbers
+            self.seq += 1
+            seq, off, base = self.seq, self.seq, None
+        else:  # captured: offsets from the device-resident base
+            self.capturing += 1
+            seq, off, base = self.seq + self.capturing, self.capturing, self.seq_base
+        s, nf = seq & 1, (4 if what else 3)
         for p in self.peers:
-            base, slot, o = self.dst[p]
+            pbase, slot, o = self.dst[p]
             first, n = self.soff[p]
-            self.b.push(what, k, first, n, base + (s * slot + o * nf) * 8, self.flag_at[p],
-                        self.seq)
-        return what, k, self.seq
+            self.b.push(what, k, first, n, pbase + (s * slot + o * nf) * 8, self.flag_at[p],
+                        off, base)
+        return what, k, seq, off, base
 
     def finish(self, handle):
-        what, k, seq = handle
-        self.b.wait_flags(self.flags, len(self.peers), seq, self.timeout_s)
+        what, k, seq, off, base = handle
+        self.b.wait_flags(self.flags, len(self.peers), off, self.timeout_s, base)
         self.b.unpack_at(what, k, self.base + (seq & 1) * self.slot * 8)
+
+    # CUDA-graph capture of whole steps: the captured pushes and waits carry
+    # sequence offsets from the device base, and the replay's last kernel advances
+    # the base by the replay's exchange count (even, so every exchange keeps its
+    # receive slot from replay to replay)
+    def sync_base(self):
+        """bring the device base to the host count (eagerly, before a capture)"""
+        if self.dev_base != self.seq:
+            self.b.seq_advance(self.seq_base, self.seq - self.dev_base)
+            self.dev_base = self.seq
+
+    def capture_begin(self):
+        if self.dev_base != self.seq:
+            raise RuntimeError("sync_base() before the capture")
+        self.capturing = 0
+
+    def capture_end(self) -> int:
+        n, self.capturing = self.capturing, None
+        if n % 2:
+            raise ValueError("a captured replay needs an even number of exchanges")
+        self.b.seq_advance(self.seq_base, n)
+        self.per_replay = n
+        return n
+
+    def replayed(self):
+        self.seq += self.per_replay
+        self.dev_base += self.per_replay
 
     def exchange(self, what: int, k: int):
         self.finish(self.start(what, k))
@@ -265,6 +302,91 @@ def try_step_distributed(b: Backend, ex, t: float, dt: float) -> bool:
     accept = not rej
     b.step_commit(accept)
     return accept
+
+
+def _step_stages(b: Backend, ex, t: float, dt: float):
+    for k in range(3):
+        if _overlap(b) and hasattr(ex, "start"):
+            _stage_overlapped(b, ex, k, t, dt)
+            continue
+        ex.exchange(0, k)
+        if b.visc:
+            b.stage_visc(k, t, dt)
+            ex.exchange(1, k)
+        b.stage_run(k, t, dt)
+
+
+class GraphStepper:
+    """Fixed-dt partitioned stepping replayed from a captured CUDA graph.  With the
+    peer-memory exchanger a whole step is stream-ordered device work (pushes,
+    device-side flag waits, unpacks, interior/boundary stage kernels), so two steps
+    -- the W/A ping-pong returns to its start -- are captured once and replayed: no
+    Python and no host synchronisation per stage or per step.  The first step runs
+    eagerly (first-launch attributes and occupancy queries stay out of the
+    capture), and so does an odd remainder.  No forcing (the captured stage
+    arguments are those of the captured steps)."""
+
+    def __init__(self, b: "GpuPartition", ex: "IpcExchanger", t: float, dt: float):
+        self.b, self.ex, self.t, self.dt = b, ex, t, dt
+        self.g = None
+        self.replays = 0
+        self.replay_launches = 0  # kernels per replay (counted while capturing)
+
+    def _eager(self):
+        _step_stages(self.b, self.ex, self.t, self.dt)
+        self.b.step_commit(True)
+
+    def _capture(self):
+        import torch
+        b, ex = self.b, self.ex
+        ex.sync_base()
+        self.g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        l0 = b.integ.launch_count()
+        with torch.cuda.graph(self.g, stream=side, capture_error_mode="thread_local"):
+            b.set_stream(torch.cuda.current_stream().cuda_stream)
+            ex.capture_begin()
+            for _ in range(2):
+                _step_stages(b, ex, self.t, self.dt)
+                b.step_commit(True)
+            ex.capture_end()
+        self.replay_launches = b.integ.launch_count() - l0
+        b.set_stream(torch.cuda.current_stream().cuda_stream)
+
+    def run(self, nsteps: int):
+        """queue nsteps steps (no host synchronisation)"""
+        if self.g is None and nsteps > 0:
+            self._eager()
+            nsteps -= 1
+            if nsteps >= 2:
+                self._capture()
+        for _ in range(nsteps // 2 if self.g is not None else 0):
+            self.g.replay()
+            self.ex.replayed()
+            self.replays += 1
+        for _ in range(nsteps % 2 if self.g is not None else nsteps):
+            self._eager()
+
+    def accepted(self) -> bool:
+        """the stage flags of every step since begin(), reduced over the ranks"""
+        rej, ab = self.b.step_flags()
+        rej, ab = self.ex.all_max([float(rej), float(ab)])
+        if ab:
+            raise swdg.NumericalAbort("negative water height without limiter")
+        return not rej
+
+    def begin(self):
+        self.b.step_begin()
+
+
+def run_steps_distributed_graph(b: "GpuPartition", ex: "IpcExchanger", nsteps: int, t: float,
+                                dt: float) -> bool:
+    """run_steps_distributed over GraphStepper (peer-memory exchanger)."""
+    st = GraphStepper(b, ex, t, dt)
+    st.begin()
+    st.run(nsteps)
+    return st.accepted()
 
 
 def run_steps_distributed(b: Backend, ex, nsteps: int, t: float, dt: float) -> bool:
@@ -443,9 +565,11 @@ class GpuPartition(Backend):
                                                    C.c_void_p]),
                            ("swdg_gpu_ipc_open", [vp, C.c_void_p, C.POINTER(C.c_void_p)]),
                            ("swdg_gpu_halo_push", [vp, C.c_int, C.c_int, C.c_int64, C.c_int64,
-                                                   C.c_void_p, C.c_void_p, C.c_uint64]),
-                           ("swdg_gpu_halo_wait", [vp, C.c_void_p, C.c_int32, C.c_uint64,
-                                                   C.c_double]),
+                                                   C.c_void_p, C.c_void_p, C.c_void_p,
+                                                   C.c_uint64]),
+                           ("swdg_gpu_halo_wait", [vp, C.c_void_p, C.c_int32, C.c_void_p,
+                                                   C.c_uint64, C.c_double]),
+                           ("swdg_gpu_seq_advance", [vp, C.c_void_p, C.c_uint64]),
                            ("swdg_gpu_halo_status", [vp, i32p])):
             f = getattr(L, name)
             f.restype = C.c_int
@@ -518,12 +642,18 @@ class GpuPartition(Backend):
         self._chk(self.L.swdg_gpu_ipc_open(self.integ._h, h, C.byref(p)))
         return p.value
 
-    def push(self, what, k, first, count, dst: int, flag: int, seq: int):
+    def push(self, what, k, first, count, dst: int, flag: int, seq: int, base: int | None = None):
         self._chk(self.L.swdg_gpu_halo_push(self.integ._h, what, k, first, count,
-                                            C.c_void_p(dst), C.c_void_p(flag), seq))
+                                            C.c_void_p(dst), C.c_void_p(flag), C.c_void_p(base),
+                                            seq))
 
-    def wait_flags(self, flags: int, n: int, seq: int, timeout_s: float):
-        self._chk(self.L.swdg_gpu_halo_wait(self.integ._h, C.c_void_p(flags), n, seq, timeout_s))
+    def wait_flags(self, flags: int, n: int, seq: int, timeout_s: float,
+                   base: int | None = None):
+        self._chk(self.L.swdg_gpu_halo_wait(self.integ._h, C.c_void_p(flags), n,
+                                            C.c_void_p(base), seq, timeout_s))
+
+    def seq_advance(self, base: int, by: int):
+        self._chk(self.L.swdg_gpu_seq_advance(self.integ._h, C.c_void_p(base), by))
 
     def halo_timed_out(self) -> bool:
         v = C.c_int32()

@@ -94,3 +94,75 @@ def test_two_processes_peer_memory_halo(tmp_path, mode, scen):
     last = res[0][3][-1]
     assert last["min_h"] == d.min_h
     assert abs(last["mass"] - d.mass) <= 1e-13 * abs(d.mass)
+
+
+def _graph_worker(rank, world, port_no, N, visc, steps, path):
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port_no}", rank=rank,
+                            world_size=world)
+    from paper_1804_02221_b200 import swdg
+    from paper_1804_02221_b200.distributed import (GpuPartition, IpcExchanger,
+                                                   run_steps_distributed_graph)
+    spec, cfg, dt = _graph_case(N, visc)
+    b = GpuPartition.structured(spec, cfg, world, rank, 0)
+    x, y = b.integ.geometry("x"), b.integ.geometry("y")
+    b.upload([1.0 + 0.1 * np.sin(2 * np.pi * x) * np.cos(2 * np.pi * y),
+              0.3 * np.ones_like(x), -0.2 * np.ones_like(x)])
+    ex = IpcExchanger(b, timeout_s=20.0)
+    ok = run_steps_distributed_graph(b, ex, steps, 0.0, dt)
+    np_ = (N + 1) ** 2
+    n_own = b.lm.n_owned
+    mine = np.stack([w[: n_own * np_] for w in b.download()])
+    out = [None] * world
+    dist.all_gather_object(out, (b.lm.global_ids[:n_own].tolist(), mine, ok, ex.seq))
+    if rank == 0:
+        np.save(path, np.array(out, dtype=object), allow_pickle=True)
+    dist.destroy_process_group()
+
+
+def _graph_case(N, visc):
+    from paper_1804_02221_b200 import swdg
+    v = swdg.ViscosityConfig(False)
+    if visc:
+        smin, smax = swdg.default_sigma_band(N)
+        v = swdg.ViscosityConfig(True, 0.1, smin, smax)
+    cfg = swdg.RunConfig(phys=swdg.PhysicsParams(9.81), visc=v, mode=swdg.MODE_FAST)
+    spec = swdg.structured_spec("wavy", N, 24, 24, periodic_x=True, periodic_y=True,
+                                bathy="smooth")
+    return spec, cfg, 5e-5
+
+
+@pytest.mark.parametrize("N,visc", [(4, False), (3, True)])
+def test_two_processes_graph_replayed_steps(tmp_path, N, visc):
+    """run_steps_distributed_graph: one eager step, two captured steps replayed twice
+    (the device-resident sequence base advancing per replay): the same state as the
+    single-GPU fixed-dt stepping of the same mesh."""
+    import torch.multiprocessing as mp
+    from paper_1804_02221_b200 import swdg
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port_no = s.getsockname()[1]
+    path = os.path.join(tmp_path, "res.npy")
+    steps = 5
+    mp.spawn(_graph_worker, args=(2, port_no, N, visc, steps, path), nprocs=2, join=True)
+    res = np.load(path, allow_pickle=True)
+    spec, cfg, dt = _graph_case(N, visc)
+    single = swdg.TimeIntegrator.structured(spec, cfg)
+    x, y = single.geometry("x"), single.geometry("y")
+    single.upload(swdg.State(1.0 + 0.1 * np.sin(2 * np.pi * x) * np.cos(2 * np.pi * y),
+                             0.3 * np.ones_like(x), -0.2 * np.ones_like(x)))
+    assert single.run_steps(steps, 0.0, dt)
+    want = [np.empty(single.mesh.n_nodes) for _ in range(3)]
+    single.download(swdg.State(*want))
+    np_ = (N + 1) ** 2
+    got = [np.zeros(single.mesh.n_nodes) for _ in range(3)]
+    per_step = 3 * (2 if visc else 1)
+    for gids, mine, ok, seq in res:
+        assert ok
+        assert seq == steps * per_step
+        sel = (np.array(gids)[:, None] * np_ + np.arange(np_)).ravel()
+        for j in range(3):
+            got[j][sel] = mine[j]
+    assert beq(got, want)
