@@ -218,9 +218,14 @@ class IpcExchanger:
         if self.b.halo_timed_out():
             raise RuntimeError("peer-memory halo exchange timed out (a peer never raised its flag)")
 
+    def _dev(self):
+        # the reductions ride on whatever process group carries the setup: NCCL
+        # needs device tensors, gloo takes host ones
+        return "cuda" if self.dist.get_backend() == "nccl" else "cpu"
+
     def all_max(self, vals):
         self._check()
-        t = self.torch.tensor(vals, dtype=self.torch.float64)
+        t = self.torch.tensor(vals, dtype=self.torch.float64, device=self._dev())
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return t.tolist()
 
@@ -229,7 +234,7 @@ class IpcExchanger:
 
     def all_gather(self, vals):
         self._check()
-        t = self.torch.tensor(vals, dtype=self.torch.float64)
+        t = self.torch.tensor(vals, dtype=self.torch.float64, device=self._dev())
         out = [self.torch.empty_like(t) for _ in range(self.dist.get_world_size())]
         self.dist.all_gather(out, t)
         return [o.tolist() for o in out]
