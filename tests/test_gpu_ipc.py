@@ -166,3 +166,25 @@ def test_two_processes_graph_replayed_steps(tmp_path, N, visc):
         for j in range(3):
             got[j][sel] = mine[j]
     assert beq(got, want)
+
+
+def test_flag_wait_times_out_instead_of_hanging():
+    """A peer that never raises its flag: the device-side wait gives up after its
+    timeout, the stream moves on, and halo_status reports it (once)."""
+    import time
+    from paper_1804_02221_b200 import partition as part
+    from paper_1804_02221_b200.distributed import GpuPartition
+    sid, k, N = "oscillating_lake", 8, 3
+    m, st = ref.scenario_mesh(sid, k, k, N)
+    p, _ = scenario_params(sid, N, visc_enabled=0.0)
+    lm = part.local_mesh(m, 2, 0)
+    b = GpuPartition(lm, _cfg(p, 1))
+    base, handle = b.ipc_alloc(4 * 8)
+    assert len(handle) == 64
+    t0 = time.perf_counter()
+    b.wait_flags(base, 2, 1, 0.2)  # nobody will store 1 there
+    assert b.halo_timed_out()
+    assert time.perf_counter() - t0 < 10.0
+    assert not b.halo_timed_out()  # the report is cleared
+    b.wait_flags(base, 2, 0, 0.2)  # already satisfied (flags start at 0)
+    assert not b.halo_timed_out()
