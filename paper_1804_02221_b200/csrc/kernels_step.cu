@@ -114,16 +114,33 @@ __device__ __forceinline__ void block_sum2(double& a, double& b) {
   }
 }
 
+// n / d for n < 2^31 by one 64-bit multiply and a shift (the round-up magic
+// number, p = 31 + ceil(log2 d)): the per-node index arithmetic (element, node, face
+// of an index) without integer divisions; the magic is formed once per thread
+struct FDiv {
+  unsigned long long m;
+  int p;
+  __device__ explicit FDiv(unsigned d) {
+    const int l = d > 1 ? 32 - __clz(d - 1) : 0;
+    p = 31 + l;
+    m = ((1ull << p) + d - 1) / d;
+  }
+  __device__ __forceinline__ unsigned operator()(unsigned n) const {
+    return (unsigned)(((unsigned long long)n * m) >> p);
+  }
+};
+
 struct NodeAcc {
   double mass = 0.0, ent = 0.0;
   unsigned long long kmin = ~0ull, kdt = ~0ull, klen = ~0ull;
 };
 
 template <bool FAST>
-__device__ __forceinline__ void node_terms(const Mesh& M, const Phys& P, double order, int n,
+__device__ __forceinline__ void node_terms(const Mesh& M, const Phys& P, double order, int loc,
                                            double h, double hu, double hv, double jac,
-                                           double b, double lxi, double leta, NodeAcc& acc) {
-  const int loc = n % M.np, i = loc / M.n1, j = loc - i * M.n1;
+                                           double b, double lxi, double leta, NodeAcc& acc,
+                                           const FDiv& div_n1) {
+  const int i = (int)div_n1((unsigned)loc), j = loc - i * M.n1;
   const double wi = M.w[i], wj = M.w[j];
   // one phys::velocity per node serves both the entropy (physics.hpp:47-62) and
   // compute_dt (timeloop.hpp:58-71): the same call in the reference, same bits
@@ -220,17 +237,15 @@ __global__ void k_limiter_entropy(Mesh M, Phys P, StageArgs A, const Flags* F,
 // positivity_dt_bounds (limiter.hpp:107-130) evaluated by every owned
 // element-face node from its own side (the reference evaluates the minus side
 // and, for interior faces, the plus side with the plus normal: the same set).
-__device__ __forceinline__ double posdt_bound(const Mesh& M, const Phys& P, const CState& S,
-                                               long long idx);
-
 template <bool FAST>
 __device__ __forceinline__ double posdt_bound(const Mesh& M, const Phys& P, const CState& S,
-                                               long long idx) {
+                                               long long idx, const FDiv& div_n1) {
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
   const int n1 = M.n1;
-  const int t = (int)(idx % n1);
-  const int face = (int)((idx / n1) % 4);
-  const int e = (int)(idx / (4 * n1));
+  const int q = (int)div_n1((unsigned)idx);  // idx / n1 = 4 e + face
+  const int t = (int)idx - q * n1;
+  const int face = q & 3;
+  const int e = q >> 2;
   const int4 ef = M.ef[e * 4 + face];
   if (!(ef.y & EF_PRESENT)) return inf;
   const long long n = (long long)e * M.np + face_node(n1, face, t);
@@ -280,6 +295,7 @@ __global__ void __launch_bounds__(kSumThreads) k_step_diag(Mesh M, Phys P, CStat
   const double order = 2.0 * M.degree + 1.0;
   NodeAcc acc;
   unsigned long long kpos = ~0ull;
+  const FDiv div_n1((unsigned)n1), div_np((unsigned)np);
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int e0 = tile * T, ne = min(T, M.n_owned - e0);
     const int n0 = e0 * np, nn = ne * np;
@@ -304,9 +320,9 @@ __global__ void __launch_bounds__(kSumThreads) k_step_diag(Mesh M, Phys P, CStat
 #pragma unroll
       for (int k = 0; k < B; ++k) {
         const int r = r0 + k * blockDim.x;
-        if (r < nn)
-          node_terms<FAST>(M, P, order, n0 + r, v[k][0], v[k][1], v[k][2], v[k][3], v[k][4],
-                           v[k][5], v[k][6], acc);
+        if (r < nn)  // n0 is a multiple of np: the node's position is r mod np
+          node_terms<FAST>(M, P, order, r - (int)div_np((unsigned)r) * np, v[k][0], v[k][1],
+                           v[k][2], v[k][3], v[k][4], v[k][5], v[k][6], acc, div_n1);
       }
     }
     const long long f0 = (long long)e0 * 4 * n1;
@@ -317,7 +333,7 @@ __global__ void __launch_bounds__(kSumThreads) k_step_diag(Mesh M, Phys P, CStat
 #pragma unroll
       for (int k = 0; k < BF; ++k) {
         const int r = r0 + k * blockDim.x;
-        bnd[k] = posdt_bound<FAST>(M, P, S, f0 + (r < nf ? r : 0));
+        bnd[k] = posdt_bound<FAST>(M, P, S, f0 + (r < nf ? r : 0), div_n1);
       }
 #pragma unroll
       for (int k = 0; k < BF; ++k) {
