@@ -366,12 +366,29 @@ class GraphStepper:
             nsteps -= 1
             if nsteps >= 2:
                 self._capture()
-        for _ in range(nsteps // 2 if self.g is not None else 0):
+                self.phase = 0  # eager steps since the capture, mod 2
+        if self.g is None:
+            for _ in range(nsteps):
+                self._eager()
+            return
+        # the graph holds the buffers of an even step: after an odd number of
+        # eager steps one more eager step re-aligns the W/A ping-pong with it
+        if self.phase and nsteps > 0:
+            self._eager()
+            self.phase, nsteps = 0, nsteps - 1
+        # eager steps advanced the host sequence count: the device base follows
+        # (an even number of eager steps since the capture, so the receive-slot
+        # parity the graph carries still holds), else the replay's flags would
+        # fall behind values the eager exchanges already stored
+        if nsteps >= 2:
+            self.ex.sync_base()
+        for _ in range(nsteps // 2):
             self.g.replay()
             self.ex.replayed()
             self.replays += 1
-        for _ in range(nsteps % 2 if self.g is not None else nsteps):
+        if nsteps % 2:
             self._eager()
+            self.phase ^= 1
 
     def accepted(self) -> bool:
         """the stage flags of every step since begin(), reduced over the ranks"""

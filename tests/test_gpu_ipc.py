@@ -111,7 +111,15 @@ def _graph_worker(rank, world, port_no, N, visc, steps, path):
     b.upload([1.0 + 0.1 * np.sin(2 * np.pi * x) * np.cos(2 * np.pi * y),
               0.3 * np.ones_like(x), -0.2 * np.ones_like(x)])
     ex = IpcExchanger(b, timeout_s=20.0)
-    ok = run_steps_distributed_graph(b, ex, steps, 0.0, dt)
+    if steps == 5:
+        ok = run_steps_distributed_graph(b, ex, steps, 0.0, dt)
+    else:  # several run() calls with odd counts: the ping-pong must stay aligned
+        from paper_1804_02221_b200.distributed import GraphStepper
+        stp = GraphStepper(b, ex, 0.0, dt)
+        stp.begin()
+        for n in (4, 3, 1, 2):
+            stp.run(n)
+        ok = stp.accepted()
     np_ = (N + 1) ** 2
     n_own = b.lm.n_owned
     mine = np.stack([w[: n_own * np_] for w in b.download()])
@@ -134,8 +142,8 @@ def _graph_case(N, visc):
     return spec, cfg, 5e-5
 
 
-@pytest.mark.parametrize("N,visc", [(4, False), (3, True)])
-def test_two_processes_graph_replayed_steps(tmp_path, N, visc):
+@pytest.mark.parametrize("N,visc,steps", [(4, False, 5), (3, True, 5), (4, False, 10)])
+def test_two_processes_graph_replayed_steps(tmp_path, N, visc, steps):
     """run_steps_distributed_graph: one eager step, two captured steps replayed twice
     (the device-resident sequence base advancing per replay): the same state as the
     single-GPU fixed-dt stepping of the same mesh."""
@@ -145,7 +153,6 @@ def test_two_processes_graph_replayed_steps(tmp_path, N, visc):
         s.bind(("127.0.0.1", 0))
         port_no = s.getsockname()[1]
     path = os.path.join(tmp_path, "res.npy")
-    steps = 5
     mp.spawn(_graph_worker, args=(2, port_no, N, visc, steps, path), nprocs=2, join=True)
     res = np.load(path, allow_pickle=True)
     spec, cfg, dt = _graph_case(N, visc)
