@@ -47,6 +47,9 @@ struct VLP {
   // staging, neutral at 7, 8, profiles/r02_ab_visc_pre_staging.txt; with the
   // metrics staged too it had measured slower at N+1 <= 8); N+1 = 3 stages
   // synchronously with every node's loads issued first (N=2 0.957 -> 0.931)
+#ifndef VL_PREFETCH_AHEAD
+#define VL_PREFETCH_AHEAD 592  // measured (profiles/r02_ab_visc_pre_prefetch.txt): viscous N=7 5.88 -> 5.66, N=12 20.5 -> 19.6 ms/stage
+#endif
 #ifndef VL_SYNC_BATCH
 #define VL_SYNC_BATCH 1
 #endif
@@ -79,6 +82,25 @@ __global__ void __launch_bounds__(VLP<N1>::THREADS)
   const double h_des = Ph.h_des, iw0 = 1.0 / M.w0;
 
   const long long base = (long long)e0 * NP;
+  // L2 prefetch of the state, metrics and J of the CTA that is dispatched about
+  // one CTA lifetime later (blockIdx + VL_PREFETCH_AHEAD): its loads then hit L2
+  if constexpr (VL_PREFETCH_AHEAD > 0) {
+    if (tid == 0 && blockIdx.x + VL_PREFETCH_AHEAD < gridDim.x) {
+      const long long pb = base + (long long)VL_PREFETCH_AHEAD * P::E * NP;
+      const long long lim = (long long)M.n_owned * NP;
+      const long long lo = pb & ~1ll;  // 16-byte aligned start
+      long long hi = pb + (long long)P::E * NP;
+      if (hi > lim) hi = lim;
+      if (hi > lo) {
+        const uint32_t bytes = (uint32_t)(((hi - lo) * 8) & ~15ll);
+        if (bytes) {
+          const double* f[8] = {S.h, S.hu, S.hv, M.ye, M.xe, M.yx, M.xx, M.jac};
+#pragma unroll
+          for (int q = 0; q < 8; ++q) bulk_prefetch_l2(f[q] + lo, bytes);
+        }
+      }
+    }
+  }
   // this thread's nodes of the final (flux-pair) phase: J prefetched now
   constexpr int R = (P::E * NP + P::THREADS - 1) / P::THREADS;
   double jr[R];
