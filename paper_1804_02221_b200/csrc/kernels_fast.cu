@@ -358,6 +358,16 @@ __host__ __device__ constexpr bool hl_roll(int n1, bool visc) {
          : visc ? (n1 >= 8 && n1 <= 10) || n1 >= 14 : (n1 == 6 || n1 == 7 || n1 == 9 || n1 == 10);
 }
 
+// The node-data bulk copies and the next-group claim (an atomic round trip) are
+// issued by one thread per group: the first xi-X lane, or (true) a lane of the
+// last eta-Y warp, which idles during the node phase.  Measured per configuration
+// (ms/stage, profiles/r02_ab_hl_issuer.txt): eta-Y faster at inviscid N+1 = 9
+// (4.05 -> 3.95), 14..16 (1-2%), viscous 8 (5.67 -> 5.53), 14, 16 (2-4%); slower at
+// inviscid N+1 = 5..8 and 11, 12 (2-4%).
+__host__ __device__ constexpr bool hl_eta_issuer(int n1, bool visc) {
+  return visc ? (n1 == 8 || n1 == 14 || n1 == 16) : (n1 == 9 || n1 >= 14);
+}
+
 // resident CTAs the register allocation must allow: 4 (<= 128 registers) for
 // N+1 = 5..7 (measured on B200, 1M elements: N=4 1.352 -> 1.132, N=5 1.635 ->
 // 1.609, N=6 2.438 -> 2.374 ms/stage; at N+1 = 8 the 128-register cap spills 88
@@ -428,7 +438,7 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
     const int e = e0 + el;
     cp_async_wait_all();
     __syncthreads();  // line(g) and connectivity(g) resident for every thread
-    if (tid == 0) {
+    if (tid == (hl_eta_issuer(N1, VISC) ? P::THREADS - 32 : 0)) {
       fence_proxy_async();
       hl_issue_node<N1, VISC>(sm, M, A, grp, bar_node);
       s_next = next_group(A.gctr, grp);  // read by all threads after the next barrier
