@@ -85,6 +85,9 @@
 #define SWDG_HL_PRE_VMIN 16  // measured: viscous N=15 44.4 -> 40.1 ms/stage; N+1 = 13..15 1-4% slower
 #endif
 
+#ifndef SWDG_HL_CLAIM_AHEAD
+#define SWDG_HL_CLAIM_AHEAD 0
+#endif
 #ifndef SWDG_HL_XROLL
 #define SWDG_HL_XROLL 0  // > 0: roll the streamed-node loops from this N+1 on (A/B)
 #endif
@@ -423,6 +426,7 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
   int buf = 0;
 
   __shared__ int s_next;  // the next group, claimed by thread 0
+  int pending = -1;       // SWDG_HL_CLAIM_AHEAD: the issuer's claim one group ahead
   unsigned long long kmin = ~0ull;  // min height key of this thread's elements
   // With HL::XI_SPLIT the group loop is instantiated per line direction (xi is
   // warp-uniform): the metric selection (y_eta, x_eta) / -(y_xi, x_xi), the padded
@@ -441,7 +445,16 @@ __global__ void __launch_bounds__(HL<N1, VISC>::THREADS, hl_min_blocks(N1, VISC)
     if (tid == (hl_eta_issuer(N1, VISC) ? P::THREADS - 32 : 0)) {
       fence_proxy_async();
       hl_issue_node<N1, VISC>(sm, M, A, grp, bar_node);
-      s_next = next_group(A.gctr, grp);  // read by all threads after the next barrier
+      if constexpr (SWDG_HL_CLAIM_AHEAD || (N1 == 8 && !VISC)) {
+        // the atomic's result is used a group later (measured: N=7 2.420 -> 2.406
+        // ms/stage; N=6 2.11 -> 2.31, others within +-1.5%,
+        // profiles/r02_ab_hl_issuer.txt)
+        if (pending < 0) pending = next_group(A.gctr, grp);
+        s_next = pending;
+        if (pending < ngroups) pending = next_group(A.gctr, pending);
+      } else {
+        s_next = next_group(A.gctr, grp);  // read by all threads after the next barrier
+      }
     }
 
     // ---- own half -> registers, gathers for the own endpoint
