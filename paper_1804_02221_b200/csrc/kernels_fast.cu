@@ -365,7 +365,7 @@ __host__ __device__ constexpr bool hl_roll(int n1, bool visc) {
 // issued by one thread per group: the first xi-X lane, or (true) a lane of the
 // last eta-Y warp, which idles during the node phase.  Measured per configuration
 // (ms/stage, profiles/r02_ab_hl_issuer.txt): eta-Y faster at inviscid N+1 = 9
-// (4.05 -> 3.95), 14..16 (1-2%), viscous 8..10 and 13..16 (1-4%: N+1 = 10 11.56 ->
+// (4.05 -> 3.95), 14..16 (1-2%), viscous 8..10 and 13..16 (1-4%: N+1 = 10 10.82 ->
 // 10.40 ms); slower at inviscid N+1 = 5..8 and 11, 12 (2-4%), viscous 5..7, 11, 12.
 __host__ __device__ constexpr bool hl_eta_issuer(int n1, bool visc) {
   return visc ? (n1 >= 8 && n1 != 11 && n1 != 12) : (n1 == 9 || n1 >= 14);
