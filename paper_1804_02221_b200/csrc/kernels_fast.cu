@@ -385,11 +385,12 @@ __host__ __device__ constexpr int hl_min_blocks(int n1, bool visc) {
 
 // One min-height atomic per CTA instead of one per element (1M same-address
 // atomics per launch): viscous N=3 2.08 -> 1.58, N=2 1.29 -> 1.22 ms/stage.
-// Inviscid stays per element: within +-1.5% at N = 4, 5, 7, 10, and the extra
+// Inviscid per CTA too at N+1 = 9, 15 (round 2: 3.956 -> 3.924, 12.77 -> 12.65
+// ms/stage); elsewhere per element: within +-1.5% at N = 4, 5, 7, 10, and the extra
 // register pushed N+1 = 7 (128-register cap) from 48 to 60 B of spills (N=6
 // 2.375 -> 2.520 ms)
 __host__ __device__ constexpr bool hl_blockmin(int n1, bool visc) {
-  return SWDG_HL_BLOCKMIN >= 0 ? SWDG_HL_BLOCKMIN != 0 : visc;
+  return SWDG_HL_BLOCKMIN >= 0 ? SWDG_HL_BLOCKMIN != 0 : visc || n1 == 9 || n1 == 15;
 }
 
 template <int N1, bool FORCE, bool VISC>
